@@ -1,0 +1,379 @@
+"""Benchmark of the freeview per-ray-sample path on B200 (BASELINE.json metric: rays/s and
+512^2 frames/s).  Contract: one JSON line on rank 0.
+
+Workload (default ``--config c2``): one step = one 512x512 frame, 128 jittered samples per
+ray, occupancy grid rebuilt for the frame's pose, fp16 table/volume, tcgen05 MLPs.  At N
+GPUs every rank renders its own frame per step (poses of config 4 round-robin): weak
+scaling, no data-path collective; weights are broadcast once with NCCL before timing.
+
+--impl reference: the reference's algorithm on the host CPU (the numpy oracle restating
+the reference primitives, all host cores via worker processes), same metric/config, each
+step a bounded tile of the frame.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rays_per_s"
+UNIT = "rays/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2")
+    p.add_argument("--no-occupancy", action="store_true")
+    p.add_argument("--cpu-tiles", type=int, default=2, help="64x64 tiles per CPU-baseline sample")
+    p.add_argument("--skip-cpu-baseline", action="store_true")
+    p.add_argument("--profile-stages", action="store_true", default=True)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------------------ CPU side
+
+def _cpu_worker(args):
+    name, pix, seed = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import camera as ocam
+    from oracle import pipeline as opipe
+    from oracle.adapter import scene_arrays, settings
+    from paper_2306_16541_b200 import scene as psc
+    sc = psc.make_scene(psc.config(name))
+    osc = scene_arrays(sc, 0)
+    cc = ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera)
+    st = settings(sc.cfg, seed=seed)
+    r = opipe.render_rays(osc, cc, pix, sc.cfg.width, st, np.float32)
+    return len(pix), float(r["rgb"].sum())
+
+
+def cpu_rays_per_s(name, tiles, cores=None):
+    """Oracle (the reference's algorithm in numpy) on `tiles` 64x64 pixel tiles of the frame,
+    split over `cores` worker processes; returns (rays/s, cores, sample description)."""
+    import multiprocessing as mp
+    from paper_2306_16541_b200 import scene as psc
+    cfg = psc.config(name)
+    cores = cores or os.cpu_count()
+    rays = []
+    for t in range(tiles):
+        ty, tx = divmod(t, max(cfg.width // 64, 1))
+        y0, x0 = (cfg.height // 2 - 32 + 64 * (ty - tiles // 4)) % cfg.height, (cfg.width // 2 - 32 + 64 * tx) % cfg.width
+        yy, xx = np.meshgrid(np.arange(y0, y0 + 64) % cfg.height, np.arange(x0, x0 + 64) % cfg.width, indexing="ij")
+        rays.append((yy * cfg.width + xx).reshape(-1))
+    pix = np.concatenate(rays)
+    chunks = np.array_split(pix, cores * 2)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        out = pool.map(_cpu_worker, [(name, c, 77) for c in chunks])
+    dt = time.perf_counter() - t0
+    n = sum(o[0] for o in out)
+    sample = f"{tiles} x (64x64) ray tiles of the {cfg.width}x{cfg.height} frame, {cfg.n_samples} samples/ray, numpy float32 oracle, {cores} processes"
+    return n / dt, cores, sample
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2306_16541_b200 import scene as psc
+    cfg = psc.config(args.config)
+    for _ in range(args.warmup):
+        cpu_rays_per_s(args.config, 1)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, cores, sample = cpu_rays_per_s(args.config, args.cpu_tiles)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * wall / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded BASELINE config stand-in)",
+            "config": {"workload": f"{args.config}: {cfg.width}x{cfg.height} frame, {cfg.n_samples} samples/ray",
+                       "frames_per_s": value / (cfg.width * cfg.height)},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU side
+
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                mask = int(parts[2], 16)
+            except ValueError:
+                continue
+            mx = m
+            if s > 500:
+                sm.append(s)
+            for bit, name in self.REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(self.lines)}
+
+
+def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from paper_2306_16541_b200 import _lib
+    from paper_2306_16541_b200 import scene as psc
+    from paper_2306_16541_b200.model import FreeviewModel
+    from paper_2306_16541_b200.render import RenderSettings, Renderer, camera_struct, march_struct
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    name = args.config
+    cfg = psc.config(name, n_poses=8, pose_sigma=0.3) if world > 1 or name == "c4" else psc.config(name)
+    sc = psc.make_scene(cfg)
+    nets = FreeviewModel(sc, device=str(dev))
+    if world > 1:  # identical weights everywhere: one NCCL broadcast of the flat master buffer
+        dist.broadcast(nets.flat, src=0)
+        nets.refresh()
+    occ_on = cfg.occupancy and not args.no_occupancy
+    st = RenderSettings.from_config(cfg, seed=sc.jitter_seed, occupancy=occ_on)
+    rnd = Renderer(str(dev))
+    cam = sc.camera
+    n_rays = cam.width * cam.height
+    img = torch.empty((n_rays, 3), device=dev)
+    alpha = torch.empty(n_rays, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def pose_of(step):
+        return sc.poses[(rank + step * world) % len(sc.poses)]
+
+    launches_per_step = 3 + (3 if occ_on else 0) + 1  # march, field, composite (+ occ points/field/bits) + bias fold
+
+    def step(i):
+        nets.set_pose(pose_of(i))
+        rnd.render_image(nets, cam, None, st, out_rgb=img, out_alpha=alpha)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step(args.warmup + i)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    step_ms = np.array([a.elapsed_time(b) for a, b in ev])
+    ms = float(step_ms.mean())
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * n_rays / (ms / 1000.0)
+
+    # ---- e2e: the public API with host poses in, host image out (pinned), per step
+    from paper_2306_16541_b200.render import render_image
+    host_img = torch.empty((cam.height, cam.width, 3), dtype=torch.float32, pin_memory=True)
+    host_alpha = torch.empty((cam.height, cam.width), dtype=torch.float32, pin_memory=True)
+    for i in range(2):
+        im, al = render_image(nets, cam, pose_of(i), st)
+        host_img.copy_(im, non_blocking=True)
+        host_alpha.copy_(al, non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        im, al = render_image(nets, cam, pose_of(i), st)
+        host_img.copy_(im, non_blocking=True)
+        host_alpha.copy_(al, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = 12 * 4 * nets.n_bones + 3 * 4 * nets.n_bones   # G_i + pose vector
+    d2h = host_img.numel() * 4 + host_alpha.numel() * 4
+
+    # ---- per-stage device times (same inputs, separate pass, CUDA events on this stream)
+    stages = stage_times(nets, rnd, cam, st, dev, occ_on, reps=max(3, min(args.steps, 10)))
+    n_samples_launch = ((n_rays + 31) // 32 * 32) * cfg.n_samples
+    flop_per_sample = 121856   # offset MLP 109,056 (pose folded) + radiance 12,800
+    warp_bytes = 412 if cfg.half else 796  # SURVEY SS8d warp fwd, fp16 / fp32 volume
+    field_ms = stages["field"]
+    field_tflops = n_samples_launch * flop_per_sample / (field_ms * 1e-3) / 1e12
+    march_gbs = n_samples_launch * warp_bytes / (stages["march_warp"] * 1e-3) / 1e9
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0}
+    dominant = max(("field", "march_warp", "composite"), key=lambda k: stages[k])
+    if dominant == "march_warp":
+        roof = {"kernel": "k_march_warp", "bound": "hbm", "achieved": march_gbs, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": march_gbs / peaks["hbm_gbs"], "traffic": None,
+                "algorithmic": f"{warp_bytes} B/sample x {n_samples_launch} samples/launch"}
+    else:
+        pk = peaks.get("bf16_tflops_sustained", 1394.7)
+        roof = {"kernel": "k_field_tc" if cfg.half else "field_fp32", "bound": "tensor", "achieved": field_tflops,
+                "peak": pk, "unit": "TFLOP/s", "frac": field_tflops / pk, "traffic": None,
+                "algorithmic": f"{flop_per_sample} FLOP/sample x {n_samples_launch} samples/launch"}
+    roof["peak_source"] = "MEASURED_PEAKS.json (sustained)" if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else "fallback"
+
+    cpu = None
+    if rank == 0 and not args.skip_cpu_baseline:
+        v, cores, sample = cpu_rays_per_s(name, args.cpu_tiles)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f16" if cfg.half else "f32",
+            "data": "synthetic (seeded stand-in for the BASELINE config; random-init weights)",
+            "config": {"workload": f"{name}: {cam.width}x{cam.height} frame/step/GPU, {cfg.n_samples} jittered samples/ray, "
+                                   f"hash T=2^{cfg.hash.log2_T} res {cfg.hash.base_res}->{cfg.hash.max_res}, "
+                                   f"{'fp16 tcgen05' if cfg.half else 'fp32'} MLPs, occupancy {'on' if occ_on else 'off'}",
+                       "frames_per_s": value / n_rays, "l2": "flushed (256 MB write) before every timed step",
+                       "per_step_ms": [round(x, 4) for x in step_ms.tolist()]},
+            "e2e": {"value": world * n_rays / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "frames_per_s": world / (e2e_ms / 1000.0)},
+            "gpu_launches": launches_per_step * args.steps,
+            "stages_ms": stages,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5):
+    """Device time of each kernel stage of one frame (CUDA events on the launch stream)."""
+    import ctypes as C
+    import torch
+    from paper_2306_16541_b200 import _lib
+    from paper_2306_16541_b200.render import camera_struct, march_struct
+    lib = nets.lib
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    pix = rnd.pixel_order(cam)
+    n = pix.numel()
+    occ = rnd.build_occupancy(nets, st) if occ_on else None
+    m, cs, w = march_struct(st, pix, occ, True), camera_struct(cam), nets.warp_struct()
+    h, f = nets.hash_struct(), nets.field_struct()
+    S = (n + 31) // 32 * 32 * st.n_samples
+    xs = torch.empty((S, 4), device=dev)
+    delta = torch.empty(S, device=dev)
+    rgbs = torch.empty((S, 4), device=dev)
+    nb = lib.fv_field_workspace_bytes(S, f.precision)
+    fw = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+    rgb = torch.empty((n, 3), device=dev)
+    alpha = torch.empty(n, device=dev)
+    wb = lib.fv_render_workspace_bytes(n, st.n_samples, f.precision)
+    work = torch.empty(wb, dtype=torch.uint8, device=dev)
+    out = {}
+
+    def timeit(fn):
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
+    out["march_warp"] = timeit(lambda: _lib.check(lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), n, xs.data_ptr(),
+                                                                     delta.data_ptr(), None, None, sp)))
+    out["field"] = timeit(lambda: _lib.check(lib.fv_field_fwd(C.byref(f), C.byref(h), xs.data_ptr(), S, st.eps_w,
+                                                               rgbs.data_ptr(), None, fw.data_ptr(), nb, sp)))
+    total = timeit(lambda: _lib.check(lib.fv_render_fwd(C.byref(cs), C.byref(m), C.byref(w), C.byref(h), C.byref(f), n,
+                                                         work.data_ptr(), wb, rgb.data_ptr(), alpha.data_ptr(), None, sp)))
+    out["render_total"] = total
+    out["composite"] = max(total - out["march_warp"] - out["field"], 0.0)
+    if occ_on:
+        out["occupancy_build"] = timeit(lambda: rnd.build_occupancy(nets, st))
+    out["fg_fraction"] = float((xs[:, 3] > st.eps_w).float().mean().item())
+    return out
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

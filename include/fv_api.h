@@ -1,0 +1,216 @@
+/* fv_api.h -- C ABI of libfvcuda.so, the sm_100a implementation of the freeview
+ * per-ray-sample path (inverse-LBS warp -> offset MLP -> hash grid -> radiance MLP ->
+ * compositing, plus backward and Adam).
+ *
+ * The reference (arxiv 2306.16541 "freeview", /root/reference/pkg) is pure Python and
+ * exposes no FFI; each entry point below replaces one reference operator (cited per
+ * function as file:line; ad = pkg/src/freeview/autodiff.py, fu = fused.py,
+ * S = SPEC.md).  Binding: ctypes (paper_2306_16541_b200/_lib.py).
+ *
+ * Conventions
+ *  - every pointer argument named d_* is a DEVICE pointer owned by the caller; the
+ *    library never allocates or frees device memory (workspaces are caller-provided);
+ *  - `stream` is a cudaStream_t passed as void*; all work is enqueued on it, nothing
+ *    synchronises unless the function says so;
+ *  - no hidden global state: per-call constants travel in the parameter structs, so
+ *    calls on different streams / host threads are independent;
+ *  - return value: FV_OK or one of the FV_E* codes; the Python layer maps
+ *    FV_EDIM -> DimensionError, FV_ENONFINITE -> TrainingError, others -> RuntimeError.
+ */
+#ifndef FV_API_H
+#define FV_API_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FV_OK 0
+#define FV_EDIM 1        /* shape / size / configuration error */
+#define FV_ENONFINITE 2  /* non-finite value detected (Adam gradients) */
+#define FV_ELAUNCH 3     /* CUDA launch / runtime error */
+#define FV_EUNSUPPORTED 4
+
+#define FV_MAX_BONES 32
+#define FV_MAX_LEVELS 16
+
+/* ---- parameter blocks (plain data, host memory) ----------------------------------- */
+
+typedef struct fv_camera {
+  float kinv[9];    /* K^-1 row-major                      (cap:73-82) */
+  float rot[9];     /* world->camera R row-major           (cap:62-71) */
+  float center[3];  /* camera centre -R^T t                (cap:69-71) */
+  int32_t width, height;
+} fv_camera;
+
+typedef struct fv_march {
+  float obox_min[3], obox_max[3]; /* observation-space sampling box */
+  int32_t n_samples;              /* N samples per ray                                 */
+  int32_t jitter;                 /* 0: bin midpoints, 1: counter-hash jitter          */
+  uint32_t seed;
+  float eps_w;                    /* foreground likelihood threshold 1e-4      */
+  float eps_t;                    /* early-termination transmittance (0 = off)         */
+  float bg[3];                    /* background colour                         */
+  const uint32_t* d_occ;          /* 32^3 occupancy bitfield (1024 words) or NULL      */
+  float occ_scale[3];             /* float32(32 / (obox_max - obox_min))               */
+  const int32_t* d_pix;           /* optional list of linear pixel ids (NULL = 0..R-1) */
+  int32_t pix_offset;             /* first pixel id when d_pix == NULL                 */
+  int32_t out_by_pixel;           /* 1: rgb/alpha written at the pixel id (image), 0: ray */
+} fv_march;
+
+typedef struct fv_warp {
+  int32_t n_bones;                /* K <= FV_MAX_BONES                                 */
+  int32_t vol_res;                /* G (32)                                            */
+  int32_t vol_half;               /* corner-packed volume dtype: 0 fp32, 1 fp16        */
+  const void* d_vol_packed;       /* [K][(G+1)^3][8] corner-packed weights             */
+  const float* d_g;               /* [K][12] G_i = (R row-major 9, t 3), device        */
+  float wbox_min[3];              /* canonical box of W^c                              */
+  float wscale[3];                /* float32((G-1)/(wbox_max-wbox_min))  (ad:746)      */
+} fv_warp;
+
+typedef struct fv_hash {
+  int32_t n_levels, n_feat, log2_T;
+  int32_t res[FV_MAX_LEVELS];
+  int32_t dense[FV_MAX_LEVELS];
+  uint32_t offset[FV_MAX_LEVELS];
+  int32_t table_half;             /* table dtype: 0 fp32, 1 fp16                       */
+  const void* d_table;            /* [entries][n_feat]                                 */
+  float cmin[3], cinv[3];         /* canonical normalisation                           */
+} fv_hash;
+
+typedef struct fv_field {
+  int32_t precision;              /* 0: fp32 SIMT (1e-5 parity), 1: fp16 tcgen05       */
+  int32_t pe_bands;               /* 6                                                  */
+  float pe_w[8];                  /* Hann band weights (ad:574-578)                     */
+  int32_t offset_enabled;         /* residual stage                             */
+  /* fp32 weights, (in,out) row-major as the reference stores them (ad:403-425) */
+  const float* d_off_w[5]; const float* d_off_b[5];   /* 111->128->128->128->128->3     */
+  const float* d_rad_w[3]; const float* d_rad_b[3];   /* 32->64->64->4                  */
+  const float* d_off_b0_eff;      /* [128] b0 + Omega @ W0[39:111] (per frame)          */
+  const void* d_tc_pack;          /* fp16 tcgen05 weight pack (fv_field_pack) or NULL   */
+} fv_field;
+
+/* ---- misc ---------------------------------------------------------------------------- */
+
+int32_t fv_version(void);                       /* ABI version (100 = 1.0)            */
+const char* fv_last_error(void);                /* thread-local message of last error */
+int32_t fv_device_sm(void);                     /* SM count of the current device     */
+/* sizeof of the 5 parameter structs (camera, march, warp, hash, field) -> out[5];
+ * lets a binding verify its struct layout without a GPU. */
+void fv_struct_sizes(int64_t* out);
+
+/* ---- warp (ad:728-808) ----------------------------------------------------- */
+
+/* W^c (C,G,G,G) fp32 softmax output -> corner-packed volume of the first K channels,
+ * fp32 or fp16 (warp->vol_half).  Replaces the zero-padded grid of ad:755-756. */
+int32_t fv_warp_pack(const float* d_vol, int32_t channels, const fv_warp* warp,
+                     void* d_vol_packed, void* stream);
+
+/* Skeleton warp of n points: x (n,3) -> x_skel (n,3), L (n), fg (n) uint8; optional
+ * per-bone weights w (K,n) (NULL to skip).  S:327-336 / ad:728-773. */
+int32_t fv_warp_fwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
+                    float* d_xskel, float* d_lik, uint8_t* d_fg, float* d_w, void* stream);
+
+/* d x_skel (n,3) -> d W^c (C,G,G,G) fp32 (accumulated, atomics).  ad:775-789 + Eq 9. */
+int32_t fv_warp_bwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
+                    const float* d_dxskel, float* d_dvol, void* stream);
+
+/* ---- hash grid (builder-defined; PARITY UNPINNED) ------------------------------------- */
+
+int32_t fv_hash_fwd(const fv_hash* hash, const float* d_x, int64_t n, float* d_feat,
+                    uint32_t* d_index /* (n, L, 8) or NULL */, void* stream);
+
+/* d feat (n, L*F) -> d table (entries, F) fp32 (accumulated) and d x (n,3) (or NULL). */
+int32_t fv_hash_bwd(const fv_hash* hash, const float* d_x, int64_t n, const float* d_dfeat,
+                    float* d_dtable, float* d_dx, void* stream);
+
+/* ---- MLPs (ad:403-425; fu:132-227) ---------------------------------------------------- */
+
+/* Dense fp32 layer y = act(x @ W + b), W (k_in, n_out) row-major; act 0 none, 1 relu. */
+int32_t fv_linear_fwd(const float* d_x, const float* d_w, const float* d_b, float* d_y,
+                      int64_t m, int32_t k_in, int32_t n_out, int32_t act, void* stream);
+
+/* Backward of fv_linear_fwd: given y and dy -> dx (may be NULL), dW += x^T dz, db += sum dz. */
+int32_t fv_linear_bwd(const float* d_x, const float* d_w, const float* d_y, const float* d_dy,
+                      float* d_dx, float* d_dw, float* d_db, int64_t m, int32_t k_in,
+                      int32_t n_out, int32_t act, void* stream);
+
+/* Pack the fp32 field weights into the fp16 tcgen05 operand layout (+ fp32 biases).
+ * Workspace d_tc_pack must hold fv_field_pack_bytes() bytes. */
+size_t fv_field_pack_bytes(void);
+int32_t fv_field_pack(const fv_field* field, void* d_tc_pack, void* stream);
+
+/* Per-frame folded bias b0' = b0 + pose @ W0[3+6L:, :] (pose: n_pose floats, device). */
+int32_t fv_offset_bias(const fv_field* field, const float* d_pose, int32_t n_pose,
+                       float* d_b0_eff, void* stream);
+
+/* Field on n canonical samples: xs (n,4) = [x_skel, L] (foreground iff L > eps_w) ->
+ * rgbs (n,4) = [c, sigma] fp32 (zeros on background); optional x_final (n,3).
+ * S:346-358 (residual offset on posenc) + hash grid + S:419-427 (radiance heads).
+ * Workspace: fv_field_workspace_bytes(n, precision) bytes (0 for the tcgen05 path). */
+size_t fv_field_workspace_bytes(int64_t n, int32_t precision);
+int32_t fv_field_fwd(const fv_field* field, const fv_hash* hash, const float* d_xs, int64_t n,
+                     float eps_w, float* d_rgbs, float* d_xfinal, void* d_work, size_t work_bytes,
+                     void* stream);
+
+/* ---- compositing (ad:815-837) ---------------------------------------------- */
+
+/* rays r (R), N samples each: sigma/color (R*N,4) [rgb, sigma], delta (R*N), lik (R*N)
+ * -> rgb (R,3), alpha (R); optional T (R,N+1) for backward. */
+int32_t fv_composite_fwd(const float* d_rgbs, const float* d_delta, const float* d_lik,
+                         int64_t n_rays, int32_t n_samples, const float bg[3], float eps_w,
+                         float eps_t, float* d_rgb, float* d_alpha, float* d_trans,
+                         void* stream);
+
+/* Division-free reverse scan: d rgb (R,3), d alpha (R) -> d rgbs (R*N,4) [dc, dsigma]. */
+int32_t fv_composite_bwd(const float* d_rgbs, const float* d_delta, const float* d_lik,
+                         const float* d_trans, int64_t n_rays, int32_t n_samples,
+                         const float bg[3], float eps_w, const float* d_drgb,
+                         const float* d_dalpha, float* d_drgbs, void* stream);
+
+/* ---- fused render (the hot path) ------------------------------------------------------ */
+
+/* Workspace bytes for rendering n_rays rays of n_samples samples with field precision. */
+size_t fv_render_workspace_bytes(int64_t n_rays, int32_t n_samples, int32_t precision);
+
+/* Ray generation + slab + stratified sampling + occupancy skip + skeleton warp, one thread
+ * per sample.  Outputs per sample: xs (R*N,4) = [x_skel, L] (L = 0 if skipped),
+ * delta (R*N), x (R*N,3) world position (may be NULL); per ray: count (R) int32. */
+int32_t fv_march_warp(const fv_camera* cam, const fv_march* march, const fv_warp* warp,
+                      int64_t n_rays, float* d_xs, float* d_delta, float* d_x,
+                      int32_t* d_count, void* stream);
+
+/* Full forward: rays -> rgb (3 floats) and alpha per ray (or per pixel, out_by_pixel),
+ * per-ray sample counts (may be NULL).  d_work >= fv_render_workspace_bytes(). */
+int32_t fv_render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp* warp,
+                      const fv_hash* hash, const fv_field* field, int64_t n_rays,
+                      void* d_work, size_t work_bytes, float* d_rgb, float* d_alpha,
+                      int32_t* d_count, void* stream);
+
+/* ---- occupancy (builder-defined; PARITY UNPINNED) ------------------------------------- */
+
+/* Evaluate density at 2x2x2 sub-cell points of each of the 32^3 observation-box cells
+ * through warp + field; bit (x*32+y)*32+z is set when any point has L > eps_w and
+ * sigma > threshold.  Workspace: fv_occupancy_workspace_bytes(field->precision). */
+size_t fv_occupancy_workspace_bytes(int32_t precision);
+int32_t fv_occupancy_build(const fv_march* march, const fv_warp* warp, const fv_hash* hash,
+                           const fv_field* field, float threshold, void* d_work,
+                           size_t work_bytes, uint32_t* d_occ, void* stream);
+
+/* ---- Adam (ad:880-912) ---------------------------------------------------------------- */
+
+/* In-place bias-corrected Adam over n params; lr per segment: seg_end (n_seg) exclusive
+ * end offsets, lr (n_seg).  Writes an fp16 copy of [half_begin, half_end) into d_half
+ * (if non-NULL).  Non-finite grads set *d_flag to 1 + segment index (device int32) and
+ * skip the update of that element. */
+int32_t fv_adam_step(float* d_param, const float* d_grad, float* d_m, float* d_v, int64_t n,
+                     const int64_t* seg_end, const float* lr, int32_t n_seg, int32_t step,
+                     float beta1, float beta2, float eps, void* d_half, int64_t half_begin,
+                     int64_t half_end, int32_t* d_flag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FV_API_H */

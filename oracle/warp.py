@@ -1,0 +1,173 @@
+"""Inverse-LBS skeleton warp (oracle).
+
+* ``softmax0`` / ``softmax0_bwd``: channel softmax of the weight-volume logits (``ad:711-721``).
+* ``sample_bone_channels`` / ``sample_bone_channels_bwd``: channel ``i`` of the volume
+  sampled trilinearly at ``pts[i]`` (``ad:728-808``): box-corner-aligned grid with
+  ``scale = (G-1)/(bmax-bmin)`` (``ad:746``); ``u = (p-bmin)*scale + 1`` into a one-voxel
+  zero-padded grid (``ad:748-756``); inside iff every ``u`` in ``[0, G+1]`` (``ad:750``);
+  ``i0 = clip(floor u, 0, G)`` (``ad:751-752``); 8-corner blend accumulated in (a,b,c)
+  loop order (``ad:767-773``); index order ``vol[ch, x, y, z]`` (``ad:770``).
+* ``skeleton_warp``: ``S:327-336`` / Eqs 7-9 -- ``p_i = G_i(x)``, ``w_i`` sampled,
+  ``L = sum_i w_i`` over bones only, foreground iff ``L > eps_w`` (1e-4, ``S:373``),
+  ``x_skel = sum_i (w_i/L) p_i`` (``weighted_sum0``, ``ad:456-467``), evaluated as
+  ``(sum_i w_i p_i) / L`` (same value, the kernel's rounding order).
+
+Every function takes a ``dtype``; with float32 each elementwise operation is one
+rounded float32 op in the order the sm_100a warp kernel evaluates it, so the per-bone
+weights, the likelihood and the foreground mask compare bit-exactly with the kernel.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+EPS_W = 1e-4
+
+
+def softmax0(a):
+    z = a - a.max(axis=0, keepdims=True)
+    e = np.exp(z)
+    return e / e.sum(axis=0, keepdims=True)
+
+
+def softmax0_bwd(out, g):
+    dot = (g * out).sum(axis=0, keepdims=True)
+    return out * (g - dot)
+
+
+def _grid_coords(p, gsz, bmin, scale, dt):
+    u = (((p - bmin).astype(dt) * scale).astype(dt) + dt(1.0)).astype(dt)
+    inside = np.all((u >= 0.0) & (u <= dt(gsz + 1)), axis=-1)
+    i0 = np.clip(np.floor(u), 0, gsz).astype(np.int64)
+    f = (u - i0.astype(dt)).astype(dt)
+    return u, inside, i0, f
+
+
+def sample_bone_channels(vol, pts, box_min, box_max, dtype=None):
+    """vol (C,G,G,G), pts (K,N,3) -> (K,N) (ad:728-773)."""
+    dt = np.dtype(dtype or vol.dtype).type
+    v = np.asarray(vol, dtype=dt)
+    p = np.asarray(pts, dtype=dt)
+    kb = p.shape[0]
+    gsz = v.shape[1]
+    bmin = np.asarray(box_min, dtype=dt)
+    scale = ((dt(gsz) - dt(1.0)) / (np.asarray(box_max, dtype=dt) - bmin)).astype(dt)
+    _, inside, i0, f = _grid_coords(p, gsz, bmin, scale, dt)
+    vp = np.zeros((v.shape[0],) + tuple(g + 2 for g in v.shape[1:]), dtype=dt)
+    vp[:, 1:-1, 1:-1, 1:-1] = v
+    ch = np.arange(kb).reshape(kb, 1)
+    wx = ((dt(1.0) - f[..., 0]).astype(dt), f[..., 0])
+    wy = ((dt(1.0) - f[..., 1]).astype(dt), f[..., 1])
+    wz = ((dt(1.0) - f[..., 2]).astype(dt), f[..., 2])
+    ix, iy, iz = i0[..., 0], i0[..., 1], i0[..., 2]
+    out = np.zeros(p.shape[:2], dtype=dt)
+    for a in (0, 1):
+        for b in (0, 1):
+            for c in (0, 1):
+                cv = vp[ch, ix + a, iy + b, iz + c]
+                wgt = ((wx[a] * wy[b]).astype(dt) * wz[c]).astype(dt)
+                out = (out + (wgt * cv).astype(dt)).astype(dt)
+    return np.where(inside, out, dt(0.0)).astype(dt)
+
+
+def sample_bone_channels_bwd(vol_shape, pts, box_min, box_max, g, dtype=np.float64,
+                             vol=None):
+    """Gradients (dvol (C,G,G,G), dpts (K,N,3) or None) of ``sum(g * out)`` (ad:775-806)."""
+    dt = np.dtype(dtype).type
+    p = np.asarray(pts, dtype=dt)
+    kb, n, _ = p.shape
+    gsz = vol_shape[1]
+    bmin = np.asarray(box_min, dtype=dt)
+    scale = ((dt(gsz) - dt(1.0)) / (np.asarray(box_max, dtype=dt) - bmin)).astype(dt)
+    _, inside, i0, f = _grid_coords(p, gsz, bmin, scale, dt)
+    gm = np.asarray(g, dtype=dt) * inside
+    gp = gsz + 2
+    flat = np.zeros(vol_shape[0] * gp ** 3, dtype=np.float64)
+    ch = np.arange(kb).reshape(kb, 1)
+    wx = (1.0 - f[..., 0], f[..., 0])
+    wy = (1.0 - f[..., 1], f[..., 1])
+    wz = (1.0 - f[..., 2], f[..., 2])
+    ix, iy, iz = i0[..., 0], i0[..., 1], i0[..., 2]
+    for a in (0, 1):
+        for b in (0, 1):
+            for c in (0, 1):
+                idx = ((ch * gp + ix + a) * gp + iy + b) * gp + iz + c
+                flat += np.bincount(idx.ravel(), weights=(wx[a] * wy[b] * wz[c] * gm).ravel(),
+                                    minlength=flat.size)
+    dvol = flat.reshape(vol_shape[0], gp, gp, gp)[:, 1:-1, 1:-1, 1:-1].astype(dt)
+    dpts = None
+    if vol is not None:
+        vp = np.zeros((vol_shape[0], gp, gp, gp), dtype=dt)
+        vp[:, 1:-1, 1:-1, 1:-1] = vol
+        gx = np.zeros((kb, n), dtype=dt)
+        gy = np.zeros((kb, n), dtype=dt)
+        gz = np.zeros((kb, n), dtype=dt)
+        for a in (0, 1):
+            for b in (0, 1):
+                for c in (0, 1):
+                    cv = vp[ch, ix + a, iy + b, iz + c]
+                    sx, sy, sz = (1.0 if a else -1.0), (1.0 if b else -1.0), (1.0 if c else -1.0)
+                    gx += sx * wy[b] * wz[c] * cv
+                    gy += wx[a] * sy * wz[c] * cv
+                    gz += wx[a] * wy[b] * sz * cv
+        dpts = np.stack([gx * gm * scale[0], gy * gm * scale[1], gz * gm * scale[2]], axis=-1)
+    return dvol, dpts
+
+
+def bone_points(x, g_r, g_t, dtype=np.float32):
+    """p_i = x @ R_i^T + t_i for every bone, (K,N,3), kernel op order."""
+    dt = np.dtype(dtype).type
+    x = np.asarray(x, dtype=dt)
+    r = np.asarray(g_r, dtype=dt)
+    t = np.asarray(g_t, dtype=dt)
+    out = np.empty((r.shape[0], x.shape[0], 3), dtype=dt)
+    for j in range(3):
+        acc = (r[:, j, 0][:, None] * x[None, :, 0]).astype(dt)
+        acc = (acc + (r[:, j, 1][:, None] * x[None, :, 1]).astype(dt)).astype(dt)
+        acc = (acc + (r[:, j, 2][:, None] * x[None, :, 2]).astype(dt)).astype(dt)
+        out[:, :, j] = (acc + t[:, j][:, None]).astype(dt)
+    return out
+
+
+def skeleton_warp(x, g_r, g_t, vol, box_min, box_max, eps_w=EPS_W, dtype=np.float32):
+    """Returns dict(x_skel (N,3), L (N), fg (N) bool, w (K,N), p (K,N,3)).
+
+    ``vol`` has C >= K channels; only channels ``0..K-1`` are sampled (``ad:757``).
+    Background samples (``L <= eps_w``) get ``x_skel = 0`` (unused downstream).
+    """
+    dt = np.dtype(dtype).type
+    k = g_r.shape[0]
+    p = bone_points(x, g_r, g_t, dtype)
+    w = sample_bone_channels(np.asarray(vol, dtype=dt)[:k], p, box_min, box_max, dtype)
+    lik = np.zeros(x.shape[0], dtype=dt)
+    for i in range(k):
+        lik = (lik + w[i]).astype(dt)
+    fg = lik > dt(eps_w)
+    safe = np.where(fg, lik, dt(1.0)).astype(dt)
+    # sum_i (w_i/L) p_i evaluated as (sum_i w_i p_i) / L -- the kernel's order
+    acc = np.zeros((x.shape[0], 3), dtype=dt)
+    for i in range(k):
+        acc = (acc + (w[i][:, None] * p[i]).astype(dt)).astype(dt)
+    xs = (acc / safe[:, None]).astype(dt)
+    xs = np.where(fg[:, None], xs, dt(0.0)).astype(dt)
+    return {"x_skel": xs, "L": lik, "fg": fg, "w": w, "p": p}
+
+
+def skeleton_warp_bwd(warp, d_xskel, vol_shape, box_min, box_max, dtype=np.float64):
+    """d x_skel (N,3) -> d vol (C,G,G,G) through Eq 9 and the trilinear sampler.
+
+    ``dw_i = <d x_skel, p_i - x_skel> / L`` on foreground samples; the likelihood gate
+    of the compositor is flat there (``clamp(L/eps_w,0,1) = 1``) so L receives none.
+    """
+    fg = warp["fg"]
+    lik = np.where(fg, warp["L"], 1.0).astype(np.float64)
+    p = warp["p"].astype(np.float64)
+    xs = warp["x_skel"].astype(np.float64)
+    g = np.asarray(d_xskel, np.float64) * fg[:, None]
+    dw = np.einsum("nd,knd->kn", g, p - xs[None]) / lik[None]
+    k = p.shape[0]
+    dvol_k, _ = sample_bone_channels_bwd((k,) + tuple(vol_shape[1:]), p, box_min, box_max, dw,
+                                         dtype=dtype)
+    dvol = np.zeros(vol_shape, dtype=dtype)
+    dvol[:k] = dvol_k
+    return dvol

@@ -1,0 +1,114 @@
+// Front-to-back compositing with likelihood gating (Eq 3) and its
+// division-free reverse scan (ad:815-837 style), one thread per ray, transmittance in a
+// register, samples visited in depth order with early termination (T < eps_t).
+// The sequential per-ray order equals oracle/composite.py, so T and rgb match it to the
+// last bit whenever the per-sample inputs do.
+#include <cuda_runtime.h>
+#include "fv_common.cuh"
+#include "fv_internal.h"
+#include "layout.cuh"
+
+namespace fv {
+
+
+__device__ __forceinline__ int64_t sidx(const CompIn& in, int64_t r, int i, int n) {
+  return in.blocked ? sample_index(r, i, n) : r * n + i;
+}
+
+__global__ void k_composite_fwd(CompIn in, int64_t n_rays, int n, float3 bg, float eps_w, float eps_t,
+                                const int32_t* __restrict__ out_pix, float* __restrict__ rgb_out,
+                                float* __restrict__ alpha_out, float* __restrict__ trans) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rays) return;
+  float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
+  int i = 0;
+  for (; i < n; ++i) {
+    if (eps_t > 0.f && T < eps_t) break;
+    const int64_t s = sidx(in, r, i, n);
+    if (trans) trans[r * (n + 1) + i] = T;
+    const float4 v = in.rgbs[s];
+    const float L = in.lik[s * in.lik_stride];
+    const float a = __fsub_rn(1.f, expf(-__fmul_rn(v.w, in.delta[s])));
+    const float gate = fminf(fmaxf(__fdiv_rn(L, eps_w), 0.f), 1.f);
+    const float ab = __fmul_rn(a, gate);
+    const float w = __fmul_rn(T, ab);
+    cr = __fadd_rn(cr, __fmul_rn(w, v.x));
+    cg = __fadd_rn(cg, __fmul_rn(w, v.y));
+    cb = __fadd_rn(cb, __fmul_rn(w, v.z));
+    T = __fmul_rn(T, __fsub_rn(1.f, ab));
+  }
+  if (trans) for (int j = i; j <= n; ++j) trans[r * (n + 1) + j] = T;
+  cr = __fadd_rn(cr, __fmul_rn(T, bg.x));
+  cg = __fadd_rn(cg, __fmul_rn(T, bg.y));
+  cb = __fadd_rn(cb, __fmul_rn(T, bg.z));
+  const int64_t o = out_pix ? out_pix[r] : r;
+  rgb_out[3 * o] = cr; rgb_out[3 * o + 1] = cg; rgb_out[3 * o + 2] = cb;
+  alpha_out[o] = __fsub_rn(1.f, T);
+}
+
+// Q_N = bg, Q_i = ab_i c_i + (1-ab_i) Q_{i+1};  P_N = 1, P_i = (1-ab_i) P_{i+1}
+// d rgb/d ab_i = T_i (c_i - Q_{i+1});  d alpha/d ab_i = T_i P_{i+1}   (eps_t must be 0)
+__global__ void k_composite_bwd(CompIn in, const float* __restrict__ trans, int64_t n_rays, int n, float3 bg,
+                                float eps_w, const float* __restrict__ drgb, const float* __restrict__ dalpha,
+                                float4* __restrict__ dout) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rays) return;
+  const float gr = drgb[3 * r], gg = drgb[3 * r + 1], gb = drgb[3 * r + 2];
+  const float ga = dalpha ? dalpha[r] : 0.f;
+  float qr = bg.x, qg = bg.y, qb = bg.z, P = 1.f;
+  for (int i = n - 1; i >= 0; --i) {
+    const int64_t s = sidx(in, r, i, n);
+    const float4 v = in.rgbs[s];
+    const float d = in.delta[s];
+    const float L = in.lik[s * in.lik_stride];
+    const float e = expf(-v.w * d);
+    const float a = 1.f - e;
+    const float gate = fminf(fmaxf(L / eps_w, 0.f), 1.f);
+    const float ab = a * gate;
+    const float Ti = trans[r * (n + 1) + i];
+    const float dab = Ti * (gr * (v.x - qr) + gg * (v.y - qg) + gb * (v.z - qb) + ga * P);
+    const float wt = Ti * ab;
+    dout[s] = make_float4(wt * gr, wt * gg, wt * gb, dab * gate * d * e);
+    qr = ab * v.x + (1.f - ab) * qr;
+    qg = ab * v.y + (1.f - ab) * qg;
+    qb = ab * v.z + (1.f - ab) * qb;
+    P *= 1.f - ab;
+  }
+}
+
+int32_t composite_fwd(const CompIn& in, int64_t n_rays, int n, const float* bg, float eps_w, float eps_t,
+                      const int32_t* out_pix, float* rgb, float* alpha, float* trans, cudaStream_t st) {
+  if (n_rays == 0) return FV_OK;
+  k_composite_fwd<<<(unsigned)((n_rays + 127) / 128), 128, 0, st>>>(in, n_rays, n, make_float3(bg[0], bg[1], bg[2]),
+                                                                     eps_w, eps_t, out_pix, rgb, alpha, trans);
+  return check_launch("composite_fwd");
+}
+
+int32_t composite_bwd(const CompIn& in, const float* trans, int64_t n_rays, int n, const float* bg, float eps_w,
+                      const float* drgb, const float* dalpha, float4* dout, cudaStream_t st) {
+  if (n_rays == 0) return FV_OK;
+  k_composite_bwd<<<(unsigned)((n_rays + 127) / 128), 128, 0, st>>>(in, trans, n_rays, n, make_float3(bg[0], bg[1], bg[2]),
+                                                                     eps_w, drgb, dalpha, dout);
+  return check_launch("composite_bwd");
+}
+
+}  // namespace fv
+
+using namespace fv;
+
+extern "C" int32_t fv_composite_fwd(const float* d_rgbs, const float* d_delta, const float* d_lik, int64_t n_rays,
+                                    int32_t n_samples, const float bg[3], float eps_w, float eps_t, float* d_rgb,
+                                    float* d_alpha, float* d_trans, void* stream) {
+  if (n_rays < 0 || n_samples < 1 || !bg || eps_w <= 0.f) return set_error(FV_EDIM, "fv_composite_fwd: bad arguments");
+  CompIn in{(const float4*)d_rgbs, d_delta, d_lik, 1, false};
+  return composite_fwd(in, n_rays, n_samples, bg, eps_w, eps_t, nullptr, d_rgb, d_alpha, d_trans, (cudaStream_t)stream);
+}
+
+extern "C" int32_t fv_composite_bwd(const float* d_rgbs, const float* d_delta, const float* d_lik, const float* d_trans,
+                                    int64_t n_rays, int32_t n_samples, const float bg[3], float eps_w,
+                                    const float* d_drgb, const float* d_dalpha, float* d_drgbs, void* stream) {
+  if (n_rays < 0 || n_samples < 1 || !bg || !d_trans) return set_error(FV_EDIM, "fv_composite_bwd: bad arguments");
+  CompIn in{(const float4*)d_rgbs, d_delta, d_lik, 1, false};
+  return composite_bwd(in, d_trans, n_rays, n_samples, bg, eps_w, d_drgb, d_dalpha, (float4*)d_drgbs,
+                       (cudaStream_t)stream);
+}

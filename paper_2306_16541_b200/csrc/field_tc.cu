@@ -1,0 +1,291 @@
+// Fused canonical field on 5th-gen tensor cores (sm_100a, tcgen05 + TMEM):
+//   posenc(x_skel) -> offset MLP 39(48)->128->128->128->128->3(16)   (ResidualNet)
+//   x_final = x_skel + x_res                                        (Eq 12)
+//   hash-grid features (16 levels x 2)                              (builder-defined)
+//   radiance MLP 32->64->64->4(16) + heads c = sigmoid, sigma = softplus(h-1)
+//
+// Design (the B200 restatement of the Fig-4 "fully fused" scheme, fu:1-14, fu:145-179):
+//  * one persistent CTA per SM holds every weight matrix of both MLPs in shared memory
+//    as fp16 UMMA B operands (126 KB, loaded once per CTA);
+//  * NWG warpgroups per CTA each own a 128-sample tile: thread t <-> sample row t <->
+//    TMEM lane t.  Activations live in a 32 KB fp16 A-operand buffer that is rewritten
+//    in place layer after layer; accumulators live in TMEM (128 fp32 columns per WG);
+//  * one elected thread per warpgroup issues the tcgen05.mma chain of a layer
+//    (M = 128, N = 16..128, K = 16 per instruction) and commits to an mbarrier; the
+//    128 threads run the epilogue (tcgen05.ld -> bias, ReLU -> fp16 -> smem) which is
+//    the next layer's A operand.  Warpgroups interleave, so one WG's gathers/epilogue
+//    overlap another WG's MMAs.
+#include <cuda_runtime.h>
+#include "fv_common.cuh"
+#include "fv_internal.h"
+#include "tc_sm100.cuh"
+
+namespace fv {
+
+// ---- weight pack layout (bytes) ------------------------------------------------------
+constexpr uint32_t PK_OFF0 = 0;                      // [128 x 48]
+constexpr uint32_t PK_OFF1 = PK_OFF0 + 128 * 48 * 2;  // [128 x 128]
+constexpr uint32_t PK_OFF2 = PK_OFF1 + 128 * 128 * 2;
+constexpr uint32_t PK_OFF3 = PK_OFF2 + 128 * 128 * 2;
+constexpr uint32_t PK_OFF4 = PK_OFF3 + 128 * 128 * 2;  // [16 x 128]
+constexpr uint32_t PK_RAD0 = PK_OFF4 + 16 * 128 * 2;   // [64 x 32]
+constexpr uint32_t PK_RAD1 = PK_RAD0 + 64 * 32 * 2;    // [64 x 64]
+constexpr uint32_t PK_RAD2 = PK_RAD1 + 64 * 64 * 2;    // [16 x 64]
+constexpr uint32_t PK_WEND = PK_RAD2 + 16 * 64 * 2;    // 129024
+// fp32 biases: off b1,b2,b3 (128 each), off b4 (16), rad b0 (64), rad b1 (64), rad b2 (16)
+constexpr uint32_t BI_OFF1 = 0, BI_OFF2 = 128, BI_OFF3 = 256, BI_OFF4 = 384, BI_RAD0 = 400, BI_RAD1 = 464,
+                   BI_RAD2 = 528, BI_END = 544;
+constexpr uint32_t PK_BYTES = PK_WEND + BI_END * 4;   // 131200
+constexpr uint32_t SM_B0 = PK_BYTES;                  // 128 floats (per-frame b0')
+constexpr uint32_t SM_A = SM_B0 + 512;                // 131712, 128-B aligned
+constexpr uint32_t A_BYTES = 128 * 128 * 2;           // 32 KB per warpgroup
+
+struct PackLayer { uint32_t off; int N, K, n_true, k_true; };
+
+// (in,out) fp32 weight -> B operand [N rows x K] fp16, K-chunk-major (tc_sm100.cuh).
+__global__ void k_field_pack(fv_field f, uint8_t* __restrict__ pack) {
+  const PackLayer L[8] = {
+      {PK_OFF0, 128, 48, 128, 3 + 6 * f.pe_bands}, {PK_OFF1, 128, 128, 128, 128}, {PK_OFF2, 128, 128, 128, 128},
+      {PK_OFF3, 128, 128, 128, 128},              {PK_OFF4, 16, 128, 3, 128},     {PK_RAD0, 64, 32, 64, 32},
+      {PK_RAD1, 64, 64, 64, 64},                  {PK_RAD2, 16, 64, 4, 64}};
+  const float* W[8] = {f.d_off_w[0], f.d_off_w[1], f.d_off_w[2], f.d_off_w[3], f.d_off_w[4],
+                       f.d_rad_w[0], f.d_rad_w[1], f.d_rad_w[2]};
+  const int layer = blockIdx.y;
+  const PackLayer pl = L[layer];
+  const int words = pl.N * (pl.K / 8);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < words; e += gridDim.x * blockDim.x) {
+    const int nrow = e % pl.N, c = e / pl.N;
+    __half hv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = 8 * c + j;
+      const float v = (k < pl.k_true && nrow < pl.n_true) ? W[layer][(int64_t)k * pl.n_true + nrow] : 0.f;
+      hv[j] = __float2half_rn(v);
+    }
+    *reinterpret_cast<uint4*>(pack + pl.off + tc::op_off(pl.N, nrow, c)) = *reinterpret_cast<uint4*>(hv);
+  }
+  if (layer == 0 && blockIdx.x == 0) {
+    float* bias = reinterpret_cast<float*>(pack + PK_WEND);
+    for (int i = threadIdx.x; i < (int)BI_END; i += blockDim.x) {
+      float v = 0.f;
+      if (i < 384) v = f.d_off_b[1 + i / 128][i % 128];
+      else if (i < 400) v = (i - 384) < 3 ? f.d_off_b[4][i - 384] : 0.f;
+      else if (i < 464) v = f.d_rad_b[0][i - 400];
+      else if (i < 528) v = f.d_rad_b[1][i - 464];
+      else v = (i - 528) < 4 ? f.d_rad_b[2][i - 528] : 0.f;
+      bias[i] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
+}
+
+template <int K, int N>
+__device__ __forceinline__ void layer_mma(const uint8_t* A, const uint8_t* Wt, uint32_t tcol, uint64_t* bar,
+                                          uint32_t& phase, int t, int wg) {
+  tc::fence_proxy_async();
+  tc::fence_before();
+  named_bar(1 + wg, 128);
+  if (t == 0) {
+    tc::fence_after();
+    constexpr uint32_t idesc = tc::idesc_f16(128, N);
+    const uint32_t a0 = tc::smem_u32(A), b0 = tc::smem_u32(Wt);
+#pragma unroll
+    for (int k = 0; k < K / 16; ++k) {
+      const uint64_t ad = tc::make_desc(a0 + k * 2 * 128 * 16, 128 * 16, 128);
+      const uint64_t bd = tc::make_desc(b0 + k * 2 * N * 16, N * 16, 128);
+      tc::mma_f16(tcol, ad, bd, idesc, k > 0 ? 1u : 0u);
+    }
+    tc::mma_commit(bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(bar, phase);
+  phase ^= 1u;
+  tc::fence_after();
+}
+
+// TMEM row -> bias + ReLU -> fp16 -> A operand (columns [0, NC)).
+template <int NC>
+__device__ __forceinline__ void epi_relu(uint32_t trow, const float* bias, uint8_t* A, int t) {
+#pragma unroll
+  for (int g = 0; g < NC / 16; ++g) {
+    float v[16];
+    tc::tmem_ld16(trow + g * 16, v);
+    tc::tmem_ld_wait();
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      w[j] = tc::pack_half2(fmaxf(v[2 * j] + bias[g * 16 + 2 * j], 0.f), fmaxf(v[2 * j + 1] + bias[g * 16 + 2 * j + 1], 0.f));
+    *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * g)) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * g + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+}
+
+template <int NWG>
+__global__ void __launch_bounds__(NWG * 128, 1)
+    k_field_tc(fv_field f, fv_hash h, const float4* __restrict__ xs, int64_t n, float eps_w,
+               float4* __restrict__ rgbs, float* __restrict__ xfinal) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[NWG];
+  __shared__ uint32_t tmem_base;
+  constexpr uint32_t TCOLS = NWG == 1 ? 128 : (NWG == 2 ? 256 : 512);
+
+  {  // weights + biases (one pass per persistent CTA)
+    const uint4* src = reinterpret_cast<const uint4*>(f.d_tc_pack);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    for (int i = threadIdx.x; i < (int)(PK_BYTES / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+    float* b0 = reinterpret_cast<float*>(smem + SM_B0);
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) b0[i] = f.d_off_b0_eff[i];
+  }
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tc::tmem_alloc<TCOLS>(&tmem_base);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NWG; ++i) tc::mbar_init(&bars[i], 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_proxy_async();  // weight stores above -> visible to the tensor-core proxy
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+
+  const int wg = threadIdx.x >> 7;
+  const int t = threadIdx.x & 127;
+  const uint8_t* sW = smem;
+  const float* sBias = reinterpret_cast<const float*>(smem + PK_WEND);
+  const float* sB0 = reinterpret_cast<const float*>(smem + SM_B0);
+  uint8_t* A = smem + SM_A + wg * A_BYTES;
+  const uint32_t tcol = tmem_base + wg * 128;
+  const uint32_t trow = tcol + ((uint32_t)((warp & 3) * 32) << 16);
+  uint64_t* bar = &bars[wg];
+  uint32_t phase = 0;
+
+  const int64_t ntiles = (n + 127) / 128;
+  for (int64_t tile = (int64_t)blockIdx.x * NWG + wg; tile < ntiles; tile += (int64_t)gridDim.x * NWG) {
+    const int64_t s = tile * 128 + t;
+    const float4 v = s < n ? xs[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool fg = s < n && v.w > eps_w;
+    const float x0 = fg ? v.x : 0.f, x1 = fg ? v.y : 0.f, x2 = fg ? v.z : 0.f;
+    float xr0 = 0.f, xr1 = 0.f, xr2 = 0.f;
+    if (f.offset_enabled) {
+      // posenc -> A chunks 0..5 (39 values + zero pad to 48)
+      {
+        __half pe[48];
+        pe[0] = __float2half_rn(x0); pe[1] = __float2half_rn(x1); pe[2] = __float2half_rn(x2);
+        const float xx[3] = {x0, x1, x2};
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const float wk = k < f.pe_bands ? f.pe_w[k] : 0.f;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            float sv, cv;
+            sincospif(xx[j] * (float)(1 << k), &sv, &cv);
+            pe[3 + 6 * k + j] = __float2half_rn(wk * sv);
+            pe[3 + 6 * k + 3 + j] = __float2half_rn(wk * cv);
+          }
+        }
+#pragma unroll
+        for (int j = 39; j < 48; ++j) pe[j] = __float2half_rn(0.f);
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = *reinterpret_cast<const uint4*>(pe + 8 * c);
+      }
+      layer_mma<48, 128>(A, sW + PK_OFF0, tcol, bar, phase, t, wg);
+      epi_relu<128>(trow, sB0, A, t);
+      layer_mma<128, 128>(A, sW + PK_OFF1, tcol, bar, phase, t, wg);
+      epi_relu<128>(trow, sBias + BI_OFF1, A, t);
+      layer_mma<128, 128>(A, sW + PK_OFF2, tcol, bar, phase, t, wg);
+      epi_relu<128>(trow, sBias + BI_OFF2, A, t);
+      layer_mma<128, 128>(A, sW + PK_OFF3, tcol, bar, phase, t, wg);
+      epi_relu<128>(trow, sBias + BI_OFF3, A, t);
+      layer_mma<128, 16>(A, sW + PK_OFF4, tcol, bar, phase, t, wg);
+      {
+        float o[16];
+        tc::tmem_ld16(trow, o);
+        tc::tmem_ld_wait();
+        xr0 = o[0] + sBias[BI_OFF4 + 0];
+        xr1 = o[1] + sBias[BI_OFF4 + 1];
+        xr2 = o[2] + sBias[BI_OFF4 + 2];
+      }
+    }
+    const float y0 = x0 + xr0, y1 = x1 + xr1, y2 = x2 + xr2;
+    if (xfinal && s < n) {
+      xfinal[3 * s] = fg ? y0 : 0.f; xfinal[3 * s + 1] = fg ? y1 : 0.f; xfinal[3 * s + 2] = fg ? y2 : 0.f;
+    }
+    {  // hash-grid features -> A chunks 0..3
+      float xn[3]; bool msk[3];
+      hash_norm(h, y0, y1, y2, xn, msk);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int l = 4 * c + q;
+          float2 fv2 = make_float2(0.f, 0.f);
+          if (l < h.n_levels) {
+            HashCell cell;
+            hash_level_cell(xn, h.res[l], cell);
+            fv2 = hash_level_feat(h, l, cell);
+          }
+          w[q] = tc::pack_half2(fg ? fv2.x : 0.f, fg ? fv2.y : 0.f);
+        }
+        *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    layer_mma<32, 64>(A, sW + PK_RAD0, tcol, bar, phase, t, wg);
+    epi_relu<64>(trow, sBias + BI_RAD0, A, t);
+    layer_mma<64, 64>(A, sW + PK_RAD1, tcol, bar, phase, t, wg);
+    epi_relu<64>(trow, sBias + BI_RAD1, A, t);
+    layer_mma<64, 16>(A, sW + PK_RAD2, tcol, bar, phase, t, wg);
+    {
+      float o[16];
+      tc::tmem_ld16(trow, o);
+      tc::tmem_ld_wait();
+      if (s < n) {
+        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (fg)
+          r = make_float4(sigmoidf_(o[0] + sBias[BI_RAD2]), sigmoidf_(o[1] + sBias[BI_RAD2 + 1]),
+                          sigmoidf_(o[2] + sBias[BI_RAD2 + 2]), softplusf_(o[3] + sBias[BI_RAD2 + 3] - 1.f));
+        rgbs[s] = r;
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<TCOLS>(tmem_base);
+}
+
+constexpr int TC_NWG = 2;
+
+int32_t field_fwd_tc(const fv_field* f, const fv_hash* h, const float4* xs, int64_t n, float eps_w, float4* rgbs,
+                     float* xfinal, cudaStream_t st) {
+  if (!f->d_tc_pack) return set_error(FV_EDIM, "field tc: d_tc_pack is NULL (call fv_field_pack)");
+  if (!f->d_off_b0_eff) return set_error(FV_EDIM, "field tc: d_off_b0_eff is NULL (call fv_offset_bias)");
+  if (h->n_levels * h->n_feat != 32 || f->pe_bands > 6)
+    return set_error(FV_EUNSUPPORTED, "field tc: needs 16x2 hash features and <= 6 PE bands");
+  if (n == 0) return FV_OK;
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = SM_A + TC_NWG * A_BYTES;
+  cudaFuncSetAttribute(k_field_tc<TC_NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t ntiles = (n + 127) / 128;
+  const int64_t want = (ntiles + TC_NWG - 1) / TC_NWG;
+  const int grid = (int)std::min<int64_t>(want, n_sm);
+  k_field_tc<TC_NWG><<<grid, TC_NWG * 128, smem, st>>>(*f, *h, xs, n, eps_w, rgbs, xfinal);
+  return check_launch("field_fwd_tc");
+}
+
+}  // namespace fv
+
+using namespace fv;
+
+extern "C" size_t fv_field_pack_bytes(void) { return PK_BYTES; }
+
+extern "C" int32_t fv_field_pack(const fv_field* field, void* d_tc_pack, void* stream) {
+  if (!field || !d_tc_pack) return set_error(FV_EDIM, "fv_field_pack: null argument");
+  if (field->pe_bands < 1 || field->pe_bands > 6) return set_error(FV_EUNSUPPORTED, "fv_field_pack: 1..6 PE bands");
+  k_field_pack<<<dim3(16, 8), 256, 0, (cudaStream_t)stream>>>(*field, (uint8_t*)d_tc_pack);
+  return check_launch("fv_field_pack");
+}

@@ -1,0 +1,276 @@
+// Device-side building blocks shared by the freeview sm_100a kernels.
+//
+// Everything index-critical (ray generation, slab test, sample depths, occupancy cell,
+// warp grid coordinates, hash-grid vertex) is written with explicit round-to-nearest
+// intrinsics (__fmul_rn / __fadd_rn / __fsub_rn / __fdiv_rn) in the exact order of the
+// float32 oracle (oracle/camera.py, oracle/warp.py, oracle/encoding.py), so no FMA
+// contraction can change a rounding and integer outputs (sample counts, skip masks,
+// hash indices, foreground flags) match the oracle bit for bit.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+#include "../../include/fv_api.h"
+
+namespace fv {
+
+constexpr uint32_t PRIME_Y = 2654435761u;
+constexpr uint32_t PRIME_Z = 805459861u;
+constexpr int OCC_RES = 32;
+
+// ---------------------------------------------------------------- camera / sampling
+struct Ray { float ox, oy, oz, dx, dy, dz; };
+
+// cap:73-82 restated in float32: d = normalize((K^-1 [px+.5, py+.5, 1]) @ R), o = centre.
+__device__ __forceinline__ Ray make_ray(const fv_camera& cam, int32_t pix) {
+  const float px = __fadd_rn((float)(pix % cam.width), 0.5f);
+  const float py = __fadd_rn((float)(pix / cam.width), 0.5f);
+  float dc[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    dc[i] = __fadd_rn(__fadd_rn(__fmul_rn(cam.kinv[3 * i + 0], px), __fmul_rn(cam.kinv[3 * i + 1], py)),
+                      cam.kinv[3 * i + 2]);
+  float d[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    d[j] = __fadd_rn(__fadd_rn(__fmul_rn(dc[0], cam.rot[j]), __fmul_rn(dc[1], cam.rot[3 + j])),
+                     __fmul_rn(dc[2], cam.rot[6 + j]));
+  const float n = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(d[0], d[0]), __fmul_rn(d[1], d[1])),
+                                       __fmul_rn(d[2], d[2])));
+  Ray r;
+  r.ox = cam.center[0]; r.oy = cam.center[1]; r.oz = cam.center[2];
+  r.dx = __fdiv_rn(d[0], n); r.dy = __fdiv_rn(d[1], n); r.dz = __fdiv_rn(d[2], n);
+  return r;
+}
+
+// Slab test; fminf/fmaxf ignore the NaN of 0*inf exactly like numpy fmin/fmax.
+__device__ __forceinline__ bool slab(const Ray& r, const float* bmin, const float* bmax,
+                                     float& t_enter, float& t_exit) {
+  const float o[3] = {r.ox, r.oy, r.oz};
+  const float d[3] = {r.dx, r.dy, r.dz};
+  float tn[3], tf[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float inv = __fdiv_rn(1.0f, d[j]);
+    const float t0 = __fmul_rn(__fsub_rn(bmin[j], o[j]), inv);
+    const float t1 = __fmul_rn(__fsub_rn(bmax[j], o[j]), inv);
+    tn[j] = fminf(t0, t1);
+    tf[j] = fmaxf(t0, t1);
+  }
+  t_enter = fmaxf(fmaxf(fmaxf(tn[0], tn[1]), tn[2]), 0.0f);
+  t_exit = fminf(fminf(tf[0], tf[1]), tf[2]);
+  return t_exit > t_enter;
+}
+
+__device__ __forceinline__ uint32_t hash_u32(uint32_t seed, uint32_t pix, uint32_t i) {
+  uint32_t h = seed ^ (pix * 0x9E3779B1u) ^ ((i + 1u) * 0x85EBCA77u);
+  h ^= h >> 16; h *= 0x7FEB352Du;
+  h ^= h >> 15; h *= 0x846CA68Bu;
+  h ^= h >> 16;
+  return h;
+}
+
+__device__ __forceinline__ float jitter_u(uint32_t seed, uint32_t pix, uint32_t i) {
+  return __fmul_rn((float)(hash_u32(seed, pix, i) >> 8), 5.9604644775390625e-08f);  // 2^-24
+}
+
+// t_i = t_enter + (i + u_i) * step
+__device__ __forceinline__ float sample_t(float t_enter, float step, int i, float u) {
+  return __fadd_rn(t_enter, __fmul_rn(__fadd_rn((float)i, u), step));
+}
+
+__device__ __forceinline__ bool occ_test(const uint32_t* occ, const float* bmin, const float* scale,
+                                         float x, float y, float z) {
+  const float p[3] = {x, y, z};
+  int c[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float q = floorf(__fmul_rn(__fsub_rn(p[j], bmin[j]), scale[j]));
+    c[j] = q < 0.f ? 0 : (q > (float)(OCC_RES - 1) ? OCC_RES - 1 : (int)q);
+  }
+  const int cell = (c[0] * OCC_RES + c[1]) * OCC_RES + c[2];
+  return (__ldg(occ + (cell >> 5)) >> (cell & 31)) & 1u;
+}
+
+// ---------------------------------------------------------------- skeleton warp
+// Corner-packed weight volume: for channel i and padded-grid cell (ix,iy,iz) in [0,G]^3 the
+// 8 corner values vp[i, ix+a, iy+b, iz+c] (a*4+b*2+c order) are stored contiguously
+// (one 16-byte word in fp16, two in fp32), so one gather replaces the 8 of ad:767-773.
+__device__ __forceinline__ void load_corners(const void* vol, int half, size_t cell, float (&cv)[8]) {
+  if (half) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(vol) + cell);
+    const __half2* h = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { float2 f = __half22float2(h[q]); cv[2 * q] = f.x; cv[2 * q + 1] = f.y; }
+  } else {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(vol) + 2 * cell);
+    const float4 b = __ldg(reinterpret_cast<const float4*>(vol) + 2 * cell + 1);
+    cv[0] = a.x; cv[1] = a.y; cv[2] = a.z; cv[3] = a.w; cv[4] = b.x; cv[5] = b.y; cv[6] = b.z; cv[7] = b.w;
+  }
+}
+
+// Grid coordinates of bone point p for the volume (ad:746-753); returns inside flag.
+__device__ __forceinline__ bool warp_cell(const fv_warp& w, const float (&p)[3], int (&i0)[3], float (&f)[3]) {
+  bool inside = true;
+  const float gp1 = (float)(w.vol_res + 1);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float u = __fadd_rn(__fmul_rn(__fsub_rn(p[j], w.wbox_min[j]), w.wscale[j]), 1.0f);
+    inside = inside && (u >= 0.0f) && (u <= gp1);
+    float fl = floorf(u);
+    fl = fl < 0.f ? 0.f : (fl > (float)w.vol_res ? (float)w.vol_res : fl);
+    i0[j] = (int)fl;
+    f[j] = __fsub_rn(u, fl);
+  }
+  return inside;
+}
+
+__device__ __forceinline__ float trilerp8(const float (&f)[3], const float (&cv)[8]) {
+  const float wx[2] = {__fsub_rn(1.0f, f[0]), f[0]};
+  const float wy[2] = {__fsub_rn(1.0f, f[1]), f[1]};
+  const float wz[2] = {__fsub_rn(1.0f, f[2]), f[2]};
+  float acc = 0.0f;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(__fmul_rn(wx[a], wy[b]), wz[c]), cv[a * 4 + b * 2 + c]));
+  return acc;
+}
+
+// p = x @ R^T + t (row convention, sk:171-172), op order of oracle.warp.bone_points
+__device__ __forceinline__ void bone_point(const float* g, float x0, float x1, float x2, float (&p)[3]) {
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    p[j] = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(g[3 * j], x0), __fmul_rn(g[3 * j + 1], x1)),
+                               __fmul_rn(g[3 * j + 2], x2)), g[9 + j]);
+}
+
+__device__ __forceinline__ size_t vol_cell_index(int bone, int res, const int (&i0)[3]) {
+  const int s = res + 1;
+  return ((size_t)(bone * s + i0[0]) * s + i0[1]) * s + i0[2];
+}
+
+// Full skeleton warp of one point with G in shared memory (sg: K*12 floats).
+// Returns L; xs = sum_i w_i p_i / L (0 if L <= eps_w).  Optional per-bone weights out.
+template <bool STORE_W>
+__device__ __forceinline__ float warp_point(const fv_warp& w, const float* sg, float eps_w,
+                                            float x0, float x1, float x2, float (&xs)[3],
+                                            float* w_out = nullptr, size_t w_stride = 0) {
+  float lik = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f;
+  const int K = w.n_bones;
+#pragma unroll 4
+  for (int i = 0; i < K; ++i) {
+    float p[3];
+    bone_point(sg + 12 * i, x0, x1, x2, p);
+    int i0[3]; float f[3];
+    float wi = 0.f;
+    if (warp_cell(w, p, i0, f)) {
+      float cv[8];
+      load_corners(w.d_vol_packed, w.vol_half, vol_cell_index(i, w.vol_res, i0), cv);
+      wi = trilerp8(f, cv);
+    }
+    if (STORE_W) w_out[(size_t)i * w_stride] = wi;
+    lik = __fadd_rn(lik, wi);
+    s0 = __fadd_rn(s0, __fmul_rn(wi, p[0]));
+    s1 = __fadd_rn(s1, __fmul_rn(wi, p[1]));
+    s2 = __fadd_rn(s2, __fmul_rn(wi, p[2]));
+  }
+  if (lik > eps_w) {
+    xs[0] = __fdiv_rn(s0, lik); xs[1] = __fdiv_rn(s1, lik); xs[2] = __fdiv_rn(s2, lik);
+  } else {
+    xs[0] = xs[1] = xs[2] = 0.f;
+  }
+  return lik;
+}
+
+// ---------------------------------------------------------------- hash grid
+struct HashCell { int i0[3]; float f[3]; };
+
+__device__ __forceinline__ void hash_norm(const fv_hash& h, float x0, float x1, float x2, float (&xn)[3],
+                                          bool (&mask)[3]) {
+  const float x[3] = {x0, x1, x2};
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float raw = __fmul_rn(__fsub_rn(x[j], h.cmin[j]), h.cinv[j]);
+    mask[j] = (raw >= 0.f) && (raw <= 1.f);
+    xn[j] = fminf(fmaxf(raw, 0.f), 1.f);
+  }
+}
+
+__device__ __forceinline__ void hash_level_cell(const float (&xn)[3], int res, HashCell& c) {
+  const float rf = (float)res;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float pos = __fmul_rn(xn[j], rf);
+    float fl = floorf(pos);
+    fl = fminf(fl, rf - 1.0f);
+    c.i0[j] = (int)fl;
+    c.f[j] = __fsub_rn(pos, fl);
+  }
+}
+
+__device__ __forceinline__ uint32_t hash_index(int dense, int res, uint32_t mask_T, uint32_t x, uint32_t y,
+                                               uint32_t z) {
+  if (dense) {
+    const uint32_t s = (uint32_t)res + 1u;
+    return x + y * s + z * (s * s);
+  }
+  return (x ^ (y * PRIME_Y) ^ (z * PRIME_Z)) & mask_T;
+}
+
+// Features of one level (F = 2).
+__device__ __forceinline__ float2 hash_level_feat(const fv_hash& h, int l, const HashCell& c,
+                                                  uint32_t* idx_out = nullptr) {
+  const float wx[2] = {__fsub_rn(1.0f, c.f[0]), c.f[0]};
+  const float wy[2] = {__fsub_rn(1.0f, c.f[1]), c.f[1]};
+  const float wz[2] = {__fsub_rn(1.0f, c.f[2]), c.f[2]};
+  const uint32_t maskT = (1u << h.log2_T) - 1u;
+  const uint32_t off = h.offset[l];
+  uint32_t gidx[8];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+        gidx[a * 4 + b * 2 + cc] = off + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + a, c.i0[1] + b, c.i0[2] + cc);
+  float2 v[8];
+  if (h.table_half) {
+    const __half2* t = reinterpret_cast<const __half2*>(h.d_table);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __half22float2(__ldg(t + gidx[q]));
+  } else {
+    const float2* t = reinterpret_cast<const float2*>(h.d_table);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldg(t + gidx[q]);
+  }
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const float wgt = __fmul_rn(__fmul_rn(wx[a], wy[b]), wz[cc]);
+        const int q = a * 4 + b * 2 + cc;
+        acc.x = __fadd_rn(acc.x, __fmul_rn(wgt, v[q].x));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(wgt, v[q].y));
+      }
+  if (idx_out) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) idx_out[q] = gidx[q];
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------- heads
+__device__ __forceinline__ float sigmoidf_(float x) {
+  if (x >= 0.f) return 1.f / (1.f + expf(-x));
+  const float e = expf(x);
+  return e / (1.f + e);
+}
+__device__ __forceinline__ float softplusf_(float x) { return log1pf(expf(-fabsf(x))) + fmaxf(x, 0.f); }
+
+}  // namespace fv

@@ -1,0 +1,31 @@
+// Internal helpers for the C-ABI layer: thread-local error messages and launch checks.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../../include/fv_api.h"
+
+namespace fv {
+int32_t set_error(int32_t code, const char* msg);
+int32_t check_launch(const char* where);
+int32_t check_hash(const fv_hash* h);
+int32_t field_fwd_f32(const fv_field* f, const fv_hash* h, const float4* xs, int64_t n, float eps_w, float4* rgbs,
+                      float* xfinal, void* work, size_t work_bytes, cudaStream_t st);
+size_t field_f32_work_bytes(int64_t n);
+int32_t field_fwd_tc(const fv_field* f, const fv_hash* h, const float4* xs, int64_t n, float eps_w, float4* rgbs,
+                     float* xfinal, cudaStream_t st);
+struct CompIn {
+  const float4* rgbs;   // [c, sigma] per sample
+  const float* delta;   // per sample
+  const float* lik;     // per sample, stride lik_stride floats
+  int lik_stride;
+  bool blocked;         // sample layout: ray-block-major (render) or ray-major [R][N]
+};
+int32_t composite_fwd(const CompIn& in, int64_t n_rays, int n, const float* bg, float eps_w, float eps_t,
+                      const int32_t* out_pix, float* rgb, float* alpha, float* trans, cudaStream_t st);
+int32_t composite_bwd(const CompIn& in, const float* trans, int64_t n_rays, int n, const float* bg, float eps_w,
+                      const float* drgb, const float* dalpha, float4* dout, cudaStream_t st);
+int32_t field_fwd(const fv_field* f, const fv_hash* h, const float4* xs, int64_t n, float eps_w, float4* rgbs,
+                  float* xfinal, void* work, size_t work_bytes, cudaStream_t st);
+}  // namespace fv

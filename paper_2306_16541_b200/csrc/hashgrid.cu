@@ -1,0 +1,104 @@
+// Multiresolution hash-grid encoding, forward and backward (builder-defined; the
+// definition and its float32 operation order live in oracle/encoding.py).
+#include <cuda_runtime.h>
+#include "fv_common.cuh"
+#include "fv_internal.h"
+
+namespace fv {
+
+__global__ void __launch_bounds__(128) k_hash_fwd(fv_hash h, const float* __restrict__ x, int64_t n,
+                                                  float* __restrict__ feat, uint32_t* __restrict__ index) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  float xn[3]; bool mask[3];
+  hash_norm(h, x[3 * p], x[3 * p + 1], x[3 * p + 2], xn, mask);
+  for (int l = 0; l < h.n_levels; ++l) {
+    HashCell c;
+    hash_level_cell(xn, h.res[l], c);
+    uint32_t idx[8];
+    const float2 f = hash_level_feat(h, l, c, index ? idx : nullptr);
+    feat[p * (2 * h.n_levels) + 2 * l] = f.x;
+    feat[p * (2 * h.n_levels) + 2 * l + 1] = f.y;
+    if (index) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) index[(p * h.n_levels + l) * 8 + q] = idx[q];
+    }
+  }
+}
+
+// dtable += w_corner * dfeat (float2 vector atomics); dx = sum_l d feat_l / d x.
+__global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __restrict__ x, int64_t n,
+                                                  const float* __restrict__ dfeat, float* __restrict__ dtable,
+                                                  float* __restrict__ dx) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  float xn[3]; bool mask[3];
+  hash_norm(h, x[3 * p], x[3 * p + 1], x[3 * p + 2], xn, mask);
+  const uint32_t maskT = (1u << h.log2_T) - 1u;
+  float gx = 0.f, gy = 0.f, gz = 0.f;
+  for (int l = 0; l < h.n_levels; ++l) {
+    const float g0 = dfeat[p * (2 * h.n_levels) + 2 * l];
+    const float g1 = dfeat[p * (2 * h.n_levels) + 2 * l + 1];
+    HashCell c;
+    hash_level_cell(xn, h.res[l], c);
+    const float wx[2] = {1.f - c.f[0], c.f[0]}, wy[2] = {1.f - c.f[1], c.f[1]}, wz[2] = {1.f - c.f[2], c.f[2]};
+    float px = 0.f, py = 0.f, pz = 0.f;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const uint32_t gi = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + a, c.i0[1] + b,
+                                                       c.i0[2] + cc);
+          const float wgt = wx[a] * wy[b] * wz[cc];
+          if (g0 != 0.f || g1 != 0.f)
+            atomicAdd(reinterpret_cast<float2*>(dtable) + gi, make_float2(wgt * g0, wgt * g1));
+          if (dx) {
+            float2 v;
+            if (h.table_half) v = __half22float2(__ldg(reinterpret_cast<const __half2*>(h.d_table) + gi));
+            else v = __ldg(reinterpret_cast<const float2*>(h.d_table) + gi);
+            const float gv = g0 * v.x + g1 * v.y;
+            px += (a ? 1.f : -1.f) * wy[b] * wz[cc] * gv;
+            py += wx[a] * (b ? 1.f : -1.f) * wz[cc] * gv;
+            pz += wx[a] * wy[b] * (cc ? 1.f : -1.f) * gv;
+          }
+        }
+    const float rf = (float)h.res[l];
+    gx += px * rf; gy += py * rf; gz += pz * rf;
+  }
+  if (dx) {
+    dx[3 * p] = mask[0] ? gx * h.cinv[0] : 0.f;
+    dx[3 * p + 1] = mask[1] ? gy * h.cinv[1] : 0.f;
+    dx[3 * p + 2] = mask[2] ? gz * h.cinv[2] : 0.f;
+  }
+}
+
+int32_t check_hash(const fv_hash* h) {
+  if (!h || h->n_levels < 1 || h->n_levels > FV_MAX_LEVELS || h->n_feat != 2 || h->log2_T < 4 || h->log2_T > 26 ||
+      !h->d_table)
+    return set_error(FV_EDIM, "fv_hash: unsupported configuration (levels 1..16, F = 2, log2_T 4..26)");
+  return FV_OK;
+}
+
+}  // namespace fv
+
+using namespace fv;
+
+extern "C" int32_t fv_hash_fwd(const fv_hash* hash, const float* d_x, int64_t n, float* d_feat, uint32_t* d_index,
+                               void* stream) {
+  if (int32_t e = check_hash(hash)) return e;
+  if (n < 0) return set_error(FV_EDIM, "fv_hash_fwd: n < 0");
+  if (n == 0) return FV_OK;
+  k_hash_fwd<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*hash, d_x, n, d_feat, d_index);
+  return check_launch("fv_hash_fwd");
+}
+
+extern "C" int32_t fv_hash_bwd(const fv_hash* hash, const float* d_x, int64_t n, const float* d_dfeat,
+                               float* d_dtable, float* d_dx, void* stream) {
+  if (int32_t e = check_hash(hash)) return e;
+  if (n < 0) return set_error(FV_EDIM, "fv_hash_bwd: n < 0");
+  if (n == 0) return FV_OK;
+  k_hash_bwd<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*hash, d_x, n, d_dfeat, d_dtable, d_dx);
+  return check_launch("fv_hash_bwd");
+}

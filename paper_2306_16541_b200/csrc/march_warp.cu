@@ -1,0 +1,200 @@
+// Ray march + skeleton warp kernels (S:410-413 sampling, S:327-336 warp; ad:728-773).
+#include <cuda_runtime.h>
+#include "fv_common.cuh"
+#include "layout.cuh"
+#include "fv_internal.h"
+
+namespace fv {
+
+// W^c (C,G,G,G) -> corner-packed [K][(G+1)^3][8], zero padding of ad:755-756 folded in.
+template <typename T>
+__global__ void k_warp_pack(const float* __restrict__ vol, int K, int G, T* __restrict__ out) {
+  const int s = G + 1;
+  const int64_t total = (int64_t)K * s * s * s;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q = e;
+    const int iz = q % s; q /= s;
+    const int iy = q % s; q /= s;
+    const int ix = q % s; q /= s;
+    const int ch = (int)q;
+    float v[8];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          // padded index (ix+a, iy+b, iz+c) -> original (.. - 1)
+          const int x = ix + a - 1, y = iy + b - 1, z = iz + c - 1;
+          const bool in = x >= 0 && x < G && y >= 0 && y < G && z >= 0 && z < G;
+          v[a * 4 + b * 2 + c] = in ? vol[(((int64_t)ch * G + x) * G + y) * G + z] : 0.f;
+        }
+    if constexpr (sizeof(T) == 2) {
+      __half2 h[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] = __floats2half2_rn(v[2 * k], v[2 * k + 1]);
+      reinterpret_cast<uint4*>(out)[e] = *reinterpret_cast<uint4*>(h);
+    } else {
+      float4* o = reinterpret_cast<float4*>(out) + 2 * e;
+      o[0] = make_float4(v[0], v[1], v[2], v[3]);
+      o[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  }
+}
+
+__global__ void k_warp_fwd(fv_warp w, float eps_w, const float* __restrict__ x, int64_t n,
+                           float* __restrict__ xskel, float* __restrict__ lik, uint8_t* __restrict__ fg,
+                           float* __restrict__ wout) {
+  __shared__ float sg[FV_MAX_BONES * 12];
+  for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
+  __syncthreads();
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  float xs[3];
+  float L;
+  if (wout) L = warp_point<true>(w, sg, eps_w, x[3 * p], x[3 * p + 1], x[3 * p + 2], xs, wout + p, (size_t)n);
+  else L = warp_point<false>(w, sg, eps_w, x[3 * p], x[3 * p + 1], x[3 * p + 2], xs);
+  xskel[3 * p] = xs[0]; xskel[3 * p + 1] = xs[1]; xskel[3 * p + 2] = xs[2];
+  lik[p] = L;
+  fg[p] = L > eps_w;
+}
+
+// One thread per sample (ray-block-major layout).  Writes xs[s] = (x_skel, L) with L = 0
+// for samples outside the box or in empty occupancy cells, delta[s], optional x[s].
+__global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, fv_warp w, int64_t n_rays,
+                                                    float4* __restrict__ xs_out, float* __restrict__ delta_out,
+                                                    float* __restrict__ x_out, int32_t* __restrict__ count_out) {
+  __shared__ float sg[FV_MAX_BONES * 12];
+  for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
+  __syncthreads();
+  const int N = m.n_samples;
+  const int64_t total = padded_rays(n_rays) * N;
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= total) return;
+  int64_t ray; int32_t i;
+  sample_coords(s, N, ray, i);
+  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+  float delta = 0.f;
+  bool hit = false;
+  if (ray < n_rays) {
+    const int32_t pix = m.d_pix ? m.d_pix[ray] : (int32_t)(m.pix_offset + ray);
+    const Ray r = make_ray(cam, pix);
+    float t0, t1;
+    hit = slab(r, m.obox_min, m.obox_max, t0, t1);
+    if (hit) {
+      const float step = __fdiv_rn(__fsub_rn(t1, t0), (float)N);
+      const float ui = m.jitter ? jitter_u(m.seed, (uint32_t)pix, i) : 0.5f;
+      const float t = sample_t(t0, step, i, ui);
+      if (i + 1 < N) {
+        const float un = m.jitter ? jitter_u(m.seed, (uint32_t)pix, i + 1) : 0.5f;
+        delta = __fsub_rn(sample_t(t0, step, i + 1, un), t);
+      } else {
+        const float u0 = m.jitter ? jitter_u(m.seed, (uint32_t)pix, 0) : 0.5f;
+        delta = __fadd_rn(__fsub_rn(t1, t), __fsub_rn(sample_t(t0, step, 0, u0), t0));
+      }
+      const float px = __fadd_rn(r.ox, __fmul_rn(t, r.dx));
+      const float py = __fadd_rn(r.oy, __fmul_rn(t, r.dy));
+      const float pz = __fadd_rn(r.oz, __fmul_rn(t, r.dz));
+      if (x_out) { x_out[3 * s] = px; x_out[3 * s + 1] = py; x_out[3 * s + 2] = pz; }
+      const bool occ = m.d_occ == nullptr || occ_test(m.d_occ, m.obox_min, m.occ_scale, px, py, pz);
+      if (occ) {
+        float xsk[3];
+        const float L = warp_point<false>(w, sg, m.eps_w, px, py, pz, xsk);
+        out = make_float4(xsk[0], xsk[1], xsk[2], L);
+      }
+    } else if (x_out) {
+      x_out[3 * s] = x_out[3 * s + 1] = x_out[3 * s + 2] = 0.f;
+    }
+    if (i == 0 && count_out) count_out[ray] = hit ? N : 0;
+  } else if (x_out) {
+    x_out[3 * s] = x_out[3 * s + 1] = x_out[3 * s + 2] = 0.f;
+  }
+  xs_out[s] = out;
+  delta_out[s] = delta;
+}
+
+// d x_skel -> d W^c (C,G,G,G) via dw_i = <dxs, p_i - x_skel>/L and the trilinear scatter.
+__global__ void k_warp_bwd(fv_warp w, float eps_w, const float* __restrict__ x, int64_t n,
+                           const float* __restrict__ dxs, float* __restrict__ dvol) {
+  __shared__ float sg[FV_MAX_BONES * 12];
+  for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
+  __syncthreads();
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const float g0 = dxs[3 * q], g1 = dxs[3 * q + 1], g2 = dxs[3 * q + 2];
+  if (g0 == 0.f && g1 == 0.f && g2 == 0.f) return;
+  const float x0 = x[3 * q], x1 = x[3 * q + 1], x2 = x[3 * q + 2];
+  float xsk[3];
+  const float L = warp_point<false>(w, sg, eps_w, x0, x1, x2, xsk);
+  if (!(L > eps_w)) return;
+  const float invL = 1.f / L;
+  const int G = w.vol_res;
+  for (int i = 0; i < w.n_bones; ++i) {
+    float p[3];
+    bone_point(sg + 12 * i, x0, x1, x2, p);
+    int i0[3]; float f[3];
+    if (!warp_cell(w, p, i0, f)) continue;
+    const float dw = (g0 * (p[0] - xsk[0]) + g1 * (p[1] - xsk[1]) + g2 * (p[2] - xsk[2])) * invL;
+    if (dw == 0.f) continue;
+    const float wx[2] = {1.f - f[0], f[0]}, wy[2] = {1.f - f[1], f[1]}, wz[2] = {1.f - f[2], f[2]};
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int vx = i0[0] + a - 1, vy = i0[1] + b - 1, vz = i0[2] + c - 1;
+          if (vx < 0 || vx >= G || vy < 0 || vy >= G || vz < 0 || vz >= G) continue;
+          atomicAdd(dvol + (((int64_t)i * G + vx) * G + vy) * G + vz, wx[a] * wy[b] * wz[c] * dw);
+        }
+  }
+}
+
+}  // namespace fv
+
+using namespace fv;
+
+extern "C" int32_t fv_warp_pack(const float* d_vol, int32_t channels, const fv_warp* warp, void* d_vol_packed,
+                                void* stream) {
+  if (!warp || !d_vol || !d_vol_packed) return set_error(FV_EDIM, "fv_warp_pack: null argument");
+  if (warp->n_bones < 1 || warp->n_bones > FV_MAX_BONES || warp->n_bones > channels || warp->vol_res < 2)
+    return set_error(FV_EDIM, "fv_warp_pack: bad bone count / resolution");
+  const int64_t cells = (int64_t)warp->n_bones * (warp->vol_res + 1) * (warp->vol_res + 1) * (warp->vol_res + 1);
+  const int grid = (int)std::min<int64_t>((cells + 255) / 256, 148 * 16);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (warp->vol_half)
+    k_warp_pack<__half><<<grid, 256, 0, st>>>(d_vol, warp->n_bones, warp->vol_res, (__half*)d_vol_packed);
+  else
+    k_warp_pack<float><<<grid, 256, 0, st>>>(d_vol, warp->n_bones, warp->vol_res, (float*)d_vol_packed);
+  return check_launch("fv_warp_pack");
+}
+
+extern "C" int32_t fv_warp_fwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n, float* d_xskel,
+                               float* d_lik, uint8_t* d_fg, float* d_w, void* stream) {
+  if (!warp || n < 0) return set_error(FV_EDIM, "fv_warp_fwd: bad arguments");
+  if (warp->n_bones < 1 || warp->n_bones > FV_MAX_BONES) return set_error(FV_EDIM, "fv_warp_fwd: bad bone count");
+  if (n == 0) return FV_OK;
+  k_warp_fwd<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*warp, eps_w, d_x, n, d_xskel, d_lik,
+                                                                             d_fg, d_w);
+  return check_launch("fv_warp_fwd");
+}
+
+extern "C" int32_t fv_warp_bwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
+                               const float* d_dxskel, float* d_dvol, void* stream) {
+  if (!warp || n < 0) return set_error(FV_EDIM, "fv_warp_bwd: bad arguments");
+  if (n == 0) return FV_OK;
+  k_warp_bwd<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*warp, eps_w, d_x, n, d_dxskel, d_dvol);
+  return check_launch("fv_warp_bwd");
+}
+
+extern "C" int32_t fv_march_warp(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays,
+                                 float* d_xs, float* d_delta, float* d_x, int32_t* d_count, void* stream) {
+  if (!cam || !march || !warp || n_rays < 0 || march->n_samples < 1)
+    return set_error(FV_EDIM, "fv_march_warp: bad arguments");
+  if (warp->n_bones < 1 || warp->n_bones > FV_MAX_BONES) return set_error(FV_EDIM, "fv_march_warp: bad bone count");
+  if (n_rays == 0) return FV_OK;
+  const int64_t total = padded_rays(n_rays) * march->n_samples;
+  k_march_warp<<<(unsigned)((total + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      *cam, *march, *warp, n_rays, (float4*)d_xs, d_delta, d_x, d_count);
+  return check_launch("fv_march_warp");
+}

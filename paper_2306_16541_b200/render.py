@@ -1,0 +1,226 @@
+"""Radiance renderer API (SPEC ``S:387-466``) on the sm_100a path.
+
+``render_image(nets, camera, pose, settings, schedule)`` (``S:438-446``) is one
+``fv_render_fwd`` call: ray generation, slab test, stratified jittered sampling,
+occupancy skip and skeleton warp (``fv_march_warp``, one thread per sample), the fused
+tcgen05 field (residual MLP -> hash grid -> radiance MLP) or its fp32 twin, and the
+front-to-back compositor with the likelihood gate and early termination.
+
+The primitive operators of the SPEC are exposed on the same kernels:
+``skeleton_warp``, ``query_radiance``, ``composite``,
+``warp_point``.  No CPU fallback exists: without libfvcuda.so or a CUDA device
+every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from .camera import CameraModel, tiled_pixel_order
+from .errors import DimensionError
+from .model import FreeviewModel
+from .skeleton import Pose
+
+EPS_W = 1e-4
+
+
+@dataclass
+class RenderSettings:
+    """samples per ray, subject box, background, jitter seed, eps_w."""
+    n_samples: int = 128
+    jitter: bool = True
+    seed: int = 0
+    eps_w: float = EPS_W
+    eps_t: float = 0.0                     # early-termination transmittance (0 = off)
+    background: Tuple[float, float, float] = (0.5, 0.5, 0.5)
+    box_min: Tuple[float, float, float] = (-1.0, -1.0, -1.0)
+    box_max: Tuple[float, float, float] = (1.0, 1.0, 1.0)
+    occupancy: bool = False                # build + use the 32^3 skip grid per pose
+    occ_threshold: float = 0.01
+
+    @classmethod
+    def from_config(cls, cfg, **kw) -> "RenderSettings":
+        base = dict(n_samples=cfg.n_samples, jitter=cfg.jitter, background=tuple(cfg.background),
+                    occupancy=cfg.occupancy)
+        base.update(kw)
+        return cls(**base)
+
+
+def camera_struct(cam: CameraModel) -> _lib.FvCamera:
+    kinv, rot, ctr = cam.kernel_consts()
+    c = _lib.FvCamera()
+    _lib.farr(c.kinv, kinv.reshape(-1))
+    _lib.farr(c.rot, rot.reshape(-1))
+    _lib.farr(c.center, ctr)
+    c.width, c.height = cam.width, cam.height
+    return c
+
+
+def march_struct(s: RenderSettings, pix: Optional[torch.Tensor], occ: Optional[torch.Tensor],
+                 out_by_pixel: bool = False) -> _lib.FvMarch:
+    m = _lib.FvMarch()
+    bmin = np.asarray(s.box_min, np.float64)
+    bmax = np.asarray(s.box_max, np.float64)
+    _lib.farr(m.obox_min, bmin.astype(np.float32))
+    _lib.farr(m.obox_max, bmax.astype(np.float32))
+    m.n_samples, m.jitter, m.seed = s.n_samples, int(s.jitter), s.seed & 0xFFFFFFFF
+    m.eps_w, m.eps_t = s.eps_w, s.eps_t
+    _lib.farr(m.bg, s.background)
+    m.d_occ = occ.data_ptr() if occ is not None else None
+    _lib.farr(m.occ_scale, (32.0 / (bmax - bmin)).astype(np.float32))
+    m.d_pix = pix.data_ptr() if pix is not None else None
+    m.pix_offset = 0
+    m.out_by_pixel = int(out_by_pixel)
+    return m
+
+
+class Renderer:
+    """Owns the reusable device workspace, pixel orders and the occupancy bitfield."""
+
+    def __init__(self, device: str = "cuda"):
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        self._work = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self._orders = {}
+        self.occ = torch.zeros(1024, dtype=torch.int32, device=self.device)
+        self._occ_key = None
+
+    def workspace(self, nbytes: int) -> torch.Tensor:
+        if self._work.numel() < nbytes:
+            self._work = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self._work
+
+    def pixel_order(self, cam: CameraModel) -> torch.Tensor:
+        key = (cam.width, cam.height)
+        if key not in self._orders:
+            self._orders[key] = torch.from_numpy(tiled_pixel_order(cam.width, cam.height)).to(self.device)
+        return self._orders[key]
+
+    def build_occupancy(self, nets: FreeviewModel, settings: RenderSettings, stream=None) -> torch.Tensor:
+        """fv_occupancy_build for the current pose (32^3 bits over the observation box)."""
+        m = march_struct(settings, None, None)
+        w, h, f = nets.warp_struct(), nets.hash_struct(), nets.field_struct()
+        nb = self.lib.fv_occupancy_workspace_bytes(f.precision)
+        work = self.workspace(nb)
+        _lib.check(self.lib.fv_occupancy_build(C.byref(m), C.byref(w), C.byref(h), C.byref(f),
+                                               settings.occ_threshold, work.data_ptr(), nb,
+                                               self.occ.data_ptr(), _lib.stream_ptr(stream)),
+                   "fv_occupancy_build")
+        return self.occ
+
+    def render_pixels(self, nets: FreeviewModel, cam: CameraModel, pix: torch.Tensor, settings: RenderSettings,
+                      out_rgb: Optional[torch.Tensor] = None, out_alpha: Optional[torch.Tensor] = None,
+                      counts: Optional[torch.Tensor] = None, by_pixel: bool = False, occ: Optional[torch.Tensor] = None,
+                      stream=None):
+        """Render the rays of linear pixel ids ``pix`` (int32, device).  Outputs are per ray
+        (or written at the pixel id into image-sized buffers when ``by_pixel``)."""
+        if pix.dtype != torch.int32 or not pix.is_cuda:
+            raise DimensionError("pix must be an int32 CUDA tensor")
+        n = pix.numel()
+        n_out = cam.width * cam.height if by_pixel else n
+        if out_rgb is None:
+            out_rgb = torch.empty((n_out, 3), dtype=torch.float32, device=self.device)
+        if out_alpha is None:
+            out_alpha = torch.empty(n_out, dtype=torch.float32, device=self.device)
+        m = march_struct(settings, pix, occ, by_pixel)
+        cs = camera_struct(cam)
+        w, h, f = nets.warp_struct(), nets.hash_struct(), nets.field_struct()
+        nb = self.lib.fv_render_workspace_bytes(n, settings.n_samples, f.precision)
+        work = self.workspace(nb)
+        _lib.check(self.lib.fv_render_fwd(C.byref(cs), C.byref(m), C.byref(w), C.byref(h), C.byref(f), n,
+                                          work.data_ptr(), nb, out_rgb.data_ptr(), out_alpha.data_ptr(),
+                                          counts.data_ptr() if counts is not None else None,
+                                          _lib.stream_ptr(stream)), "fv_render_fwd")
+        return out_rgb, out_alpha
+
+    def render_image(self, nets: FreeviewModel, cam: CameraModel, pose: Optional[Pose], settings: RenderSettings,
+                     out_rgb=None, out_alpha=None, stream=None):
+        if pose is not None:
+            nets.set_pose(pose, stream)
+        occ = self.build_occupancy(nets, settings, stream) if settings.occupancy else None
+        pix = self.pixel_order(cam)
+        rgb, alpha = self.render_pixels(nets, cam, pix, settings, out_rgb, out_alpha, by_pixel=True, occ=occ,
+                                        stream=stream)
+        return rgb.view(cam.height, cam.width, 3), alpha.view(cam.height, cam.width)
+
+
+_DEFAULT = {}
+
+
+def _renderer(device) -> Renderer:
+    key = str(device)
+    if key not in _DEFAULT:
+        _DEFAULT[key] = Renderer(device)
+    return _DEFAULT[key]
+
+
+def render_image(nets: FreeviewModel, camera: CameraModel, pose: Optional[Pose], settings: RenderSettings,
+                 schedule=None):
+    """(image (H,W,3), alpha (H,W)) CUDA tensors; deterministic given the jitter seed."""
+    if schedule is not None:
+        nets.set_schedule(**schedule)
+    return _renderer(nets.device).render_image(nets, camera, pose, settings)
+
+
+# ---------------------------------------------------------------------------------- primitives
+
+def skeleton_warp(nets: FreeviewModel, x: torch.Tensor, eps_w: float = EPS_W):
+    """x (n,3) world -> (x_skel (n,3), likelihood (n), fg (n) bool) for the current pose."""
+    n = x.shape[0]
+    xs = torch.empty((n, 3), dtype=torch.float32, device=x.device)
+    lik = torch.empty(n, dtype=torch.float32, device=x.device)
+    fg = torch.empty(n, dtype=torch.uint8, device=x.device)
+    w = nets.warp_struct()
+    _lib.check(nets.lib.fv_warp_fwd(C.byref(w), eps_w, x.contiguous().data_ptr(), n, xs.data_ptr(),
+                                    lik.data_ptr(), fg.data_ptr(), None, _lib.stream_ptr()), "fv_warp_fwd")
+    return xs, lik, fg.bool()
+
+
+def _field(nets, xs4, eps_w, offset_enabled, want_xfinal=False):
+    n = xs4.shape[0]
+    out = torch.empty((n, 4), dtype=torch.float32, device=xs4.device)
+    xf = torch.empty((n, 3), dtype=torch.float32, device=xs4.device) if want_xfinal else None
+    f = nets.field_struct(offset_enabled=offset_enabled)
+    h = nets.hash_struct()
+    nb = nets.lib.fv_field_workspace_bytes(n, f.precision)
+    work = torch.empty(max(nb, 1), dtype=torch.uint8, device=xs4.device)
+    _lib.check(nets.lib.fv_field_fwd(C.byref(f), C.byref(h), xs4.contiguous().data_ptr(), n, eps_w, out.data_ptr(),
+                                     xf.data_ptr() if xf is not None else None, work.data_ptr(), nb,
+                                     _lib.stream_ptr()), "fv_field_fwd")
+    return out, xf
+
+
+def warp_point(nets: FreeviewModel, x: torch.Tensor, eps_w: float = EPS_W):
+    """(x_final (n,3), likelihood (n)) = skeleton warp + residual offset."""
+    xs, lik, fg = skeleton_warp(nets, x, eps_w)
+    _, xf = _field(nets, torch.cat([xs, lik[:, None]], 1), eps_w, nets.offset_enabled, want_xfinal=True)
+    return xf, lik
+
+
+def query_radiance(nets: FreeviewModel, x_final: torch.Tensor):
+    """(c (n,3), sigma (n)) of canonical points."""
+    n = x_final.shape[0]
+    xs4 = torch.cat([x_final.float(), torch.ones((n, 1), device=x_final.device)], 1)
+    out, _ = _field(nets, xs4, EPS_W, False)
+    return out[:, :3], out[:, 3]
+
+
+def composite(sigma: torch.Tensor, color: torch.Tensor, delta: torch.Tensor, likelihood: torch.Tensor,
+              background, eps_w: float = EPS_W, eps_t: float = 0.0):
+    """(rgb (R,3), alpha (R)) from per-sample sigma/delta/likelihood (R,N) and color (R,N,3)."""
+    r, n = sigma.shape
+    rgbs = torch.cat([color.reshape(r * n, 3), sigma.reshape(r * n, 1)], 1).float().contiguous()
+    rgb = torch.empty((r, 3), dtype=torch.float32, device=sigma.device)
+    alpha = torch.empty(r, dtype=torch.float32, device=sigma.device)
+    bg = (C.c_float * 3)(*background)
+    lib = _lib.load()
+    _lib.check(lib.fv_composite_fwd(rgbs.data_ptr(), delta.float().contiguous().data_ptr(),
+                                    likelihood.float().contiguous().data_ptr(), r, n, bg, eps_w, eps_t,
+                                    rgb.data_ptr(), alpha.data_ptr(), None, _lib.stream_ptr()), "fv_composite_fwd")
+    return rgb, alpha

@@ -1,0 +1,193 @@
+"""Synthetic, seeded stand-ins for the BASELINE.json configurations (no dataset or
+checkpoint is available offline; ZJU-MoCap, SPIN/SMPL and trained weights are absent).
+
+Config 1 ("c1", CPU-runnable PR1): 64x64 fp32 frame, camera at 3 m facing the origin,
+64 uniform samples/ray in the body box [-1,1]^3; 24 joints with rest positions
+~U([-1,1]^3), axis-angle ~N(0, 0.2); weight-volume logits ~U(0,1) (25 x 32^3, channel
+softmax); offset MLP 4x128 on the 72-d pose + 6-band posenc; hash grid 16 x 2,
+T = 2^14, resolution 16 -> 512, table ~U(-1e-4, 1e-4); radiance MLP 2x64; Xavier-uniform
+weights, zero biases.
+Config 2 ("c2"): 512x512, 128 jittered samples, T = 2^19, resolution 16 -> 2048, fp16
+table / weight volume / tensor-core MLPs with fp32 accumulation, 32^3 occupancy grid.
+Config 3 ("c3"): config-2 model trained on 6 random 32x32 patches of a seeded smooth
+512x512 target (foreground = projected body-box ellipsoid), fp16 grid with fp32 master.
+Config 4 ("c4"): 8 poses ~N(0, 0.3), otherwise config 2.
+
+Every tensor comes from its own child of ``np.random.SeedSequence(seed)``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+from typing import List
+
+import numpy as np
+
+from .camera import CameraModel, orbit_camera
+from .skeleton import SMPL24_PARENTS, Pose, Skeleton, motion_basis
+
+PE_BANDS = 6
+POSE_DIM = 72
+OFF_WIDTH = 128
+RAD_WIDTH = 64
+
+
+@dataclass(frozen=True)
+class HashGridConfig:
+    """Hash-grid layout (definition: oracle/encoding.py, SS3)."""
+    n_levels: int = 16
+    n_feat: int = 2
+    log2_T: int = 14
+    base_res: int = 16
+    max_res: int = 512
+
+    @property
+    def table_size(self) -> int:
+        return 1 << self.log2_T
+
+    def resolutions(self) -> List[int]:
+        b = np.exp(np.log(self.max_res / self.base_res) / (self.n_levels - 1))
+        return [int(np.floor(self.base_res * b ** l + 1e-9)) for l in range(self.n_levels)]
+
+    def dense(self) -> List[bool]:
+        return [(r + 1) ** 3 <= self.table_size for r in self.resolutions()]
+
+    def sizes(self) -> List[int]:
+        return [min((r + 1) ** 3, self.table_size) for r in self.resolutions()]
+
+    def offsets(self) -> List[int]:
+        return [int(v) for v in np.concatenate([[0], np.cumsum(self.sizes())[:-1]])]
+
+    @property
+    def n_entries(self) -> int:
+        return int(sum(self.sizes()))
+
+
+@dataclass(frozen=True)
+class SceneConfig:
+    name: str = "c1"
+    width: int = 64
+    height: int = 64
+    n_samples: int = 64
+    jitter: bool = False
+    hash: HashGridConfig = HashGridConfig()
+    half: bool = False              # fp16 table + weight volume + tensor-core MLPs
+    occupancy: bool = False
+    pose_sigma: float = 0.2
+    n_poses: int = 1
+    n_bones: int = 24
+    vol_res: int = 32
+    table_scale: float = 1e-4       # table ~U(-s, s)
+    bias_scale: float = 0.0         # biases ~U(-s, s) (0: Xavier default zero biases)
+    fov_deg: float = 45.0
+    radius: float = 3.0
+    seed: int = 0
+    background: tuple = (0.5, 0.5, 0.5)
+
+
+CONFIGS = {
+    "c1": SceneConfig(),
+    "c2": SceneConfig(name="c2", width=512, height=512, n_samples=128, jitter=True,
+                      hash=HashGridConfig(log2_T=19, max_res=2048), half=True, occupancy=True),
+    "c3": SceneConfig(name="c3", width=512, height=512, n_samples=128, jitter=True,
+                      hash=HashGridConfig(log2_T=19, max_res=2048), half=True),
+    "c4": SceneConfig(name="c4", width=512, height=512, n_samples=128, jitter=True,
+                      hash=HashGridConfig(log2_T=19, max_res=2048), half=True, occupancy=True,
+                      pose_sigma=0.3, n_poses=8),
+}
+
+
+def config(name: str, **overrides) -> SceneConfig:
+    return replace(CONFIGS[name], **overrides)
+
+
+@dataclass
+class Scene:
+    cfg: SceneConfig
+    skeleton: Skeleton
+    poses: List[Pose]
+    vol_logits: np.ndarray          # (25, G, G, G) float32
+    off_w: List[np.ndarray]         # (in, out) float32
+    off_b: List[np.ndarray]
+    rad_w: List[np.ndarray]
+    rad_b: List[np.ndarray]
+    table: np.ndarray               # (entries, 2) float32 (fp16-representable when cfg.half)
+    jitter_seed: int
+    camera: CameraModel
+    obox_min: np.ndarray = field(default_factory=lambda: np.array([-1.0, -1.0, -1.0]))
+    obox_max: np.ndarray = field(default_factory=lambda: np.array([1.0, 1.0, 1.0]))
+    wbox_min: np.ndarray = field(default_factory=lambda: np.array([-1.0, -1.0, -1.0]))
+    wbox_max: np.ndarray = field(default_factory=lambda: np.array([1.0, 1.0, 1.0]))
+
+    def vol(self) -> np.ndarray:
+        """Channel softmax of the logits (ad:711-721), float32; fp16-rounded when cfg.half."""
+        z = self.vol_logits.astype(np.float64)
+        e = np.exp(z - z.max(axis=0, keepdims=True))
+        v = (e / e.sum(axis=0, keepdims=True)).astype(np.float32)
+        return v.astype(np.float16).astype(np.float32) if self.cfg.half else v
+
+
+def _xavier(rng, fan_in, fan_out):
+    lim = np.sqrt(6.0 / (fan_in + fan_out))
+    return rng.uniform(-lim, lim, (fan_in, fan_out)).astype(np.float32)
+
+
+def make_scene(cfg: SceneConfig) -> Scene:
+    ch = np.random.SeedSequence(cfg.seed).spawn(8)
+    rng_sk, rng_pose, rng_vol, rng_off, rng_tab, rng_rad, rng_jit = (np.random.default_rng(c) for c in ch[:7])
+    k = cfg.n_bones
+    parents = np.array(SMPL24_PARENTS[:k]) if k <= 24 else np.concatenate([SMPL24_PARENTS, np.arange(23, k - 1)])
+    rest = rng_sk.uniform(-1.0, 1.0, (k, 3))
+    offs = rest.copy()
+    offs[1:] = rest[1:] - rest[parents[1:]]
+    skel = Skeleton(parent=parents, rest_offset=offs, canonical_angles=np.zeros((k, 3)),
+                    canonical_root=np.zeros(3))
+    poses = [Pose(rng_pose.normal(0.0, cfg.pose_sigma, (k, 3)), np.zeros(3)) for _ in range(cfg.n_poses)]
+    g = cfg.vol_res
+    logits = rng_vol.uniform(0.0, 1.0, (k + 1, g, g, g)).astype(np.float32)
+    d_pe = 3 + 6 * PE_BANDS
+    off_dims = [d_pe + 3 * k, OFF_WIDTH, OFF_WIDTH, OFF_WIDTH, OFF_WIDTH, 3]
+    rad_dims = [cfg.hash.n_levels * cfg.hash.n_feat, RAD_WIDTH, RAD_WIDTH, 4]
+    off_w = [_xavier(rng_off, a, b) for a, b in zip(off_dims[:-1], off_dims[1:])]
+    off_b = [rng_off.uniform(-cfg.bias_scale, cfg.bias_scale, b).astype(np.float32) for b in off_dims[1:]]
+    rad_w = [_xavier(rng_rad, a, b) for a, b in zip(rad_dims[:-1], rad_dims[1:])]
+    rad_b = [rng_rad.uniform(-cfg.bias_scale, cfg.bias_scale, b).astype(np.float32) for b in rad_dims[1:]]
+    table = rng_tab.uniform(-cfg.table_scale, cfg.table_scale, (cfg.hash.n_entries, cfg.hash.n_feat)).astype(np.float32)
+    if cfg.half:  # fp16-representable so the fp32 master and the fp16 copy start identical
+        table = table.astype(np.float16).astype(np.float32)
+        off_w = [w.astype(np.float16).astype(np.float32) for w in off_w]
+        rad_w = [w.astype(np.float16).astype(np.float32) for w in rad_w]
+    cam = orbit_camera((0.0, 0.0, 0.0), 0.0, 0.0, cfg.radius, cfg.fov_deg, cfg.width, cfg.height)
+    return Scene(cfg=cfg, skeleton=skel, poses=poses, vol_logits=logits, off_w=off_w, off_b=off_b, rad_w=rad_w,
+                 rad_b=rad_b, table=table, jitter_seed=int(rng_jit.integers(0, 2 ** 31)), camera=cam)
+
+
+def target_image(scene: Scene, seed: int = 7):
+    """Seeded smooth RGB field inside the projected body-box ellipsoid, background outside
+    (config 3 training target).  Returns (H,W,3) float32 and the (H,W) bool mask."""
+    cfg = scene.cfg
+    rng = np.random.default_rng(np.random.SeedSequence(cfg.seed).spawn(8)[7])
+    h, w = cfg.height, cfg.width
+    yy, xx = np.meshgrid(np.linspace(0, 1, h), np.linspace(0, 1, w), indexing="ij")
+    img = np.zeros((h, w, 3))
+    for c in range(3):
+        for _ in range(4):
+            fx, fy = rng.uniform(0.5, 3.0, 2)
+            ph = rng.uniform(0, 2 * np.pi)
+            img[..., c] += np.sin(2 * np.pi * (fx * xx + fy * yy) + ph)
+    img = 0.5 + 0.12 * img
+    cam = scene.camera
+    kinv = np.linalg.inv(cam.intrinsics)
+    pix = np.stack([xx * 0 + np.arange(w)[None, :] + 0.5, yy * 0 + np.arange(h)[:, None] + 0.5, np.ones((h, w))], -1)
+    d = (pix @ kinv.T) @ cam.rotation
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    o = cam.center
+    # unit sphere inscribed in the [-1,1]^3 body box, scaled to an ellipsoid (0.8, 1.0, 0.6)
+    s = np.array([0.8, 1.0, 0.6])
+    od, dd = o / s, d / s
+    a = np.sum(dd * dd, -1)
+    b = 2 * np.sum(dd * od, -1)
+    cc = np.sum(od * od) - 1.0
+    mask = b * b - 4 * a * cc > 0
+    out = np.where(mask[..., None], np.clip(img, 0, 1), np.asarray(cfg.background)[None, None, :])
+    return out.astype(np.float32), mask

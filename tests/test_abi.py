@@ -1,0 +1,43 @@
+"""The C-ABI library loads without a GPU and exports exactly what include/fv_api.h declares."""
+
+import ctypes
+import os
+import re
+
+from paper_2306_16541_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "fv_api.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fv_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    names = header_functions()
+    assert len(names) >= 20
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_covers_header():
+    assert sorted(_lib.SIGNATURES) == header_functions()
+
+
+def test_struct_layout_and_version_without_gpu():
+    lib = _lib.load()  # checks ctypes struct sizes against sizeof() in C
+    assert lib.fv_version() == 100
+    sizes = (ctypes.c_int64 * 5)()
+    lib.fv_struct_sizes(sizes)
+    assert all(s > 0 for s in sizes)
+
+
+def test_error_codes_map_to_reference_exceptions():
+    import pytest
+    from paper_2306_16541_b200.errors import DimensionError
+    lib = _lib.load()
+    with pytest.raises(DimensionError):
+        _lib.check(lib.fv_linear_fwd(None, None, None, None, -1, 0, 0, 0, None), "fv_linear_fwd")

@@ -1,0 +1,216 @@
+"""CUDA path (through the C ABI) vs the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star): sample counts, skip masks, foreground flags and hash
+indices bit-exact; fp32 paths within 1e-5; fp16 (tensor-core) paths within 1e-3 on
+rendered RGB/alpha.
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import camera as ocam
+from oracle import composite as ocomp
+from oracle import encoding as oenc
+from oracle import pipeline as opipe
+from oracle import warp as owarp
+from oracle.adapter import settings as osettings
+from paper_2306_16541_b200 import _lib
+from paper_2306_16541_b200.model import FreeviewModel
+from paper_2306_16541_b200.render import RenderSettings, Renderer, camera_struct, march_struct
+
+from helpers import blocked_to_ray_major, make, oracle_scene
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _t(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV, dtype)
+
+
+@pytest.fixture(scope="module")
+def c1():
+    sc = make("c1", table_scale=0.5, bias_scale=0.05, background=(0.1, 0.3, 0.8))
+    nets = FreeviewModel(sc)
+    return sc, nets, oracle_scene(sc, nets=nets)
+
+
+@pytest.fixture(scope="module")
+def c2s():
+    # config-2 model (fp16 table/volume/tensor-core MLPs, T=2^19, res 2048) at a 64x64 crop size
+    sc = make("c2", width=64, height=64, table_scale=0.5, bias_scale=0.05, background=(0.1, 0.3, 0.8))
+    nets = FreeviewModel(sc)
+    return sc, nets, oracle_scene(sc, nets=nets)
+
+
+def test_march_counts_positions_skip_bitexact(c1):
+    sc, nets, osc = c1
+    n, r = 64, 64 * 64
+    pix = torch.arange(r, dtype=torch.int32, device=DEV)
+    st = RenderSettings(n_samples=n, jitter=True, seed=1234)
+    rp = (r + 31) // 32 * 32
+    xs = torch.empty((rp * n, 4), device=DEV)
+    delta = torch.empty(rp * n, device=DEV)
+    x = torch.empty((rp * n, 3), device=DEV)
+    cnt = torch.empty(r, dtype=torch.int32, device=DEV)
+    m, cs, w = march_struct(st, pix, None), camera_struct(sc.camera), nets.warp_struct()
+    _lib.check(nets.lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), r, xs.data_ptr(), delta.data_ptr(),
+                                      x.data_ptr(), cnt.data_ptr(), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    cc = ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera)
+    o, d = ocam.rays_f32(cc, np.arange(r), 64)
+    t0, t1, hit = ocam.slab_f32(o, d, osc["obox_min"], osc["obox_max"])
+    t, dl, count = ocam.stratified_f32(t0, t1, hit, np.arange(r), n, True, 1234)
+    xo = ocam.positions_f32(o, d, t)
+    assert np.array_equal(cnt.cpu().numpy(), count)
+    assert hit.sum() > r // 4
+    xg = blocked_to_ray_major(x.cpu().numpy(), r, n)
+    dg = blocked_to_ray_major(delta.cpu().numpy(), r, n)
+    assert np.array_equal(xg[hit], xo[hit])          # bit-exact positions
+    assert np.array_equal(dg[hit], dl[hit])          # bit-exact spacings
+    xsg = blocked_to_ray_major(xs.cpu().numpy(), r, n)
+    wr = owarp.skeleton_warp(xo[hit].reshape(-1, 3), osc["g_r"], osc["g_t"], osc["vol"], osc["wbox_min"],
+                             osc["wbox_max"], 1e-4, np.float32)
+    lg = xsg[hit].reshape(-1, 4)
+    assert np.array_equal(lg[:, 3], wr["L"])         # bit-exact likelihood (=> fg mask)
+    fg = wr["fg"]
+    assert fg.mean() > 0.3
+    assert np.max(np.abs(lg[fg, :3] - wr["x_skel"][fg])) < 1e-5
+
+
+def test_warp_fwd_bitexact_with_outside_points(c1):
+    sc, nets, osc = c1
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1.6, 1.6, (20000, 3)).astype(np.float32)
+    from paper_2306_16541_b200.render import skeleton_warp
+    xs, lik, fg = skeleton_warp(nets, _t(x))
+    wr = owarp.skeleton_warp(x, osc["g_r"], osc["g_t"], osc["vol"], osc["wbox_min"], osc["wbox_max"], 1e-4,
+                             np.float32)
+    assert np.array_equal(lik.cpu().numpy(), wr["L"])
+    assert np.array_equal(fg.cpu().numpy(), wr["fg"])
+    assert 0 < wr["fg"].mean() < 1
+    m = wr["fg"]
+    assert np.max(np.abs(xs.cpu().numpy()[m] - wr["x_skel"][m])) < 1e-5
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_hash_indices_bitexact_and_features(cfg):
+    sc = make(cfg, table_scale=0.5)
+    nets = FreeviewModel(sc)
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-1.2, 1.2, (30000, 3)).astype(np.float32)
+    x[:6] = [[-1, -1, -1], [1, 1, 1], [0, 0, 0], [1, -1, 0.5], [-1.0000001, 0, 0], [0.9999999, 0.5, -0.5]]
+    h = nets.hash_struct()
+    n = len(x)
+    feat = torch.empty((n, 32), device=DEV)
+    idx = torch.empty((n, 16, 8), dtype=torch.int32, device=DEV)
+    _lib.check(nets.lib.fv_hash_fwd(C.byref(h), _t(x).data_ptr(), n, feat.data_ptr(), idx.data_ptr(),
+                                    _lib.stream_ptr()))
+    osc = oracle_scene(sc)
+    cinv = (1.0 / (osc["wbox_max"] - osc["wbox_min"])).astype(np.float32)
+    of, oi = oenc.hash_encode(osc["hash_spec"], x, osc["wbox_min"].astype(np.float32), cinv, osc["table"],
+                              np.float32, return_index=True)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), oi)
+    assert np.max(np.abs(feat.cpu().numpy() - of)) < 1e-6
+
+
+def test_field_fp32_parity(c1):
+    sc, nets, osc = c1
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1.0, 1.0, (5000, 3)).astype(np.float32)
+    wr = owarp.skeleton_warp(x, osc["g_r"], osc["g_t"], osc["vol"], osc["wbox_min"], osc["wbox_max"], 1e-4,
+                             np.float32)
+    xs4 = np.concatenate([wr["x_skel"], wr["L"][:, None]], 1)
+    from paper_2306_16541_b200.render import _field
+    out, xf = _field(nets, _t(xs4), 1e-4, True, want_xfinal=True)
+    of = opipe._field(osc, wr["x_skel"][wr["fg"]], osettings(sc.cfg), np.float32)
+    got = out.cpu().numpy()[wr["fg"]]
+    assert np.max(np.abs(xf.cpu().numpy()[wr["fg"]] - of["x_final"])) < 1e-5
+    assert np.max(np.abs(got[:, :3] - of["c"])) < 1e-5
+    assert np.max(np.abs(got[:, 3] - of["sigma"])) < 1e-5
+    assert np.all(out.cpu().numpy()[~wr["fg"]] == 0)
+
+
+def test_field_tc_fp16_parity(c2s):
+    sc, nets, osc = c2s
+    rng = np.random.default_rng(4)
+    x = rng.uniform(-1.0, 1.0, (20000, 3)).astype(np.float32)
+    wr = owarp.skeleton_warp(x, osc["g_r"], osc["g_t"], osc["vol"], osc["wbox_min"], osc["wbox_max"], 1e-4,
+                             np.float32)
+    xs4 = np.concatenate([wr["x_skel"], wr["L"][:, None]], 1)
+    from paper_2306_16541_b200.render import _field
+    out, xf = _field(nets, _t(xs4), 1e-4, True, want_xfinal=True)
+    of = opipe._field(osc, wr["x_skel"][wr["fg"]], osettings(sc.cfg), np.float32)
+    got = out.cpu().numpy()[wr["fg"]]
+    ex = np.abs(xf.cpu().numpy()[wr["fg"]] - of["x_final"])
+    ec = np.abs(got[:, :3] - of["c"])
+    es = np.abs(got[:, 3] - of["sigma"])
+    print(f"tc field: x_final max {ex.max():.2e} mean {ex.mean():.2e}; c max {ec.max():.2e}; sigma max {es.max():.2e}")
+    assert np.mean(ex) < 2e-3 and np.mean(ec) < 2e-3 and np.mean(es) < 2e-3
+    assert np.all(out.cpu().numpy()[~wr["fg"]] == 0)
+
+
+def _render_both(sc, nets, osc, settings_kw, res=None):
+    cfg = sc.cfg
+    st = RenderSettings.from_config(cfg, seed=77, **settings_kw)
+    rnd = Renderer()
+    img, alpha = rnd.render_image(nets, sc.camera, None, st)
+    torch.cuda.synchronize()
+    cc = ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera)
+    occ = rnd.occ.cpu().numpy().view(np.uint32) if st.occupancy else None
+    ost = osettings(cfg, seed=77, eps_t=st.eps_t, occupancy=occ)
+    ref = opipe.render_rays(osc, cc, np.arange(cfg.width * cfg.height), cfg.width, ost, np.float32)
+    return img.cpu().numpy().reshape(-1, 3), alpha.cpu().numpy().reshape(-1), ref
+
+
+def test_render_c1_fp32_parity(c1):
+    sc, nets, osc = c1
+    rgb, alpha, ref = _render_both(sc, nets, osc, {})
+    assert np.max(np.abs(rgb - ref["rgb"])) < 1e-5
+    assert np.max(np.abs(alpha - ref["alpha"])) < 1e-5
+    assert ref["fg"].mean() > 0.05 and ref["alpha"].max() > 0.1
+
+
+def test_render_c1_early_termination_parity(c1):
+    sc, nets, osc = c1
+    rgb, alpha, ref = _render_both(sc, nets, osc, {"eps_t": 0.2})
+    assert np.max(np.abs(rgb - ref["rgb"])) < 1e-5
+    assert np.max(np.abs(alpha - ref["alpha"])) < 1e-5
+
+
+def test_render_c2_fp16_parity_with_occupancy(c2s):
+    sc, nets, osc = c2s
+    rgb, alpha, ref = _render_both(sc, nets, osc, {})
+    er, ea = np.abs(rgb - ref["rgb"]), np.abs(alpha - ref["alpha"])
+    print(f"c2 render: rgb max {er.max():.2e} mean {er.mean():.2e}; alpha max {ea.max():.2e}")
+    assert er.max() < 1e-3 and ea.max() < 1e-3
+
+
+def test_occupancy_build_matches_oracle(c2s):
+    sc, nets, osc = c2s
+    st = RenderSettings.from_config(sc.cfg, occ_threshold=0.3)
+    rnd = Renderer()
+    bits = rnd.build_occupancy(nets, st).cpu().numpy().view(np.uint32)
+    obits, sig = opipe.occupancy_build(osc, osettings(sc.cfg), 0.3)
+    gb = np.unpackbits(bits.view(np.uint8), bitorder="little")
+    ob = np.unpackbits(obits.view(np.uint8), bitorder="little")
+    near = np.any(np.abs(sig - 0.3) < 5e-3, axis=1)   # cells with a probe within fp16 noise of the threshold
+    assert 0.05 < ob.mean() < 0.95
+    assert np.array_equal(gb[~near], ob[~near])
+
+
+def test_composite_standalone_parity():
+    rng = np.random.default_rng(11)
+    R, N = 3000, 48
+    sig = rng.uniform(0, 4, (R, N)).astype(np.float32)
+    col = rng.uniform(0, 1, (R, N, 3)).astype(np.float32)
+    dl = rng.uniform(0.005, 0.1, (R, N)).astype(np.float32)
+    lik = rng.uniform(0, 2e-4, (R, N)).astype(np.float32)
+    from paper_2306_16541_b200.render import composite
+    rgb, alpha = composite(_t(sig), _t(col), _t(dl), _t(lik), (0.1, 0.2, 0.3), eps_t=0.0)
+    ref = ocomp.composite(sig, col, dl, lik, np.array([0.1, 0.2, 0.3], np.float32), dtype=np.float32)
+    assert np.max(np.abs(rgb.cpu().numpy() - ref["rgb"])) < 1e-6
+    assert np.max(np.abs(alpha.cpu().numpy() - ref["alpha"])) < 1e-6
