@@ -202,13 +202,13 @@ def run_ours(args, rank, world, local_rank):
         nets.set_pose(pose_of(i))
         rnd.render_image(nets, cam, None, st, out_rgb=img, out_alpha=alpha)
 
+    clk = ClockSampler(local_rank)   # started before warm-up so its start-up never lands in a timed step
+    clk.start()
+    time.sleep(0.3)
     for i in range(args.warmup):
+        flush.zero_()
         step(i)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = ClockSampler(local_rank)
-    clk.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
     if world > 1:

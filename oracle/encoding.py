@@ -10,7 +10,9 @@ Hash grid -- PARITY UNPINNED (absent from the reference, SPEC non-goal ``S:139``
 * level ``l`` has vertices ``0..N_l`` per axis; it is dense (``idx = x + y(N+1) + z(N+1)^2``)
   when ``(N_l+1)^3 <= T`` else hashed
   (``idx = (x*1 ^ y*2654435761 ^ z*805459861) mod T``, uint32 arithmetic);
-  level ``l`` occupies ``min((N_l+1)^3, T)`` consecutive table entries;
+  level ``l`` occupies ``min((N_l+1)^3, T)`` consecutive table entries starting at a
+  multiple of 4 (16-byte aligned in fp16, so a cell's two x-corners share one aligned
+  4-entry block 3/4 of the time);
 * a canonical point is normalised ``xn = clamp((x - cmin) * cinv, 0, 1)`` (float32, two
   rounded ops), ``pos = xn * N_l``, ``i0 = min(floor(pos), N_l - 1)``, ``f = pos - i0``;
 * feature ``l`` = trilinear blend of the 8 corner entries accumulated in (a,b,c) order
@@ -92,11 +94,15 @@ class HashGridSpec:
         return [(r + 1) ** 3 <= self.table_size for r in self.resolutions()]
 
     def offsets(self):
-        return np.concatenate([[0], np.cumsum(self.level_sizes())]).astype(np.int64)
+        out, o = [], 0
+        for sz in self.level_sizes():
+            out.append(o)
+            o += (sz + 3) // 4 * 4
+        return np.array(out + [o], dtype=np.int64)
 
     @property
     def n_entries(self) -> int:
-        return int(sum(self.level_sizes()))
+        return int(self.offsets()[-1])
 
     @property
     def out_dim(self) -> int:

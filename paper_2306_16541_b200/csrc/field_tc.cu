@@ -5,17 +5,23 @@
 //   radiance MLP 32->64->64->4(16) + heads c = sigmoid, sigma = softplus(h-1)
 //
 // Design (the B200 restatement of the Fig-4 "fully fused" scheme, fu:1-14, fu:145-179):
-//  * one persistent CTA per SM holds every weight matrix of both MLPs in shared memory
-//    as fp16 UMMA B operands (126 KB, loaded once per CTA);
+//  * two persistent kernels, one CTA per SM each, with the MLP weights resident in shared
+//    memory as fp16 UMMA B operands (loaded once per CTA):
+//      k_offset_tc   posenc + residual MLP (112 KB of weights), pure tensor-core work,
+//                    writes x_final in place of x_skel;
+//      k_radiance_tc hash-grid gathers + radiance MLP + heads (14 KB of weights), so
+//                    ~150 KB of the SM's L1 stays free for the table gathers (profiling
+//                    the single fused kernel showed its 126-230 KB of smem starving L1);
 //  * NWG warpgroups per CTA each own a 128-sample tile: thread t <-> sample row t <->
-//    TMEM lane t.  Activations live in a 32 KB fp16 A-operand buffer that is rewritten
-//    in place layer after layer; accumulators live in TMEM (128 fp32 columns per WG);
+//    TMEM lane t.  Activations live in an fp16 A-operand buffer rewritten in place
+//    layer after layer; accumulators live in TMEM;
 //  * one elected thread per warpgroup issues the tcgen05.mma chain of a layer
 //    (M = 128, N = 16..128, K = 16 per instruction) and commits to an mbarrier; the
 //    128 threads run the epilogue (tcgen05.ld -> bias, ReLU -> fp16 -> smem) which is
 //    the next layer's A operand.  Warpgroups interleave, so one WG's gathers/epilogue
 //    overlap another WG's MMAs.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include "fv_common.cuh"
 #include "fv_internal.h"
 #include "tc_sm100.cuh"
@@ -110,144 +116,121 @@ __device__ __forceinline__ void layer_mma(const uint8_t* A, const uint8_t* Wt, u
 template <int NC>
 __device__ __forceinline__ void epi_relu(uint32_t trow, const float* bias, uint8_t* A, int t) {
 #pragma unroll
-  for (int g = 0; g < NC / 16; ++g) {
-    float v[16];
-    tc::tmem_ld16(trow + g * 16, v);
+  for (int g = 0; g < NC / 16; g += 2) {
+    float v[2][16];
+    tc::tmem_ld16(trow + g * 16, v[0]);
+    tc::tmem_ld16(trow + g * 16 + 16, v[1]);
     tc::tmem_ld_wait();
-    uint32_t w[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      w[j] = tc::pack_half2(fmaxf(v[2 * j] + bias[g * 16 + 2 * j], 0.f), fmaxf(v[2 * j + 1] + bias[g * 16 + 2 * j + 1], 0.f));
-    *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * g)) = make_uint4(w[0], w[1], w[2], w[3]);
-    *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * g + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
+    for (int u = 0; u < 2; ++u) {
+      uint32_t w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        w[j] = tc::pack_half2(fmaxf(v[u][2 * j] + bias[(g + u) * 16 + 2 * j], 0.f),
+                              fmaxf(v[u][2 * j + 1] + bias[(g + u) * 16 + 2 * j + 1], 0.f));
+      *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * (g + u))) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * (g + u) + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
+    }
   }
 }
 
-template <int NWG>
-__global__ void __launch_bounds__(NWG * 128, 1)
-    k_field_tc(fv_field f, fv_hash h, const float4* __restrict__ xs, int64_t n, float eps_w,
-               float4* __restrict__ rgbs, float* __restrict__ xfinal) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bars[NWG];
-  __shared__ uint32_t tmem_base;
-  constexpr uint32_t TCOLS = NWG == 1 ? 128 : (NWG == 2 ? 256 : 512);
 
-  {  // weights + biases (one pass per persistent CTA)
-    const uint4* src = reinterpret_cast<const uint4*>(f.d_tc_pack);
-    uint4* dst = reinterpret_cast<uint4*>(smem);
-    for (int i = threadIdx.x; i < (int)(PK_BYTES / 16); i += blockDim.x) dst[i] = __ldg(src + i);
-    float* b0 = reinterpret_cast<float*>(smem + SM_B0);
-    for (int i = threadIdx.x; i < 128; i += blockDim.x) b0[i] = f.d_off_b0_eff[i];
-  }
-  const int warp = threadIdx.x >> 5;
-  if (warp == 0) tc::tmem_alloc<TCOLS>(&tmem_base);
+// ---- shared prologue: copy [w_begin, w_end) of the pack and `nbias` biases into smem
+template <int NWG, uint32_t TCOLS>
+__device__ __forceinline__ void tc_prologue(const uint8_t* pack, uint32_t w_begin, uint32_t w_end, uint32_t b_begin,
+                                            uint32_t nbias, uint8_t* smem, float* sbias, uint64_t* bars,
+                                            uint32_t* tmem_base) {
+  const uint4* src = reinterpret_cast<const uint4*>(pack + w_begin);
+  uint4* dst = reinterpret_cast<uint4*>(smem);
+  for (int i = threadIdx.x; i < (int)((w_end - w_begin) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+  const float* bsrc = reinterpret_cast<const float*>(pack + PK_WEND) + b_begin;
+  for (int i = threadIdx.x; i < (int)nbias; i += blockDim.x) sbias[i] = bsrc[i];
+  if ((threadIdx.x >> 5) == 0) tc::tmem_alloc<TCOLS>(tmem_base);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NWG; ++i) tc::mbar_init(&bars[i], 1);
     tc::mbar_fence_init();
   }
-  tc::fence_proxy_async();  // weight stores above -> visible to the tensor-core proxy
+}
+
+__device__ __forceinline__ void tc_prologue_sync() {
+  tc::fence_proxy_async();  // weight stores -> visible to the tensor-core proxy
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+}
 
-  const int wg = threadIdx.x >> 7;
-  const int t = threadIdx.x & 127;
-  const uint8_t* sW = smem;
-  const float* sBias = reinterpret_cast<const float*>(smem + PK_WEND);
-  const float* sB0 = reinterpret_cast<const float*>(smem + SM_B0);
-  uint8_t* A = smem + SM_A + wg * A_BYTES;
+// ---- k_offset_tc: xs (x_skel, L) -> out (x_final, L) ------------------------------------
+constexpr uint32_t OF_W = PK_RAD0 - PK_OFF0;             // 114688
+constexpr uint32_t OF_BIAS = OF_W;                       // off b1..b4: 400 floats
+constexpr uint32_t OF_B0 = OF_BIAS + 400 * 4;            // 128 floats
+constexpr uint32_t OF_A = (OF_B0 + 512 + 127) / 128 * 128;
+
+template <int NWG>
+__global__ void __launch_bounds__(NWG * 128, 1)
+    k_offset_tc(fv_field f, const float4* __restrict__ xs, int64_t n, float eps_w, float4* __restrict__ out,
+                float* __restrict__ xfinal) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[NWG];
+  __shared__ uint32_t tmem_base;
+  constexpr uint32_t TCOLS = NWG == 1 ? 128 : (NWG == 2 ? 256 : 512);
+  float* sBias = reinterpret_cast<float*>(smem + OF_BIAS);
+  float* sB0 = reinterpret_cast<float*>(smem + OF_B0);
+  tc_prologue<NWG, TCOLS>(reinterpret_cast<const uint8_t*>(f.d_tc_pack), PK_OFF0, PK_RAD0, BI_OFF1, 400, smem,
+                          sBias, bars, &tmem_base);
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) sB0[i] = f.d_off_b0_eff[i];
+  tc_prologue_sync();
+
+  const int warp = threadIdx.x >> 5, wg = threadIdx.x >> 7, t = threadIdx.x & 127;
+  uint8_t* A = smem + OF_A + wg * A_BYTES;
   const uint32_t tcol = tmem_base + wg * 128;
   const uint32_t trow = tcol + ((uint32_t)((warp & 3) * 32) << 16);
   uint64_t* bar = &bars[wg];
   uint32_t phase = 0;
-
   const int64_t ntiles = (n + 127) / 128;
   for (int64_t tile = (int64_t)blockIdx.x * NWG + wg; tile < ntiles; tile += (int64_t)gridDim.x * NWG) {
     const int64_t s = tile * 128 + t;
     const float4 v = s < n ? xs[s] : make_float4(0.f, 0.f, 0.f, 0.f);
     const bool fg = s < n && v.w > eps_w;
     const float x0 = fg ? v.x : 0.f, x1 = fg ? v.y : 0.f, x2 = fg ? v.z : 0.f;
-    float xr0 = 0.f, xr1 = 0.f, xr2 = 0.f;
-    if (f.offset_enabled) {
-      // posenc -> A chunks 0..5 (39 values + zero pad to 48)
-      {
-        __half pe[48];
-        pe[0] = __float2half_rn(x0); pe[1] = __float2half_rn(x1); pe[2] = __float2half_rn(x2);
-        const float xx[3] = {x0, x1, x2};
+    {  // posenc -> A chunks 0..5 (39 values + zero pad to 48); sin(pi x 2^k) via sincospif
+      __half pe[48];
+      pe[0] = __float2half_rn(x0); pe[1] = __float2half_rn(x1); pe[2] = __float2half_rn(x2);
+      const float xx[3] = {x0, x1, x2};
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          const float wk = k < f.pe_bands ? f.pe_w[k] : 0.f;
+      for (int k = 0; k < 6; ++k) {
+        const float wk = k < f.pe_bands ? f.pe_w[k] : 0.f;
 #pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            float sv, cv;
-            sincospif(xx[j] * (float)(1 << k), &sv, &cv);
-            pe[3 + 6 * k + j] = __float2half_rn(wk * sv);
-            pe[3 + 6 * k + 3 + j] = __float2half_rn(wk * cv);
-          }
+        for (int j = 0; j < 3; ++j) {
+          float sv, cv;
+          sincospif(xx[j] * (float)(1 << k), &sv, &cv);
+          pe[3 + 6 * k + j] = __float2half_rn(wk * sv);
+          pe[3 + 6 * k + 3 + j] = __float2half_rn(wk * cv);
         }
-#pragma unroll
-        for (int j = 39; j < 48; ++j) pe[j] = __float2half_rn(0.f);
-#pragma unroll
-        for (int c = 0; c < 6; ++c)
-          *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = *reinterpret_cast<const uint4*>(pe + 8 * c);
       }
-      layer_mma<48, 128>(A, sW + PK_OFF0, tcol, bar, phase, t, wg);
-      epi_relu<128>(trow, sB0, A, t);
-      layer_mma<128, 128>(A, sW + PK_OFF1, tcol, bar, phase, t, wg);
-      epi_relu<128>(trow, sBias + BI_OFF1, A, t);
-      layer_mma<128, 128>(A, sW + PK_OFF2, tcol, bar, phase, t, wg);
-      epi_relu<128>(trow, sBias + BI_OFF2, A, t);
-      layer_mma<128, 128>(A, sW + PK_OFF3, tcol, bar, phase, t, wg);
-      epi_relu<128>(trow, sBias + BI_OFF3, A, t);
-      layer_mma<128, 16>(A, sW + PK_OFF4, tcol, bar, phase, t, wg);
-      {
-        float o[16];
-        tc::tmem_ld16(trow, o);
-        tc::tmem_ld_wait();
-        xr0 = o[0] + sBias[BI_OFF4 + 0];
-        xr1 = o[1] + sBias[BI_OFF4 + 1];
-        xr2 = o[2] + sBias[BI_OFF4 + 2];
-      }
-    }
-    const float y0 = x0 + xr0, y1 = x1 + xr1, y2 = x2 + xr2;
-    if (xfinal && s < n) {
-      xfinal[3 * s] = fg ? y0 : 0.f; xfinal[3 * s + 1] = fg ? y1 : 0.f; xfinal[3 * s + 2] = fg ? y2 : 0.f;
-    }
-    {  // hash-grid features -> A chunks 0..3
-      float xn[3]; bool msk[3];
-      hash_norm(h, y0, y1, y2, xn, msk);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t w[4];
+      for (int j = 39; j < 48; ++j) pe[j] = __float2half_rn(0.f);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int l = 4 * c + q;
-          float2 fv2 = make_float2(0.f, 0.f);
-          if (l < h.n_levels) {
-            HashCell cell;
-            hash_level_cell(xn, h.res[l], cell);
-            fv2 = hash_level_feat(h, l, cell);
-          }
-          w[q] = tc::pack_half2(fg ? fv2.x : 0.f, fg ? fv2.y : 0.f);
-        }
-        *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = make_uint4(w[0], w[1], w[2], w[3]);
-      }
+      for (int c = 0; c < 6; ++c)
+        *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = *reinterpret_cast<const uint4*>(pe + 8 * c);
     }
-    layer_mma<32, 64>(A, sW + PK_RAD0, tcol, bar, phase, t, wg);
-    epi_relu<64>(trow, sBias + BI_RAD0, A, t);
-    layer_mma<64, 64>(A, sW + PK_RAD1, tcol, bar, phase, t, wg);
-    epi_relu<64>(trow, sBias + BI_RAD1, A, t);
-    layer_mma<64, 16>(A, sW + PK_RAD2, tcol, bar, phase, t, wg);
-    {
-      float o[16];
-      tc::tmem_ld16(trow, o);
-      tc::tmem_ld_wait();
-      if (s < n) {
-        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (fg)
-          r = make_float4(sigmoidf_(o[0] + sBias[BI_RAD2]), sigmoidf_(o[1] + sBias[BI_RAD2 + 1]),
-                          sigmoidf_(o[2] + sBias[BI_RAD2 + 2]), softplusf_(o[3] + sBias[BI_RAD2 + 3] - 1.f));
-        rgbs[s] = r;
+    layer_mma<48, 128>(A, smem + (PK_OFF0 - PK_OFF0), tcol, bar, phase, t, wg);
+    epi_relu<128>(trow, sB0, A, t);
+    layer_mma<128, 128>(A, smem + (PK_OFF1 - PK_OFF0), tcol, bar, phase, t, wg);
+    epi_relu<128>(trow, sBias + (BI_OFF1 - BI_OFF1), A, t);
+    layer_mma<128, 128>(A, smem + (PK_OFF2 - PK_OFF0), tcol, bar, phase, t, wg);
+    epi_relu<128>(trow, sBias + (BI_OFF2 - BI_OFF1), A, t);
+    layer_mma<128, 128>(A, smem + (PK_OFF3 - PK_OFF0), tcol, bar, phase, t, wg);
+    epi_relu<128>(trow, sBias + (BI_OFF3 - BI_OFF1), A, t);
+    layer_mma<128, 16>(A, smem + (PK_OFF4 - PK_OFF0), tcol, bar, phase, t, wg);
+    float o[16];
+    tc::tmem_ld16(trow, o);
+    tc::tmem_ld_wait();
+    if (s < n) {
+      const float* b4 = sBias + (BI_OFF4 - BI_OFF1);
+      const float y0 = x0 + (o[0] + b4[0]), y1 = x1 + (o[1] + b4[1]), y2 = x2 + (o[2] + b4[2]);
+      out[s] = fg ? make_float4(y0, y1, y2, v.w) : make_float4(0.f, 0.f, 0.f, v.w);
+      if (xfinal) {
+        xfinal[3 * s] = fg ? y0 : 0.f; xfinal[3 * s + 1] = fg ? y1 : 0.f; xfinal[3 * s + 2] = fg ? y2 : 0.f;
       }
     }
   }
@@ -256,8 +239,111 @@ __global__ void __launch_bounds__(NWG * 128, 1)
   if (warp == 0) tc::tmem_free<TCOLS>(tmem_base);
 }
 
-constexpr int TC_NWG = 2;
+// ---- k_radiance_tc: (x_final, L) -> (c, sigma) ----------------------------------------
+constexpr uint32_t RA_W = PK_WEND - PK_RAD0;             // 14336
+constexpr uint32_t RA_BIAS = RA_W;                       // rad b0,b1,b2: 144 floats
+constexpr uint32_t RA_A = (RA_BIAS + 144 * 4 + 127) / 128 * 128;
+constexpr uint32_t RA_A_BYTES = 128 * 64 * 2;            // 16 KB per warpgroup
 
+template <int NWG, bool BATCH>
+__global__ void __launch_bounds__(NWG * 128, 1)
+    k_radiance_tc(fv_field f, fv_hash h, const float4* __restrict__ xf, int64_t n, float eps_w,
+                  float4* __restrict__ rgbs) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[NWG];
+  __shared__ uint32_t tmem_base;
+  constexpr uint32_t TCOLS = NWG <= 2 ? 128 : (NWG <= 4 ? 256 : 512);
+  float* sBias = reinterpret_cast<float*>(smem + RA_BIAS);
+  tc_prologue<NWG, TCOLS>(reinterpret_cast<const uint8_t*>(f.d_tc_pack), PK_RAD0, PK_WEND, BI_RAD0, 144, smem,
+                          sBias, bars, &tmem_base);
+  tc_prologue_sync();
+
+  const int warp = threadIdx.x >> 5, wg = threadIdx.x >> 7, t = threadIdx.x & 127;
+  uint8_t* A = smem + RA_A + wg * RA_A_BYTES;
+  const uint32_t tcol = tmem_base + wg * 64;
+  const uint32_t trow = tcol + ((uint32_t)((warp & 3) * 32) << 16);
+  uint64_t* bar = &bars[wg];
+  uint32_t phase = 0;
+  const int64_t ntiles = (n + 127) / 128;
+  for (int64_t tile = (int64_t)blockIdx.x * NWG + wg; tile < ntiles; tile += (int64_t)gridDim.x * NWG) {
+    const int64_t s = tile * 128 + t;
+    const float4 v = s < n ? xf[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool fg = s < n && v.w > eps_w;
+    {  // hash-grid features -> A chunks 0..3
+      float xn[3]; bool msk[3];
+      hash_norm(h, fg ? v.x : 0.f, fg ? v.y : 0.f, fg ? v.z : 0.f, xn, msk);
+      if (BATCH) {
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          float2 fv4[4];
+          hash_4levels(h, 4 * c, xn, fv4);
+          uint32_t w[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) w[q] = tc::pack_half2(fg ? fv4[q].x : 0.f, fg ? fv4[q].y : 0.f);
+          *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t w[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int l = 4 * c + q;
+            float2 fv2 = make_float2(0.f, 0.f);
+            if (l < h.n_levels) {
+              HashCell cell;
+              hash_level_cell(xn, h.res[l], cell);
+              fv2 = hash_level_feat(h, l, cell);
+            }
+            w[q] = tc::pack_half2(fg ? fv2.x : 0.f, fg ? fv2.y : 0.f);
+          }
+          *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }
+    layer_mma<32, 64>(A, smem + (PK_RAD0 - PK_RAD0), tcol, bar, phase, t, wg);
+    epi_relu<64>(trow, sBias + (BI_RAD0 - BI_RAD0), A, t);
+    layer_mma<64, 64>(A, smem + (PK_RAD1 - PK_RAD0), tcol, bar, phase, t, wg);
+    epi_relu<64>(trow, sBias + (BI_RAD1 - BI_RAD0), A, t);
+    layer_mma<64, 16>(A, smem + (PK_RAD2 - PK_RAD0), tcol, bar, phase, t, wg);
+    float o[16];
+    tc::tmem_ld16(trow, o);
+    tc::tmem_ld_wait();
+    if (s < n) {
+      const float* b2 = sBias + (BI_RAD2 - BI_RAD0);
+      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (fg)
+        r = make_float4(sigmoidf_(o[0] + b2[0]), sigmoidf_(o[1] + b2[1]), sigmoidf_(o[2] + b2[2]),
+                        softplusf_(o[3] + b2[3] - 1.f));
+      rgbs[s] = r;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<TCOLS>(tmem_base);
+}
+
+template <int NWG>
+static void launch_offset(const fv_field* f, const float4* xs, int64_t n, float eps_w, float4* out, float* xfinal,
+                          int n_sm, cudaStream_t st) {
+  const size_t smem = OF_A + NWG * A_BYTES;
+  cudaFuncSetAttribute(k_offset_tc<NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t ntiles = (n + 127) / 128;
+  const int grid = (int)std::min<int64_t>((ntiles + NWG - 1) / NWG, n_sm);
+  k_offset_tc<NWG><<<grid, NWG * 128, smem, st>>>(*f, xs, n, eps_w, out, xfinal);
+}
+
+template <int NWG, bool BATCH>
+static void launch_radiance(const fv_field* f, const fv_hash* h, const float4* xf, int64_t n, float eps_w,
+                            float4* rgbs, int n_sm, cudaStream_t st) {
+  const size_t smem = RA_A + NWG * RA_A_BYTES;
+  cudaFuncSetAttribute(k_radiance_tc<NWG, BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t ntiles = (n + 127) / 128;
+  const int grid = (int)std::min<int64_t>((ntiles + NWG - 1) / NWG, n_sm);
+  k_radiance_tc<NWG, BATCH><<<grid, NWG * 128, smem, st>>>(*f, *h, xf, n, eps_w, rgbs);
+}
+
+// x_skel -> x_final (into rgbs as scratch) -> (c, sigma) in place.
 int32_t field_fwd_tc(const fv_field* f, const fv_hash* h, const float4* xs, int64_t n, float eps_w, float4* rgbs,
                      float* xfinal, cudaStream_t st) {
   if (!f->d_tc_pack) return set_error(FV_EDIM, "field tc: d_tc_pack is NULL (call fv_field_pack)");
@@ -268,13 +354,33 @@ int32_t field_fwd_tc(const fv_field* f, const fv_hash* h, const float4* xs, int6
   int dev = 0, n_sm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = SM_A + TC_NWG * A_BYTES;
-  cudaFuncSetAttribute(k_field_tc<TC_NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t ntiles = (n + 127) / 128;
-  const int64_t want = (ntiles + TC_NWG - 1) / TC_NWG;
-  const int grid = (int)std::min<int64_t>(want, n_sm);
-  k_field_tc<TC_NWG><<<grid, TC_NWG * 128, smem, st>>>(*f, *h, xs, n, eps_w, rgbs, xfinal);
-  return check_launch("field_fwd_tc");
+  // tuning knobs (experiments only): FV_OFF_NWG in 1..3, FV_RAD_VARIANT = <1|2|4|8><b|s>
+  static const char* ov = getenv("FV_OFF_NWG");
+  static const char* rv = getenv("FV_RAD_VARIANT");
+  const int onwg = ov ? atoi(ov) : 2;
+  const int rnwg = rv ? rv[0] - '0' : 4;
+  const bool batch = rv ? rv[1] == 'b' : true;
+  const float4* src = xs;
+  if (f->offset_enabled) {
+    if (onwg == 1) launch_offset<1>(f, xs, n, eps_w, rgbs, xfinal, n_sm, st);
+    else if (onwg == 3) launch_offset<3>(f, xs, n, eps_w, rgbs, xfinal, n_sm, st);
+    else launch_offset<2>(f, xs, n, eps_w, rgbs, xfinal, n_sm, st);
+    if (int32_t e = check_launch("k_offset_tc")) return e;
+    src = rgbs;
+  } else if (xfinal) {
+    return set_error(FV_EUNSUPPORTED, "field tc: x_final output needs the residual stage enabled");
+  }
+  switch (rnwg * 2 + (batch ? 1 : 0)) {
+    case 2: launch_radiance<1, false>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
+    case 3: launch_radiance<1, true>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
+    case 4: launch_radiance<2, false>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
+    case 5: launch_radiance<2, true>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
+    case 8: launch_radiance<4, false>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
+    case 16: launch_radiance<8, false>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
+    case 17: launch_radiance<8, true>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
+    default: launch_radiance<4, true>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
+  }
+  return check_launch("k_radiance_tc");
 }
 
 }  // namespace fv

@@ -265,6 +265,49 @@ __device__ __forceinline__ float2 hash_level_feat(const fv_hash& h, int l, const
   return acc;
 }
 
+// Four levels at once: 32 independent gathers in flight per thread before any is consumed
+// (the serial per-level form stalls on long-scoreboard for every level).
+__device__ __forceinline__ void hash_4levels(const fv_hash& h, int l0, const float (&xn)[3], float2 (&out)[4]) {
+  const uint32_t maskT = (1u << h.log2_T) - 1u;
+  uint32_t gidx[32];
+  float f[4][3];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int l = l0 + q < h.n_levels ? l0 + q : h.n_levels - 1;
+    HashCell c;
+    hash_level_cell(xn, h.res[l], c);
+    f[q][0] = c.f[0]; f[q][1] = c.f[1]; f[q][2] = c.f[2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      gidx[q * 8 + k] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + ((k >> 2) & 1),
+                                                  c.i0[1] + ((k >> 1) & 1), c.i0[2] + (k & 1));
+  }
+  float2 v[32];
+  if (h.table_half) {
+    const __half2* t = reinterpret_cast<const __half2*>(h.d_table);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = __half22float2(__ldg(t + gidx[k]));
+  } else {
+    const float2* t = reinterpret_cast<const float2*>(h.d_table);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = __ldg(t + gidx[k]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float wx[2] = {__fsub_rn(1.0f, f[q][0]), f[q][0]};
+    const float wy[2] = {__fsub_rn(1.0f, f[q][1]), f[q][1]};
+    const float wz[2] = {__fsub_rn(1.0f, f[q][2]), f[q][2]};
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float wgt = __fmul_rn(__fmul_rn(wx[(k >> 2) & 1], wy[(k >> 1) & 1]), wz[k & 1]);
+      acc.x = __fadd_rn(acc.x, __fmul_rn(wgt, v[q * 8 + k].x));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(wgt, v[q * 8 + k].y));
+    }
+    out[q] = l0 + q < h.n_levels ? acc : make_float2(0.f, 0.f);
+  }
+}
+
 // ---------------------------------------------------------------- heads
 __device__ __forceinline__ float sigmoidf_(float x) {
   if (x >= 0.f) return 1.f / (1.f + expf(-x));

@@ -56,11 +56,16 @@ class HashGridConfig:
         return [min((r + 1) ** 3, self.table_size) for r in self.resolutions()]
 
     def offsets(self) -> List[int]:
-        return [int(v) for v in np.concatenate([[0], np.cumsum(self.sizes())[:-1]])]
+        """Level start entries, each a multiple of 4 (16-byte aligned fp16 blocks)."""
+        out, o = [], 0
+        for sz in self.sizes():
+            out.append(o)
+            o += (sz + 3) // 4 * 4
+        return out
 
     @property
     def n_entries(self) -> int:
-        return int(sum(self.sizes()))
+        return self.offsets()[-1] + (self.sizes()[-1] + 3) // 4 * 4
 
 
 @dataclass(frozen=True)
