@@ -157,18 +157,46 @@ int32_t fv_field_fwd(const fv_field* field, const fv_hash* hash, const float* d_
 
 /* ---- compositing (ad:815-837) ---------------------------------------------- */
 
-/* rays r (R), N samples each: sigma/color (R*N,4) [rgb, sigma], delta (R*N), lik (R*N)
- * -> rgb (R,3), alpha (R); optional T (R,N+1) for backward. */
+/* rays r (R), N samples each: rgbs (R*N,4) [rgb, sigma], delta (R*N), lik (R*N)
+ * -> rgb (R,3), alpha (R); optional T (R,N+1) for backward.  Sample layout: ray-major
+ * [R][N] (blocked = 0) or the render's ray-block-major layout (blocked = 1). */
 int32_t fv_composite_fwd(const float* d_rgbs, const float* d_delta, const float* d_lik,
-                         int64_t n_rays, int32_t n_samples, const float bg[3], float eps_w,
-                         float eps_t, float* d_rgb, float* d_alpha, float* d_trans,
-                         void* stream);
+                         int32_t lik_stride, int32_t blocked, int64_t n_rays, int32_t n_samples,
+                         const float bg[3], float eps_w, float eps_t, float* d_rgb,
+                         float* d_alpha, float* d_trans, void* stream);
 
 /* Division-free reverse scan: d rgb (R,3), d alpha (R) -> d rgbs (R*N,4) [dc, dsigma]. */
 int32_t fv_composite_bwd(const float* d_rgbs, const float* d_delta, const float* d_lik,
-                         const float* d_trans, int64_t n_rays, int32_t n_samples,
-                         const float bg[3], float eps_w, const float* d_drgb,
-                         const float* d_dalpha, float* d_drgbs, void* stream);
+                         int32_t lik_stride, int32_t blocked, const float* d_trans,
+                         int64_t n_rays, int32_t n_samples, const float bg[3], float eps_w,
+                         const float* d_drgb, const float* d_dalpha, float* d_drgbs,
+                         void* stream);
+
+/* ---- training-step operators ---------------------------------------------------------- */
+
+/* posenc of x_skel (xs (n,4) = [x_skel, L]; zero rows where L <= eps_w) -> (n, 3+6*bands)
+ * with Hann band weights w (ad:574-600); backward accumulates into dx (n,3) (ad:602-609). */
+int32_t fv_posenc_fwd(const float* d_xs, int64_t n, float eps_w, int32_t bands, const float* w,
+                      float* d_pe, void* stream);
+int32_t fv_posenc_bwd(const float* d_xs, int64_t n, float eps_w, int32_t bands, const float* w,
+                      const float* d_dpe, int64_t ld, float* d_dx, void* stream);
+/* x_final = x_skel + x_res on foreground rows; d_xres may be NULL. */
+int32_t fv_xfinal(const float* d_xs, const float* d_xres, int64_t n, float eps_w, float* d_xf,
+                  void* stream);
+/* radiance heads c = sigmoid(h[:3]), sigma = softplus(h[3]-1) and backward. */
+int32_t fv_heads_fwd(const float* d_xs, const float* d_h, int64_t n, float eps_w, float* d_rgbs,
+                     void* stream);
+int32_t fv_heads_bwd(const float* d_xs, const float* d_h, const float* d_drgbs, int64_t n,
+                     float eps_w, float* d_dh, void* stream);
+/* softmax over the channel axis of a (C, V) volume (ad:711-721); bwd accumulates. */
+int32_t fv_softmax0_fwd(const float* d_a, int32_t channels, int64_t voxels, float* d_out,
+                        void* stream);
+int32_t fv_softmax0_bwd(const float* d_out, const float* d_g, int32_t channels, int64_t voxels,
+                        float* d_da, void* stream);
+/* L2 loss over rays (target gathered at pixel ids, or row r when d_pix is NULL):
+ * *d_loss = mean((rgb - t)^2) (device scalar), d_drgb = its gradient. */
+int32_t fv_mse_loss(const float* d_rgb, const float* d_target, const int32_t* d_pix,
+                    int64_t n_rays, float* d_loss, float* d_drgb, void* stream);
 
 /* ---- fused render (the hot path) ------------------------------------------------------ */
 

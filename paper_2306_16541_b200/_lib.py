@@ -75,8 +75,16 @@ SIGNATURES = {
     "fv_offset_bias": (i32, [P(FvField), vp, i32, vp, vp]),
     "fv_field_workspace_bytes": (sz, [i64, i32]),
     "fv_field_fwd": (i32, [P(FvField), P(FvHash), vp, i64, f32, vp, vp, vp, sz, vp]),
-    "fv_composite_fwd": (i32, [vp, vp, vp, i64, i32, P(f32), f32, f32, vp, vp, vp, vp]),
-    "fv_composite_bwd": (i32, [vp, vp, vp, vp, i64, i32, P(f32), f32, vp, vp, vp, vp]),
+    "fv_composite_fwd": (i32, [vp, vp, vp, i32, i32, i64, i32, P(f32), f32, f32, vp, vp, vp, vp]),
+    "fv_composite_bwd": (i32, [vp, vp, vp, i32, i32, vp, i64, i32, P(f32), f32, vp, vp, vp, vp]),
+    "fv_posenc_fwd": (i32, [vp, i64, f32, i32, P(f32), vp, vp]),
+    "fv_posenc_bwd": (i32, [vp, i64, f32, i32, P(f32), vp, i64, vp, vp]),
+    "fv_xfinal": (i32, [vp, vp, i64, f32, vp, vp]),
+    "fv_heads_fwd": (i32, [vp, vp, i64, f32, vp, vp]),
+    "fv_heads_bwd": (i32, [vp, vp, vp, i64, f32, vp, vp]),
+    "fv_softmax0_fwd": (i32, [vp, i32, i64, vp, vp]),
+    "fv_softmax0_bwd": (i32, [vp, vp, i32, i64, vp, vp]),
+    "fv_mse_loss": (i32, [vp, vp, vp, i64, vp, vp, vp]),
     "fv_render_workspace_bytes": (sz, [i64, i32, i32]),
     "fv_march_warp": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), i64, vp, vp, vp, vp, vp]),
     "fv_render_fwd": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), P(FvHash), P(FvField), i64, vp, sz,

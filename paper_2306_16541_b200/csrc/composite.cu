@@ -96,19 +96,22 @@ int32_t composite_bwd(const CompIn& in, const float* trans, int64_t n_rays, int 
 
 using namespace fv;
 
-extern "C" int32_t fv_composite_fwd(const float* d_rgbs, const float* d_delta, const float* d_lik, int64_t n_rays,
-                                    int32_t n_samples, const float bg[3], float eps_w, float eps_t, float* d_rgb,
-                                    float* d_alpha, float* d_trans, void* stream) {
-  if (n_rays < 0 || n_samples < 1 || !bg || eps_w <= 0.f) return set_error(FV_EDIM, "fv_composite_fwd: bad arguments");
-  CompIn in{(const float4*)d_rgbs, d_delta, d_lik, 1, false};
+extern "C" int32_t fv_composite_fwd(const float* d_rgbs, const float* d_delta, const float* d_lik, int32_t lik_stride,
+                                    int32_t blocked, int64_t n_rays, int32_t n_samples, const float bg[3], float eps_w,
+                                    float eps_t, float* d_rgb, float* d_alpha, float* d_trans, void* stream) {
+  if (n_rays < 0 || n_samples < 1 || !bg || eps_w <= 0.f || lik_stride < 1)
+    return set_error(FV_EDIM, "fv_composite_fwd: bad arguments");
+  CompIn in{(const float4*)d_rgbs, d_delta, d_lik, lik_stride, blocked != 0};
   return composite_fwd(in, n_rays, n_samples, bg, eps_w, eps_t, nullptr, d_rgb, d_alpha, d_trans, (cudaStream_t)stream);
 }
 
-extern "C" int32_t fv_composite_bwd(const float* d_rgbs, const float* d_delta, const float* d_lik, const float* d_trans,
-                                    int64_t n_rays, int32_t n_samples, const float bg[3], float eps_w,
-                                    const float* d_drgb, const float* d_dalpha, float* d_drgbs, void* stream) {
-  if (n_rays < 0 || n_samples < 1 || !bg || !d_trans) return set_error(FV_EDIM, "fv_composite_bwd: bad arguments");
-  CompIn in{(const float4*)d_rgbs, d_delta, d_lik, 1, false};
+extern "C" int32_t fv_composite_bwd(const float* d_rgbs, const float* d_delta, const float* d_lik, int32_t lik_stride,
+                                    int32_t blocked, const float* d_trans, int64_t n_rays, int32_t n_samples,
+                                    const float bg[3], float eps_w, const float* d_drgb, const float* d_dalpha,
+                                    float* d_drgbs, void* stream) {
+  if (n_rays < 0 || n_samples < 1 || !bg || !d_trans || lik_stride < 1)
+    return set_error(FV_EDIM, "fv_composite_bwd: bad arguments");
+  CompIn in{(const float4*)d_rgbs, d_delta, d_lik, lik_stride, blocked != 0};
   return composite_bwd(in, d_trans, n_rays, n_samples, bg, eps_w, d_drgb, d_dalpha, (float4*)d_drgbs,
                        (cudaStream_t)stream);
 }

@@ -7,6 +7,7 @@
 #include "../../include/fv_api.h"
 
 namespace fv {
+struct PeW { float w[8]; };
 int32_t set_error(int32_t code, const char* msg);
 int32_t check_launch(const char* where);
 int32_t check_hash(const fv_hash* h);

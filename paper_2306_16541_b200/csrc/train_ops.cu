@@ -1,0 +1,211 @@
+// Per-op kernels of the training step (each mirrors one reference operator and its
+// hand-written backward): posenc (ad:581-611), radiance heads (ad:200-222),
+// softmax0 (ad:711-721), x_final = x_skel + x_res, MSE loss (S:496-504, L2 only).
+#include <cuda_runtime.h>
+#include "fv_common.cuh"
+#include "fv_internal.h"
+
+namespace fv {
+
+// xs (n,4) = [x_skel, L]; rows with L <= eps_w produce zeros.
+__global__ void k_posenc_fwd(const float4* __restrict__ xs, int64_t n, float eps_w, int bands, PeW w,
+                             float* __restrict__ pe) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int D = 3 + 6 * bands;
+  const float4 v = xs[p];
+  float* o = pe + p * D;
+  if (!(v.w > eps_w)) { for (int j = 0; j < D; ++j) o[j] = 0.f; return; }
+  const float x[3] = {v.x, v.y, v.z};
+  o[0] = x[0]; o[1] = x[1]; o[2] = x[2];
+  for (int k = 0; k < bands; ++k) {
+    const float freq = __fmul_rn((float)(1 << k), 3.14159265358979323846f);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      float s, c;
+      sincosf(__fmul_rn(x[j], freq), &s, &c);
+      o[3 + 6 * k + j] = __fmul_rn(w.w[k], s);
+      o[3 + 6 * k + 3 + j] = __fmul_rn(w.w[k], c);
+    }
+  }
+}
+
+// dx[p] += d posenc / d x  (ad:602-609): raw columns + sum_k w_k f_k (gs cos - gc sin)
+__global__ void k_posenc_bwd(const float4* __restrict__ xs, int64_t n, float eps_w, int bands, PeW w,
+                             const float* __restrict__ dpe, int64_t ld, float* __restrict__ dx) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float4 v = xs[p];
+  if (!(v.w > eps_w)) return;
+  const float x[3] = {v.x, v.y, v.z};
+  const float* g = dpe + p * ld;
+  float acc[3] = {g[0], g[1], g[2]};
+  for (int k = 0; k < bands; ++k) {
+    const float freq = (float)(1 << k) * 3.14159265358979323846f;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      float s, c;
+      sincosf(x[j] * freq, &s, &c);
+      acc[j] += w.w[k] * freq * (g[3 + 6 * k + j] * c - g[3 + 6 * k + 3 + j] * s);
+    }
+  }
+  dx[3 * p] += acc[0]; dx[3 * p + 1] += acc[1]; dx[3 * p + 2] += acc[2];
+}
+
+__global__ void k_xfinal(const float4* __restrict__ xs, const float* __restrict__ xres, int64_t n, float eps_w,
+                         float* __restrict__ xf) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float4 v = xs[p];
+  const bool fg = v.w > eps_w;
+  xf[3 * p] = fg ? __fadd_rn(v.x, xres ? xres[3 * p] : 0.f) : 0.f;
+  xf[3 * p + 1] = fg ? __fadd_rn(v.y, xres ? xres[3 * p + 1] : 0.f) : 0.f;
+  xf[3 * p + 2] = fg ? __fadd_rn(v.z, xres ? xres[3 * p + 2] : 0.f) : 0.f;
+}
+
+__global__ void k_heads_fwd(const float4* __restrict__ xs, const float* __restrict__ hd, int64_t n, float eps_w,
+                            float4* __restrict__ rgbs) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  if (!(xs[p].w > eps_w)) { rgbs[p] = make_float4(0.f, 0.f, 0.f, 0.f); return; }
+  const float* h = hd + 4 * p;
+  rgbs[p] = make_float4(sigmoidf_(h[0]), sigmoidf_(h[1]), sigmoidf_(h[2]), softplusf_(h[3] - 1.f));
+}
+
+// dh = [dc * c (1-c), dsigma * sigmoid(h3 - 1)] on foreground rows, 0 elsewhere
+__global__ void k_heads_bwd(const float4* __restrict__ xs, const float* __restrict__ hd,
+                            const float4* __restrict__ drgbs, int64_t n, float eps_w, float* __restrict__ dh) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  float* o = dh + 4 * p;
+  if (!(xs[p].w > eps_w)) { o[0] = o[1] = o[2] = o[3] = 0.f; return; }
+  const float* h = hd + 4 * p;
+  const float4 g = drgbs[p];
+  const float c0 = sigmoidf_(h[0]), c1 = sigmoidf_(h[1]), c2 = sigmoidf_(h[2]);
+  o[0] = g.x * c0 * (1.f - c0);
+  o[1] = g.y * c1 * (1.f - c1);
+  o[2] = g.z * c2 * (1.f - c2);
+  o[3] = g.w * sigmoidf_(h[3] - 1.f);
+}
+
+// softmax over the leading (channel) axis of a (C, V) volume, one thread per voxel
+__global__ void k_softmax0_fwd(const float* __restrict__ a, int C, int64_t V, float* __restrict__ out) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  float m = -INFINITY;
+  for (int c = 0; c < C; ++c) m = fmaxf(m, a[c * V + v]);
+  float s = 0.f;
+  for (int c = 0; c < C; ++c) s += expf(a[c * V + v] - m);
+  const float inv = 1.f / s;
+  for (int c = 0; c < C; ++c) out[c * V + v] = expf(a[c * V + v] - m) * inv;
+}
+
+__global__ void k_softmax0_bwd(const float* __restrict__ out, const float* __restrict__ g, int C, int64_t V,
+                               float* __restrict__ da) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  float dot = 0.f;
+  for (int c = 0; c < C; ++c) dot += g[c * V + v] * out[c * V + v];
+  for (int c = 0; c < C; ++c) da[c * V + v] += out[c * V + v] * (g[c * V + v] - dot);
+}
+
+// loss = mean((rgb - target[pix])^2) over R*3 values; drgb = 2 (rgb - t) / (3R)
+__global__ void k_mse(const float* __restrict__ rgb, const float* __restrict__ target, const int32_t* __restrict__ pix,
+                      int64_t R, float* __restrict__ loss, float* __restrict__ drgb) {
+  __shared__ float red[8];
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  float acc = 0.f;
+  if (r < R) {
+    const int64_t q = pix ? pix[r] : r;
+    const float inv = 1.f / (3.f * (float)R);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float d = rgb[3 * r + c] - target[3 * q + c];
+      acc += d * d;
+      drgb[3 * r + c] = 2.f * d * inv;
+    }
+    acc *= inv;
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    atomicAdd(loss, s);
+  }
+}
+
+static unsigned g1(int64_t n) { return (unsigned)((n + 127) / 128); }
+
+}  // namespace fv
+
+using namespace fv;
+
+extern "C" int32_t fv_posenc_fwd(const float* d_xs, int64_t n, float eps_w, int32_t bands, const float* w,
+                                 float* d_pe, void* stream) {
+  if (n < 0 || bands < 1 || bands > 8 || !w) return set_error(FV_EDIM, "fv_posenc_fwd: bad arguments");
+  if (n == 0) return FV_OK;
+  PeW pw{};
+  for (int i = 0; i < bands; ++i) pw.w[i] = w[i];
+  k_posenc_fwd<<<g1(n), 128, 0, (cudaStream_t)stream>>>((const float4*)d_xs, n, eps_w, bands, pw, d_pe);
+  return check_launch("fv_posenc_fwd");
+}
+
+extern "C" int32_t fv_posenc_bwd(const float* d_xs, int64_t n, float eps_w, int32_t bands, const float* w,
+                                 const float* d_dpe, int64_t ld, float* d_dx, void* stream) {
+  if (n < 0 || bands < 1 || bands > 8 || !w || ld < 3 + 6 * bands) return set_error(FV_EDIM, "fv_posenc_bwd: bad arguments");
+  if (n == 0) return FV_OK;
+  PeW pw{};
+  for (int i = 0; i < bands; ++i) pw.w[i] = w[i];
+  k_posenc_bwd<<<g1(n), 128, 0, (cudaStream_t)stream>>>((const float4*)d_xs, n, eps_w, bands, pw, d_dpe, ld, d_dx);
+  return check_launch("fv_posenc_bwd");
+}
+
+extern "C" int32_t fv_xfinal(const float* d_xs, const float* d_xres, int64_t n, float eps_w, float* d_xf, void* stream) {
+  if (n < 0) return set_error(FV_EDIM, "fv_xfinal: n < 0");
+  if (n == 0) return FV_OK;
+  k_xfinal<<<g1(n), 128, 0, (cudaStream_t)stream>>>((const float4*)d_xs, d_xres, n, eps_w, d_xf);
+  return check_launch("fv_xfinal");
+}
+
+extern "C" int32_t fv_heads_fwd(const float* d_xs, const float* d_h, int64_t n, float eps_w, float* d_rgbs,
+                                void* stream) {
+  if (n < 0) return set_error(FV_EDIM, "fv_heads_fwd: n < 0");
+  if (n == 0) return FV_OK;
+  k_heads_fwd<<<g1(n), 128, 0, (cudaStream_t)stream>>>((const float4*)d_xs, d_h, n, eps_w, (float4*)d_rgbs);
+  return check_launch("fv_heads_fwd");
+}
+
+extern "C" int32_t fv_heads_bwd(const float* d_xs, const float* d_h, const float* d_drgbs, int64_t n, float eps_w,
+                                float* d_dh, void* stream) {
+  if (n < 0) return set_error(FV_EDIM, "fv_heads_bwd: n < 0");
+  if (n == 0) return FV_OK;
+  k_heads_bwd<<<g1(n), 128, 0, (cudaStream_t)stream>>>((const float4*)d_xs, d_h, (const float4*)d_drgbs, n, eps_w, d_dh);
+  return check_launch("fv_heads_bwd");
+}
+
+extern "C" int32_t fv_softmax0_fwd(const float* d_a, int32_t channels, int64_t voxels, float* d_out, void* stream) {
+  if (channels < 1 || voxels < 0) return set_error(FV_EDIM, "fv_softmax0_fwd: bad shape");
+  if (voxels == 0) return FV_OK;
+  k_softmax0_fwd<<<g1(voxels), 128, 0, (cudaStream_t)stream>>>(d_a, channels, voxels, d_out);
+  return check_launch("fv_softmax0_fwd");
+}
+
+extern "C" int32_t fv_softmax0_bwd(const float* d_out, const float* d_g, int32_t channels, int64_t voxels, float* d_da,
+                                   void* stream) {
+  if (channels < 1 || voxels < 0) return set_error(FV_EDIM, "fv_softmax0_bwd: bad shape");
+  if (voxels == 0) return FV_OK;
+  k_softmax0_bwd<<<g1(voxels), 128, 0, (cudaStream_t)stream>>>(d_out, d_g, channels, voxels, d_da);
+  return check_launch("fv_softmax0_bwd");
+}
+
+extern "C" int32_t fv_mse_loss(const float* d_rgb, const float* d_target, const int32_t* d_pix, int64_t n_rays,
+                               float* d_loss, float* d_drgb, void* stream) {
+  if (n_rays < 0) return set_error(FV_EDIM, "fv_mse_loss: n < 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(d_loss, 0, sizeof(float), st);
+  if (n_rays == 0) return FV_OK;
+  k_mse<<<(unsigned)((n_rays + 255) / 256), 256, 0, st>>>(d_rgb, d_target, d_pix, n_rays, d_loss, d_drgb);
+  return check_launch("fv_mse_loss");
+}

@@ -137,10 +137,7 @@ class FreeviewModel:
     def refresh(self, stream=None) -> None:
         """Rebuild every derived device buffer from the fp32 master parameters."""
         st = _lib.stream_ptr(stream)
-        torch.softmax(self.views["vol_logits"], dim=0, out=self.vol)
-        w = self.warp_struct()
-        _lib.check(self.lib.fv_warp_pack(self.vol.data_ptr(), self.n_bones + 1, C.byref(w),
-                                         self.vol_packed.data_ptr(), st), "fv_warp_pack")
+        self._softmax_pack(st)
         if self.half:
             self.table_half.copy_(self.views["table"])
         if self.tc_pack is not None:
@@ -148,6 +145,24 @@ class FreeviewModel:
             _lib.check(self.lib.fv_field_pack(C.byref(f), self.tc_pack.data_ptr(), st), "fv_field_pack")
         if self._pose is not None:
             self._fold_pose(st)
+
+    def refresh_after_step(self, stream=None) -> None:
+        """After an Adam step (which already rewrote the fp16 table copy): W^c, packs, pose fold."""
+        st = _lib.stream_ptr(stream)
+        self._softmax_pack(st)
+        if self.tc_pack is not None:
+            f = self.field_struct()
+            _lib.check(self.lib.fv_field_pack(C.byref(f), self.tc_pack.data_ptr(), st), "fv_field_pack")
+        if self._pose is not None:
+            self._fold_pose(st)
+
+    def _softmax_pack(self, st) -> None:
+        k1, g = self.vol.shape[0], self.vol.shape[1]
+        _lib.check(self.lib.fv_softmax0_fwd(self.views["vol_logits"].data_ptr(), k1, g ** 3, self.vol.data_ptr(), st),
+                   "fv_softmax0_fwd")
+        w = self.warp_struct()
+        _lib.check(self.lib.fv_warp_pack(self.vol.data_ptr(), self.n_bones + 1, C.byref(w),
+                                         self.vol_packed.data_ptr(), st), "fv_warp_pack")
 
     def set_pose(self, pose: Pose, stream=None) -> None:
         """Upload the frame's motion bases G_i and fold the pose into the residual bias."""

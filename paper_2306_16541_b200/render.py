@@ -221,6 +221,6 @@ def composite(sigma: torch.Tensor, color: torch.Tensor, delta: torch.Tensor, lik
     bg = (C.c_float * 3)(*background)
     lib = _lib.load()
     _lib.check(lib.fv_composite_fwd(rgbs.data_ptr(), delta.float().contiguous().data_ptr(),
-                                    likelihood.float().contiguous().data_ptr(), r, n, bg, eps_w, eps_t,
+                                    likelihood.float().contiguous().data_ptr(), 1, 0, r, n, bg, eps_w, eps_t,
                                     rgb.data_ptr(), alpha.data_ptr(), None, _lib.stream_ptr()), "fv_composite_fwd")
     return rgb, alpha

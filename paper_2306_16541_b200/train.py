@@ -1,0 +1,224 @@
+"""Patch-based training step on the sm_100a path (SPEC ``S:468-551``; BASELINE config 3).
+
+One iteration (``S:505-513``): sample G patches of S x S pixels whose window meets the
+mask's dilated bounding box (``S:487-490``), render their rays through the full per-sample
+pipeline keeping every activation, L2 loss against the target (``S:496-504``; the
+perceptual term is off in config 3), backward through compositing, radiance heads and MLP,
+hash-grid scatter, residual MLP, posenc and the skinning-weight volume, then one fused
+Adam step over all parameter blocks (lr 5e-4 for table + radiance MLP, 5e-5 for the
+residual MLP and W^c logits; beta = (0.9, 0.99), ``P:227``).
+
+The reference replays a numpy Tape of per-op closures (``ad:87-150``); here every op of
+that tape is one libfvcuda entry point on the current CUDA stream.  Gradients are fp32;
+the hash table is kept as an fp32 master with the fp16 copy the forward reads rewritten
+by the Adam kernel.  With ``torch.distributed`` initialised (NCCL), the flat gradient
+buffer is all-reduced (mean) between backward and Adam -- the only exchange of the path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .camera import CameraModel
+from .errors import TrainingError
+from .model import FreeviewModel, hann_band_weights
+from .render import RenderSettings, camera_struct, march_struct
+from .scene import PE_BANDS
+
+
+def sample_patches(mask: np.ndarray, n_patches: int, size: int, seed: int, step: int) -> np.ndarray:
+    """Top-left origins (G,2) = (y0, x0) of S x S windows meeting the mask's bounding box
+    dilated by S/2; uniform, deterministic per (seed, step); an empty mask falls
+    back to image-uniform origins."""
+    h, w = mask.shape
+    rng = np.random.default_rng([seed, step])
+    ys, xs = np.nonzero(mask)
+    if len(ys) == 0:
+        y_lo, y_hi, x_lo, x_hi = 0, h - size, 0, w - size
+    else:
+        d = size // 2
+        by0, by1 = max(ys.min() - d, 0), min(ys.max() + d, h - 1)
+        bx0, bx1 = max(xs.min() - d, 0), min(xs.max() + d, w - 1)
+        y_lo, y_hi = max(0, by0 - size + 1), min(h - size, by1)
+        x_lo, x_hi = max(0, bx0 - size + 1), min(w - size, bx1)
+    return np.stack([rng.integers(y_lo, y_hi + 1, n_patches), rng.integers(x_lo, x_hi + 1, n_patches)], axis=1)
+
+
+def patch_pixels(origins: np.ndarray, size: int, width: int) -> np.ndarray:
+    """Linear pixel ids of the patches, each patch row-major (32 rays per row = one ray block)."""
+    yy, xx = np.meshgrid(np.arange(size), np.arange(size), indexing="ij")
+    return np.concatenate([((o[0] + yy) * width + o[1] + xx).reshape(-1) for o in origins]).astype(np.int32)
+
+
+class Trainer:
+    """Owns every activation / gradient buffer of one training step (no allocation per step)."""
+
+    def __init__(self, nets: FreeviewModel, camera: CameraModel, target: np.ndarray, mask: np.ndarray,
+                 settings: RenderSettings, n_patches: int = 6, patch: int = 32, seed: int = 0,
+                 process_group=None):
+        self.nets, self.cam, self.st = nets, camera, settings
+        self.lib = nets.lib
+        self.dev = nets.device
+        self.mask = mask
+        self.n_patches, self.patch, self.seed = n_patches, patch, seed
+        self.pg = process_group
+        self.R = n_patches * patch * patch
+        self.N = settings.n_samples
+        self.S = (self.R + 31) // 32 * 32 * self.N
+        S, dev = self.S, self.dev
+        f32 = dict(device=dev, dtype=torch.float32)
+        self.target = torch.from_numpy(np.ascontiguousarray(target.reshape(-1, 3), np.float32)).to(dev)
+        self.pix = torch.empty(self.R, device=dev, dtype=torch.int32)
+        self.pix_host = torch.empty(self.R, dtype=torch.int32, pin_memory=True)
+        d_pe = 3 + 6 * PE_BANDS
+        self.d_pe = d_pe
+        self.xs = torch.empty((S, 4), **f32)
+        self.delta = torch.empty(S, **f32)
+        self.x = torch.empty((S, 3), **f32)
+        self.pe = torch.empty((S, d_pe), **f32)
+        self.h = [torch.empty((S, 128), **f32) for _ in range(4)]
+        self.xres = torch.empty((S, 3), **f32)
+        self.xf = torch.empty((S, 3), **f32)
+        self.feat = torch.empty((S, 32), **f32)
+        self.r = [torch.empty((S, 64), **f32) for _ in range(2)]
+        self.hd = torch.empty((S, 4), **f32)
+        self.rgbs = torch.empty((S, 4), **f32)
+        self.rgb = torch.empty((self.R, 3), **f32)
+        self.alpha = torch.empty(self.R, **f32)
+        self.trans = torch.empty((self.R, self.N + 1), **f32)
+        self.loss = torch.zeros(1, **f32)
+        self.drgb = torch.empty((self.R, 3), **f32)
+        self.d_rgbs = torch.empty((S, 4), **f32)
+        self.dh = torch.empty((S, 4), **f32)
+        self.g128 = [torch.empty((S, 128), **f32) for _ in range(2)]
+        self.g64 = [torch.empty((S, 64), **f32) for _ in range(2)]
+        self.dfeat = torch.empty((S, 32), **f32)
+        self.dxf = torch.empty((S, 3), **f32)
+        self.dxs = torch.empty((S, 3), **f32)
+        self.dpe = torch.empty((S, d_pe), **f32)
+        self.dvol = torch.empty_like(nets.vol)
+        # optimizer state over the flat master buffer
+        self.grad = torch.zeros_like(nets.flat)
+        self.m = torch.zeros_like(nets.flat)
+        self.v = torch.zeros_like(nets.flat)
+        self.flag = torch.zeros(1, device=dev, dtype=torch.int32)
+        self.t = 0
+        self.gviews = {}
+        for name, (a, b) in nets.block_ranges.items():
+            self.gviews[name] = self.grad[a:b].view(nets.views[name].shape)
+        self.seg_end = (C.c_int64 * 2)(*[int(e) for e, _ in nets.segments])
+        self.seg_lr = (C.c_float * 2)(*[float(lr) for _, lr in nets.segments])
+        self.pe_w = (C.c_float * 8)(*hann_band_weights(PE_BANDS, nets.pe_alpha).tolist())
+        self.bg = (C.c_float * 3)(*settings.background)
+        self.table_elems = nets.views["table"].numel()
+
+    # ------------------------------------------------------------------------------------
+    def _lin(self, x, w, b, y, k, n, act, sp):
+        _lib.check(self.lib.fv_linear_fwd(x.data_ptr(), w.data_ptr(), b.data_ptr() if b is not None else None,
+                                          y.data_ptr(), self.S, k, n, act, sp), "fv_linear_fwd")
+
+    def _lin_bwd(self, x, w, y, dy, dx, dw, db, k, n, act, sp):
+        _lib.check(self.lib.fv_linear_bwd(x.data_ptr(), w.data_ptr(), y.data_ptr(), dy.data_ptr(),
+                                          dx.data_ptr() if dx is not None else None, dw.data_ptr(),
+                                          db.data_ptr(), self.S, k, n, act, sp), "fv_linear_bwd")
+
+    def forward(self, pix_np: Optional[np.ndarray] = None, step: int = 0):
+        nets, lib, S = self.nets, self.lib, self.S
+        sp = _lib.stream_ptr()
+        if pix_np is None:
+            pix_np = patch_pixels(sample_patches(self.mask, self.n_patches, self.patch, self.seed, step),
+                                  self.patch, self.cam.width)
+        self.pix_host.numpy()[:] = pix_np
+        self.pix.copy_(self.pix_host, non_blocking=True)
+        m, cs, w = march_struct(self.st, self.pix, None), camera_struct(self.cam), nets.warp_struct()
+        h, eps = nets.hash_struct(), self.st.eps_w
+        _lib.check(lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), self.R, self.xs.data_ptr(),
+                                     self.delta.data_ptr(), self.x.data_ptr(), None, sp), "fv_march_warp")
+        V = nets.views
+        _lib.check(lib.fv_posenc_fwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.pe.data_ptr(), sp))
+        self._lin(self.pe, V["off_w0"], nets.b0_eff, self.h[0], self.d_pe, 128, 1, sp)
+        for i in range(1, 4):
+            self._lin(self.h[i - 1], V[f"off_w{i}"], V[f"off_b{i}"], self.h[i], 128, 128, 1, sp)
+        self._lin(self.h[3], V["off_w4"], V["off_b4"], self.xres, 128, 3, 0, sp)
+        _lib.check(lib.fv_xfinal(self.xs.data_ptr(), self.xres.data_ptr(), S, eps, self.xf.data_ptr(), sp))
+        _lib.check(lib.fv_hash_fwd(C.byref(h), self.xf.data_ptr(), S, self.feat.data_ptr(), None, sp), "fv_hash_fwd")
+        self._lin(self.feat, V["rad_w0"], V["rad_b0"], self.r[0], 32, 64, 1, sp)
+        self._lin(self.r[0], V["rad_w1"], V["rad_b1"], self.r[1], 64, 64, 1, sp)
+        self._lin(self.r[1], V["rad_w2"], V["rad_b2"], self.hd, 64, 4, 0, sp)
+        _lib.check(lib.fv_heads_fwd(self.xs.data_ptr(), self.hd.data_ptr(), S, eps, self.rgbs.data_ptr(), sp))
+        _lib.check(lib.fv_composite_fwd(self.rgbs.data_ptr(), self.delta.data_ptr(), self.xs[:, 3:].data_ptr(), 4, 1,
+                                        self.R, self.N, self.bg, eps, 0.0, self.rgb.data_ptr(), self.alpha.data_ptr(),
+                                        self.trans.data_ptr(), sp), "fv_composite_fwd")
+        _lib.check(lib.fv_mse_loss(self.rgb.data_ptr(), self.target.data_ptr(), self.pix.data_ptr(), self.R,
+                                   self.loss.data_ptr(), self.drgb.data_ptr(), sp), "fv_mse_loss")
+        return self.loss
+
+    def backward(self):
+        nets, lib, S, V, G = self.nets, self.lib, self.S, self.nets.views, self.gviews
+        sp = _lib.stream_ptr()
+        eps = self.st.eps_w
+        self.grad.zero_()
+        self.dvol.zero_()
+        _lib.check(lib.fv_composite_bwd(self.rgbs.data_ptr(), self.delta.data_ptr(), self.xs[:, 3:].data_ptr(), 4, 1,
+                                        self.trans.data_ptr(), self.R, self.N, self.bg, eps, self.drgb.data_ptr(),
+                                        None, self.d_rgbs.data_ptr(), sp), "fv_composite_bwd")
+        _lib.check(lib.fv_heads_bwd(self.xs.data_ptr(), self.hd.data_ptr(), self.d_rgbs.data_ptr(), S, eps,
+                                    self.dh.data_ptr(), sp))
+        self._lin_bwd(self.r[1], V["rad_w2"], self.hd, self.dh, self.g64[0], G["rad_w2"], G["rad_b2"], 64, 4, 0, sp)
+        self._lin_bwd(self.r[0], V["rad_w1"], self.r[1], self.g64[0], self.g64[1], G["rad_w1"], G["rad_b1"], 64, 64, 1, sp)
+        self._lin_bwd(self.feat, V["rad_w0"], self.r[0], self.g64[1], self.dfeat, G["rad_w0"], G["rad_b0"], 32, 64, 1, sp)
+        h = nets.hash_struct()
+        _lib.check(lib.fv_hash_bwd(C.byref(h), self.xf.data_ptr(), S, self.dfeat.data_ptr(), G["table"].data_ptr(),
+                                   self.dxf.data_ptr(), sp), "fv_hash_bwd")
+        self._lin_bwd(self.h[3], V["off_w4"], self.xres, self.dxf, self.g128[0], G["off_w4"], G["off_b4"], 128, 3, 0, sp)
+        self._lin_bwd(self.h[2], V["off_w3"], self.h[3], self.g128[0], self.g128[1], G["off_w3"], G["off_b3"], 128, 128, 1, sp)
+        self._lin_bwd(self.h[1], V["off_w2"], self.h[2], self.g128[1], self.g128[0], G["off_w2"], G["off_b2"], 128, 128, 1, sp)
+        self._lin_bwd(self.h[0], V["off_w1"], self.h[1], self.g128[0], self.g128[1], G["off_w1"], G["off_b1"], 128, 128, 1, sp)
+        self._lin_bwd(self.pe, V["off_w0"], self.h[0], self.g128[1], self.dpe, G["off_w0"], G["off_b0"], self.d_pe, 128, 1, sp)
+        # the folded pose rows of W0: dW0[D:, :] = pose (outer) d b0_eff  (b0_eff = b0 + pose @ W0[D:])
+        G["off_w0"][self.d_pe:].addr_(nets.pose_dev, G["off_b0"])
+        self.dxs.copy_(self.dxf)
+        _lib.check(lib.fv_posenc_bwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.dpe.data_ptr(), self.d_pe,
+                                     self.dxs.data_ptr(), sp))
+        w = nets.warp_struct()
+        _lib.check(lib.fv_warp_bwd(C.byref(w), eps, self.x.data_ptr(), S, self.dxs.data_ptr(), self.dvol.data_ptr(), sp),
+                   "fv_warp_bwd")
+        k1, g = self.dvol.shape[0], self.dvol.shape[1]
+        _lib.check(lib.fv_softmax0_bwd(nets.vol.data_ptr(), self.dvol.data_ptr(), k1, g ** 3,
+                                       G["vol_logits"].data_ptr(), sp))
+
+    def allreduce(self):
+        import torch.distributed as dist
+        if self.pg is not None or (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+            dist.all_reduce(self.grad, op=dist.ReduceOp.SUM, group=self.pg)
+            self.grad.mul_(1.0 / dist.get_world_size(self.pg))
+
+    def optimizer_step(self):
+        nets = self.nets
+        self.t += 1
+        half = nets.table_half
+        _lib.check(self.lib.fv_adam_step(nets.flat.data_ptr(), self.grad.data_ptr(), self.m.data_ptr(),
+                                         self.v.data_ptr(), nets.n_params, self.seg_end, self.seg_lr, 2, self.t,
+                                         0.9, 0.99, 1e-8, half.data_ptr() if half is not None else None, 0,
+                                         self.table_elems if half is not None else 0, self.flag.data_ptr(),
+                                         _lib.stream_ptr()), "fv_adam_step")
+        nets.refresh_after_step()
+
+    def check_finite(self):
+        """Raise TrainingError naming the block if the last Adam pass saw a non-finite gradient."""
+        f = int(self.flag.item())
+        if f:
+            names = ["table / radiance MLP (lr_nerf)", "residual MLP / weight volume (lr_other)"]
+            raise TrainingError(f"non-finite gradient in parameter block '{names[f - 1]}'")
+
+    def step(self, step: int):
+        loss = self.forward(step=step)
+        self.backward()
+        self.allreduce()
+        self.optimizer_step()
+        return loss

@@ -27,8 +27,13 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
+_KEEP = []  # device copies stay referenced: a raw data_ptr() of a dropped temporary may be reused
+
+
 def _t(a, dtype=torch.float32):
-    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV, dtype)
+    t = torch.from_numpy(np.ascontiguousarray(a)).to(DEV, dtype)
+    _KEEP.append(t)
+    return t
 
 
 @pytest.fixture(scope="module")
