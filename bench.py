@@ -40,7 +40,8 @@ def parse():
     p.add_argument("--no-occupancy", action="store_true")
     p.add_argument("--cpu-tiles", type=int, default=2, help="64x64 tiles per CPU-baseline sample")
     p.add_argument("--skip-cpu-baseline", action="store_true")
-    p.add_argument("--profile-stages", action="store_true", default=True)
+    p.add_argument("--no-train", action="store_true", help="skip the config-3 training-step measurement")
+    p.add_argument("--train-steps", type=int, default=20)
     return p.parse_args()
 
 
@@ -173,6 +174,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2306_16541_b200 import scene as psc
     from paper_2306_16541_b200.model import FreeviewModel
     from paper_2306_16541_b200.render import RenderSettings, Renderer, camera_struct, march_struct
+    from paper_2306_16541_b200 import shard
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -194,7 +196,7 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
 
     def pose_of(step):
-        return sc.poses[(rank + step * world) % len(sc.poses)]
+        return sc.poses[shard.frame_of(rank, world, step, len(sc.poses))]
 
     launches_per_step = 3 + (3 if occ_on else 0) + 1  # march, field, composite (+ occ points/field/bits) + bias fold
 
@@ -260,24 +262,11 @@ def run_ours(args, rank, world, local_rank):
     # ---- per-stage device times (same inputs, separate pass, CUDA events on this stream)
     stages = stage_times(nets, rnd, cam, st, dev, occ_on, reps=max(3, min(args.steps, 10)))
     n_samples_launch = ((n_rays + 31) // 32 * 32) * cfg.n_samples
-    flop_per_sample = 121856   # offset MLP 109,056 (pose folded) + radiance 12,800
-    warp_bytes = 412 if cfg.half else 796  # SURVEY SS8d warp fwd, fp16 / fp32 volume
-    field_ms = stages["field"]
-    field_tflops = n_samples_launch * flop_per_sample / (field_ms * 1e-3) / 1e12
-    march_gbs = n_samples_launch * warp_bytes / (stages["march_warp"] * 1e-3) / 1e9
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0}
-    dominant = max(("field", "march_warp", "composite"), key=lambda k: stages[k])
-    if dominant == "march_warp":
-        roof = {"kernel": "k_march_warp", "bound": "hbm", "achieved": march_gbs, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": march_gbs / peaks["hbm_gbs"], "traffic": None,
-                "algorithmic": f"{warp_bytes} B/sample x {n_samples_launch} samples/launch"}
-    else:
-        pk = peaks.get("bf16_tflops_sustained", 1394.7)
-        roof = {"kernel": "k_field_tc" if cfg.half else "field_fp32", "bound": "tensor", "achieved": field_tflops,
-                "peak": pk, "unit": "TFLOP/s", "frac": field_tflops / pk, "traffic": None,
-                "algorithmic": f"{flop_per_sample} FLOP/sample x {n_samples_launch} samples/launch"}
-    roof["peak_source"] = "MEASURED_PEAKS.json (sustained)" if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else "fallback"
+    roofs = stage_rooflines(stages, cfg, n_samples_launch)
+    dominant = max(roofs, key=lambda k: stages.get(k, 0.0))
+    roof = dict(roofs[dominant])
+
+    train = None if args.no_train else train_throughput(args, rank, world, dev)
 
     cpu = None
     if rank == 0 and not args.skip_cpu_baseline:
@@ -297,12 +286,101 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": world * n_rays / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "frames_per_s": world / (e2e_ms / 1000.0)},
             "gpu_launches": launches_per_step * args.steps,
+            "train": train,
             "stages_ms": stages,
             "roofline": roof,
+            "stage_rooflines": roofs,
             "cpu_baseline": cpu,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+
+
+# algorithmic units (SS4): bytes or FLOPs per sample of each kernel
+KERNEL_UNITS = {
+    "march_warp": ("k_march_warp", "hbm", "24 bones x 16 B corner-packed fp16 gathers + 28 B in/out = 412 B/sample", 412.0),
+    "offset": ("k_offset_tc", "tensor", "residual MLP 109,056 FLOP/sample (pose term folded into a per-frame bias)", 109056.0),
+    "radiance": ("k_radiance_tc", "hbm", "hash gathers 16 levels x 8 corners x 4 B = 512 B + 32 B in/out = 544 B/sample", 544.0),
+    "composite": ("k_composite_fwd", "hbm", "per sample 16 B [c,sigma] + 4 B delta + 4 B L (+16 B/ray out) = 24 B/sample", 24.0),
+}
+
+
+def stage_rooflines(stages, cfg, n_samples):
+    """Per-kernel roofline from the live CUDA-event stage times; peaks from MEASURED_PEAKS.json."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(path)) if os.path.exists(path) else {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0}
+    src = "MEASURED_PEAKS.json" if os.path.exists(path) else "fallback (B200_PROFILING.md)"
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    out = {}
+    for key, (kname, bound, algo, unit) in KERNEL_UNITS.items():
+        if key not in stages or stages[key] <= 0:
+            continue
+        sec = stages[key] * 1e-3
+        if bound == "tensor":
+            ach, pk, u = n_samples * unit / sec / 1e12, peaks.get("bf16_tflops_sustained", 1394.7), "TFLOP/s"
+            psrc = src + " bf16_tflops_sustained (fp16 MMA assumed equal)"
+        else:
+            if key == "march_warp" and not cfg.half:
+                unit = 796.0
+            ach, pk, u = n_samples * unit / sec / 1e9, peaks["hbm_gbs"], "GB/s"
+            psrc = src + " hbm_gbs"
+        tr = traffic.get(kname)
+        out[key] = {"kernel": kname, "bound": bound, "achieved": ach, "peak": pk, "unit": u, "frac": ach / pk,
+                    "traffic": tr, "ms": stages[key], "algorithmic": algo, "peak_source": psrc}
+    return out
+
+
+def train_throughput(args, rank, world, dev):
+    """Config 3: one iteration = 6 random 32x32 patches x 128 samples, forward + full backward
+    + (NCCL all-reduce of the 52 MB gradient when N > 1) + fused Adam.  Data-parallel: every
+    rank trains on its own patches; iters/s is the job's step rate (max step time over ranks)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2306_16541_b200 import scene as psc
+    from paper_2306_16541_b200.model import FreeviewModel
+    from paper_2306_16541_b200.render import RenderSettings
+    from paper_2306_16541_b200.train import Trainer
+    sc = psc.make_scene(psc.config("c3"))
+    nets = FreeviewModel(sc, device=str(dev))
+    if world > 1:
+        dist.broadcast(nets.flat, src=0)
+        nets.refresh()
+    target, mask = psc.target_image(sc)
+    st = RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed)
+    tr = Trainer(nets, sc.camera, target, mask, st, n_patches=6, patch=32, seed=1000 + rank)
+    for i in range(3):
+        tr.step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
+    a.record(stream)
+    for i in range(args.train_steps):
+        tr.step(3 + i)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.train_steps
+    # e2e: host loss read-back every step (patch ids go host->device inside forward)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.train_steps):
+        float(tr.step(100 + i).item())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.train_steps
+    tr.check_finite()
+    if world > 1:
+        t = torch.tensor([ms, e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = float(t[0]), float(t[1])
+    return {"metric": "train_iters_per_s", "value": 1000.0 / ms, "unit": "it/s", "ms_per_iter": ms,
+            "e2e_iters_per_s": 1000.0 / e2e_ms, "rays_per_iter_per_gpu": tr.R,
+            "samples_per_iter_per_gpu": tr.S, "n_params": nets.n_params,
+            "workload": "c3: 6 x 32x32 patches of a 512^2 target, 128 samples/ray, fwd + full bwd + Adam"
+                        + (f", NCCL all-reduce over {world} GPUs" if world > 1 else ""),
+            "final_loss": float(tr.loss.item())}
 
 
 def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5):
@@ -350,6 +428,14 @@ def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5):
                                                          work.data_ptr(), wb, rgb.data_ptr(), alpha.data_ptr(), None, sp)))
     out["render_total"] = total
     out["composite"] = max(total - out["march_warp"] - out["field"], 0.0)
+    if f.precision == 1:  # time the two tensor-core kernels separately (k_offset_tc, k_radiance_tc)
+        xf = torch.empty((S, 4), device=dev)
+        f_rad = nets.field_struct(offset_enabled=False)
+        out["offset"] = timeit(lambda: _lib.check(lib.fv_residual_offset(C.byref(f), xs.data_ptr(), S, st.eps_w,
+                                                                         xf.data_ptr(), sp)))
+        out["radiance"] = timeit(lambda: _lib.check(lib.fv_field_fwd(C.byref(f_rad), C.byref(h), xf.data_ptr(), S,
+                                                                     st.eps_w, rgbs.data_ptr(), None, fw.data_ptr(),
+                                                                     nb, sp)))
     if occ_on:
         out["occupancy_build"] = timeit(lambda: rnd.build_occupancy(nets, st))
     out["fg_fraction"] = float((xs[:, 3] > st.eps_w).float().mean().item())

@@ -151,6 +151,10 @@ int32_t fv_offset_bias(const fv_field* field, const float* d_pose, int32_t n_pos
  * S:346-358 (residual offset on posenc) + hash grid + S:419-427 (radiance heads).
  * Workspace: fv_field_workspace_bytes(n, precision) bytes (0 for the tcgen05 path). */
 size_t fv_field_workspace_bytes(int64_t n, int32_t precision);
+/* Residual stage alone (tensor-core path): xs (n,4) [x_skel, L] -> out (n,4) [x_final, L].
+ * query_radiance alone is fv_field_fwd with offset_enabled = 0. */
+int32_t fv_residual_offset(const fv_field* field, const float* d_xs, int64_t n, float eps_w,
+                           float* d_out, void* stream);
 int32_t fv_field_fwd(const fv_field* field, const fv_hash* hash, const float* d_xs, int64_t n,
                      float eps_w, float* d_rgbs, float* d_xfinal, void* d_work, size_t work_bytes,
                      void* stream);

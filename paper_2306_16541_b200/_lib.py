@@ -74,6 +74,7 @@ SIGNATURES = {
     "fv_field_pack": (i32, [P(FvField), vp, vp]),
     "fv_offset_bias": (i32, [P(FvField), vp, i32, vp, vp]),
     "fv_field_workspace_bytes": (sz, [i64, i32]),
+    "fv_residual_offset": (i32, [P(FvField), vp, i64, f32, vp, vp]),
     "fv_field_fwd": (i32, [P(FvField), P(FvHash), vp, i64, f32, vp, vp, vp, sz, vp]),
     "fv_composite_fwd": (i32, [vp, vp, vp, i32, i32, i64, i32, P(f32), f32, f32, vp, vp, vp, vp]),
     "fv_composite_bwd": (i32, [vp, vp, vp, i32, i32, vp, i64, i32, P(f32), f32, vp, vp, vp, vp]),

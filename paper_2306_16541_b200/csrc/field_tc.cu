@@ -389,6 +389,21 @@ using namespace fv;
 
 extern "C" size_t fv_field_pack_bytes(void) { return PK_BYTES; }
 
+// residual_offset + warp_point composition on the tensor cores:
+// xs (n,4) = [x_skel, L] -> out (n,4) = [x_final, L]  (one k_offset_tc launch)
+extern "C" int32_t fv_residual_offset(const fv_field* field, const float* d_xs, int64_t n, float eps_w, float* d_out,
+                                      void* stream) {
+  if (!field || n < 0) return set_error(FV_EDIM, "fv_residual_offset: bad arguments");
+  if (field->precision != 1 || !field->d_tc_pack || !field->d_off_b0_eff)
+    return set_error(FV_EUNSUPPORTED, "fv_residual_offset: tensor-core path only (precision 1, packed weights)");
+  if (n == 0) return FV_OK;
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  launch_offset<2>(field, (const float4*)d_xs, n, eps_w, (float4*)d_out, nullptr, n_sm, (cudaStream_t)stream);
+  return check_launch("fv_residual_offset");
+}
+
 extern "C" int32_t fv_field_pack(const fv_field* field, void* d_tc_pack, void* stream) {
   if (!field || !d_tc_pack) return set_error(FV_EDIM, "fv_field_pack: null argument");
   if (field->pe_bands < 1 || field->pe_bands > 6) return set_error(FV_EUNSUPPORTED, "fv_field_pack: 1..6 PE bands");

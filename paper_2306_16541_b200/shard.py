@@ -1,0 +1,57 @@
+"""How the path is spread over the GPUs of one node.
+
+Rays are independent, so inference needs no data-path collective: each rank renders
+whole frames (config 4) or interleaved image tiles (config 5 style); weights are
+broadcast once.  Training is data-parallel: every rank renders its own patches and the
+flat fp32 gradient is all-reduced (mean) before Adam -- the path's only exchange.
+All functions work for any torch.distributed backend (NCCL on B200, gloo in CPU tests).
+"""
+
+from __future__ import annotations
+
+from typing import List, Optional
+
+import torch
+
+
+def frame_of(rank: int, world: int, step: int, n_frames: int) -> int:
+    """Frame rendered by `rank` at `step`: round-robin so a round of `world` steps covers
+    consecutive frames exactly once across ranks."""
+    return (rank + step * world) % n_frames
+
+
+def frames_for_rank(rank: int, world: int, n_frames: int) -> List[int]:
+    """Static partition of `n_frames` frames (config 4: 8 poses over 1/2/4/8 GPUs)."""
+    return list(range(rank, n_frames, world))
+
+
+def tiles_for_rank(rank: int, world: int, n_tiles: int) -> List[int]:
+    """Interleaved image-tile assignment (uneven subject coverage balances out)."""
+    return list(range(rank, n_tiles, world))
+
+
+def broadcast_params(flat: torch.Tensor, src: int = 0, group=None) -> None:
+    """Identical weights on every rank: one broadcast of the flat master buffer."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.broadcast(flat, src=src, group=group)
+
+
+def allreduce_mean(grad: torch.Tensor, group=None) -> None:
+    """Data-parallel gradient exchange: sum over ranks, divide by the world size."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        n = dist.get_world_size(group)
+        if n > 1:
+            dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
+            grad.mul_(1.0 / n)
+
+
+def max_over_ranks(value: float, device: Optional[torch.device] = None, group=None) -> float:
+    """Job time = slowest rank (bench timing rule)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return float(value)
+    t = torch.tensor([float(value)], device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

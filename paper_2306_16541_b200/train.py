@@ -29,6 +29,7 @@ from .errors import TrainingError
 from .model import FreeviewModel, hann_band_weights
 from .render import RenderSettings, camera_struct, march_struct
 from .scene import PE_BANDS
+from .shard import allreduce_mean
 
 
 def sample_patches(mask: np.ndarray, n_patches: int, size: int, seed: int, step: int) -> np.ndarray:
@@ -193,10 +194,7 @@ class Trainer:
                                        G["vol_logits"].data_ptr(), sp))
 
     def allreduce(self):
-        import torch.distributed as dist
-        if self.pg is not None or (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
-            dist.all_reduce(self.grad, op=dist.ReduceOp.SUM, group=self.pg)
-            self.grad.mul_(1.0 / dist.get_world_size(self.pg))
+        allreduce_mean(self.grad, self.pg)
 
     def optimizer_step(self):
         nets = self.nets

@@ -1,0 +1,107 @@
+"""Multi-rank host logic on CPU: world size 2 over gloo (127.0.0.1)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2306_16541_b200 import shard
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, fn, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, fn(rank, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(fn, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def _allreduce(rank, world):
+    g = torch.full((1000,), float(rank + 1))
+    g[rank] = 100.0
+    shard.allreduce_mean(g)
+    return g.numpy()
+
+
+def _broadcast(rank, world):
+    flat = torch.arange(10, dtype=torch.float32) * (rank + 1)
+    shard.broadcast_params(flat)
+    return flat.numpy()
+
+
+def _maxtime(rank, world):
+    return shard.max_over_ranks(1.0 + rank)
+
+
+def _trainer_allreduce(rank, world):
+    # the Trainer's exchange on its flat gradient buffer (CPU tensor stands in for CUDA)
+    from paper_2306_16541_b200.train import Trainer
+    class T:  # minimal stand-in with the attributes Trainer.allreduce uses
+        pg = None
+        grad = torch.full((17,), float(rank * 2 + 1))
+    Trainer.allreduce(T)
+    return T.grad.numpy()
+
+
+def test_allreduce_mean_world2():
+    out = _run(_allreduce)
+    want = np.full(1000, 1.5)
+    want[0] = (100.0 + 2.0) / 2
+    want[1] = (1.0 + 100.0) / 2
+    for r in (0, 1):
+        assert np.allclose(out[r], want)
+
+
+def test_broadcast_world2():
+    out = _run(_broadcast)
+    assert np.array_equal(out[0], out[1]) and np.array_equal(out[1], np.arange(10, dtype=np.float32))
+
+
+def test_max_over_ranks_world2():
+    out = _run(_maxtime)
+    assert out[0] == out[1] == 2.0
+
+
+def test_trainer_gradient_exchange_world2():
+    out = _run(_trainer_allreduce)
+    assert np.allclose(out[0], 2.0) and np.allclose(out[1], 2.0)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_frame_schedule_covers_each_frame_once_per_round(world):
+    n = 8
+    for step in range(4):
+        frames = [shard.frame_of(r, world, step, n) for r in range(world)]
+        assert len(set(frames)) == world
+    seen = sorted(f for r in range(world) for f in shard.frames_for_rank(r, world, n))
+    assert seen == list(range(n))
+    tiles = sorted(t for r in range(world) for t in shard.tiles_for_rank(r, world, 64))
+    assert tiles == list(range(64))
