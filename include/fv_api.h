@@ -181,7 +181,17 @@ int32_t fv_composite_bwd(const float* d_rgbs, const float* d_delta, const float*
 /* posenc of x_skel (xs (n,4) = [x_skel, L]; zero rows where L <= eps_w) -> (n, 3+6*bands)
  * with Hann band weights w (ad:574-600); backward accumulates into dx (n,3) (ad:602-609). */
 int32_t fv_posenc_fwd(const float* d_xs, int64_t n, float eps_w, int32_t bands, const float* w,
-                      float* d_pe, void* stream);
+                      float* d_pe, int64_t ld, void* stream);
+/* TF32 tensor-core layer ops (training): y = act(x @ W + b); backward from dz (masked
+ * pre-activation gradient): dx = (dz @ W^T) * (x_mask > 0) [x_mask may be NULL],
+ * dW += x^T dz, db += colsum(dz).  Rows may be padded (ld >= width). */
+int32_t fv_linear_fwd_tc(const float* d_x, int64_t ldx, const float* d_w, const float* d_b,
+                         float* d_y, int64_t ldy, int64_t m, int32_t k_in, int32_t n_out,
+                         int32_t act, void* stream);
+int32_t fv_linear_bwd_tc(const float* d_x, int64_t ldx, const float* d_w, const float* d_dz,
+                         int64_t ldz, float* d_dx, int64_t lddx, const float* d_xmask,
+                         float* d_dw, float* d_db, int64_t m, int32_t k_in, int32_t n_out,
+                         void* stream);
 int32_t fv_posenc_bwd(const float* d_xs, int64_t n, float eps_w, int32_t bands, const float* w,
                       const float* d_dpe, int64_t ld, float* d_dx, void* stream);
 /* x_final = x_skel + x_res on foreground rows; d_xres may be NULL. */

@@ -78,7 +78,9 @@ SIGNATURES = {
     "fv_field_fwd": (i32, [P(FvField), P(FvHash), vp, i64, f32, vp, vp, vp, sz, vp]),
     "fv_composite_fwd": (i32, [vp, vp, vp, i32, i32, i64, i32, P(f32), f32, f32, vp, vp, vp, vp]),
     "fv_composite_bwd": (i32, [vp, vp, vp, i32, i32, vp, i64, i32, P(f32), f32, vp, vp, vp, vp]),
-    "fv_posenc_fwd": (i32, [vp, i64, f32, i32, P(f32), vp, vp]),
+    "fv_posenc_fwd": (i32, [vp, i64, f32, i32, P(f32), vp, i64, vp]),
+    "fv_linear_fwd_tc": (i32, [vp, i64, vp, vp, vp, i64, i64, i32, i32, i32, vp]),
+    "fv_linear_bwd_tc": (i32, [vp, i64, vp, vp, i64, vp, i64, vp, vp, vp, i64, i32, i32, vp]),
     "fv_posenc_bwd": (i32, [vp, i64, f32, i32, P(f32), vp, i64, vp, vp]),
     "fv_xfinal": (i32, [vp, vp, i64, f32, vp, vp]),
     "fv_heads_fwd": (i32, [vp, vp, i64, f32, vp, vp]),

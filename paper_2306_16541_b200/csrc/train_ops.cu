@@ -9,12 +9,13 @@ namespace fv {
 
 // xs (n,4) = [x_skel, L]; rows with L <= eps_w produce zeros.
 __global__ void k_posenc_fwd(const float4* __restrict__ xs, int64_t n, float eps_w, int bands, PeW w,
-                             float* __restrict__ pe) {
+                             float* __restrict__ pe, int64_t ld) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int D = 3 + 6 * bands;
   const float4 v = xs[p];
-  float* o = pe + p * D;
+  float* o = pe + p * ld;
+  for (int j = D; j < ld; ++j) o[j] = 0.f;  // row padding (16-byte aligned rows for the GEMMs)
   if (!(v.w > eps_w)) { for (int j = 0; j < D; ++j) o[j] = 0.f; return; }
   const float x[3] = {v.x, v.y, v.z};
   o[0] = x[0]; o[1] = x[1]; o[2] = x[2];
@@ -143,12 +144,13 @@ static unsigned g1(int64_t n) { return (unsigned)((n + 127) / 128); }
 using namespace fv;
 
 extern "C" int32_t fv_posenc_fwd(const float* d_xs, int64_t n, float eps_w, int32_t bands, const float* w,
-                                 float* d_pe, void* stream) {
-  if (n < 0 || bands < 1 || bands > 8 || !w) return set_error(FV_EDIM, "fv_posenc_fwd: bad arguments");
+                                 float* d_pe, int64_t ld, void* stream) {
+  if (n < 0 || bands < 1 || bands > 8 || !w || ld < 3 + 6 * bands)
+    return set_error(FV_EDIM, "fv_posenc_fwd: bad arguments");
   if (n == 0) return FV_OK;
   PeW pw{};
   for (int i = 0; i < bands; ++i) pw.w[i] = w[i];
-  k_posenc_fwd<<<g1(n), 128, 0, (cudaStream_t)stream>>>((const float4*)d_xs, n, eps_w, bands, pw, d_pe);
+  k_posenc_fwd<<<g1(n), 128, 0, (cudaStream_t)stream>>>((const float4*)d_xs, n, eps_w, bands, pw, d_pe, ld);
   return check_launch("fv_posenc_fwd");
 }
 

@@ -61,7 +61,10 @@ class Trainer:
 
     def __init__(self, nets: FreeviewModel, camera: CameraModel, target: np.ndarray, mask: np.ndarray,
                  settings: RenderSettings, n_patches: int = 6, patch: int = 32, seed: int = 0,
-                 process_group=None):
+                 process_group=None, precision: str = "tf32"):
+        if precision not in ("tf32", "fp32"):
+            raise ValueError("precision must be 'tf32' (tcgen05 kind::tf32 layers) or 'fp32' (SIMT, strict parity)")
+        self.tc = precision == "tf32"
         self.nets, self.cam, self.st = nets, camera, settings
         self.lib = nets.lib
         self.dev = nets.device
@@ -78,10 +81,11 @@ class Trainer:
         self.pix_host = torch.empty(self.R, dtype=torch.int32, pin_memory=True)
         d_pe = 3 + 6 * PE_BANDS
         self.d_pe = d_pe
+        self.pe_ld = (d_pe + 3) // 4 * 4 if self.tc else d_pe   # 16-byte rows for the TF32 GEMMs
         self.xs = torch.empty((S, 4), **f32)
         self.delta = torch.empty(S, **f32)
         self.x = torch.empty((S, 3), **f32)
-        self.pe = torch.empty((S, d_pe), **f32)
+        self.pe = torch.empty((S, self.pe_ld), **f32)
         self.h = [torch.empty((S, 128), **f32) for _ in range(4)]
         self.xres = torch.empty((S, 3), **f32)
         self.xf = torch.empty((S, 3), **f32)
@@ -101,7 +105,7 @@ class Trainer:
         self.dfeat = torch.empty((S, 32), **f32)
         self.dxf = torch.empty((S, 3), **f32)
         self.dxs = torch.empty((S, 3), **f32)
-        self.dpe = torch.empty((S, d_pe), **f32)
+        self.dpe = torch.empty((S, self.pe_ld), **f32)
         self.dvol = torch.empty_like(nets.vol)
         # optimizer state over the flat master buffer
         self.grad = torch.zeros_like(nets.flat)
@@ -120,8 +124,22 @@ class Trainer:
 
     # ------------------------------------------------------------------------------------
     def _lin(self, x, w, b, y, k, n, act, sp):
-        _lib.check(self.lib.fv_linear_fwd(x.data_ptr(), w.data_ptr(), b.data_ptr() if b is not None else None,
-                                          y.data_ptr(), self.S, k, n, act, sp), "fv_linear_fwd")
+        bp = b.data_ptr() if b is not None else None
+        if self.tc:
+            _lib.check(self.lib.fv_linear_fwd_tc(x.data_ptr(), x.shape[1], w.data_ptr(), bp, y.data_ptr(), y.shape[1],
+                                                 self.S, k, n, act, sp), "fv_linear_fwd_tc")
+        else:
+            _lib.check(self.lib.fv_linear_fwd(x.data_ptr(), w.data_ptr(), bp, y.data_ptr(), self.S, k, n, act, sp),
+                       "fv_linear_fwd")
+
+    def _lin_bwd_tc(self, x, w, dz, dx, xmask, dw, db, k, n, sp):
+        """dz = masked pre-activation gradient of this layer; dx gets (dz W^T) * (xmask > 0),
+        i.e. the masked dz of the previous layer when xmask is that layer's ReLU output."""
+        _lib.check(self.lib.fv_linear_bwd_tc(x.data_ptr(), x.shape[1], w.data_ptr(), dz.data_ptr(), dz.shape[1],
+                                             dx.data_ptr() if dx is not None else None,
+                                             dx.shape[1] if dx is not None else 0,
+                                             xmask.data_ptr() if xmask is not None else None, dw.data_ptr(),
+                                             db.data_ptr(), self.S, k, n, sp), "fv_linear_bwd_tc")
 
     def _lin_bwd(self, x, w, y, dy, dx, dw, db, k, n, act, sp):
         _lib.check(self.lib.fv_linear_bwd(x.data_ptr(), w.data_ptr(), y.data_ptr(), dy.data_ptr(),
@@ -141,7 +159,8 @@ class Trainer:
         _lib.check(lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), self.R, self.xs.data_ptr(),
                                      self.delta.data_ptr(), self.x.data_ptr(), None, sp), "fv_march_warp")
         V = nets.views
-        _lib.check(lib.fv_posenc_fwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.pe.data_ptr(), sp))
+        _lib.check(lib.fv_posenc_fwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.pe.data_ptr(), self.pe_ld,
+                                     sp))
         self._lin(self.pe, V["off_w0"], nets.b0_eff, self.h[0], self.d_pe, 128, 1, sp)
         for i in range(1, 4):
             self._lin(self.h[i - 1], V[f"off_w{i}"], V[f"off_b{i}"], self.h[i], 128, 128, 1, sp)
@@ -170,21 +189,33 @@ class Trainer:
                                         None, self.d_rgbs.data_ptr(), sp), "fv_composite_bwd")
         _lib.check(lib.fv_heads_bwd(self.xs.data_ptr(), self.hd.data_ptr(), self.d_rgbs.data_ptr(), S, eps,
                                     self.dh.data_ptr(), sp))
-        self._lin_bwd(self.r[1], V["rad_w2"], self.hd, self.dh, self.g64[0], G["rad_w2"], G["rad_b2"], 64, 4, 0, sp)
-        self._lin_bwd(self.r[0], V["rad_w1"], self.r[1], self.g64[0], self.g64[1], G["rad_w1"], G["rad_b1"], 64, 64, 1, sp)
-        self._lin_bwd(self.feat, V["rad_w0"], self.r[0], self.g64[1], self.dfeat, G["rad_w0"], G["rad_b0"], 32, 64, 1, sp)
         h = nets.hash_struct()
-        _lib.check(lib.fv_hash_bwd(C.byref(h), self.xf.data_ptr(), S, self.dfeat.data_ptr(), G["table"].data_ptr(),
-                                   self.dxf.data_ptr(), sp), "fv_hash_bwd")
-        self._lin_bwd(self.h[3], V["off_w4"], self.xres, self.dxf, self.g128[0], G["off_w4"], G["off_b4"], 128, 3, 0, sp)
-        self._lin_bwd(self.h[2], V["off_w3"], self.h[3], self.g128[0], self.g128[1], G["off_w3"], G["off_b3"], 128, 128, 1, sp)
-        self._lin_bwd(self.h[1], V["off_w2"], self.h[2], self.g128[1], self.g128[0], G["off_w2"], G["off_b2"], 128, 128, 1, sp)
-        self._lin_bwd(self.h[0], V["off_w1"], self.h[1], self.g128[0], self.g128[1], G["off_w1"], G["off_b1"], 128, 128, 1, sp)
-        self._lin_bwd(self.pe, V["off_w0"], self.h[0], self.g128[1], self.dpe, G["off_w0"], G["off_b0"], self.d_pe, 128, 1, sp)
+        if self.tc:  # dz-form: each dx epilogue applies the previous layer's ReLU mask
+            self._lin_bwd_tc(self.r[1], V["rad_w2"], self.dh, self.g64[0], self.r[1], G["rad_w2"], G["rad_b2"], 64, 4, sp)
+            self._lin_bwd_tc(self.r[0], V["rad_w1"], self.g64[0], self.g64[1], self.r[0], G["rad_w1"], G["rad_b1"], 64, 64, sp)
+            self._lin_bwd_tc(self.feat, V["rad_w0"], self.g64[1], self.dfeat, None, G["rad_w0"], G["rad_b0"], 32, 64, sp)
+            _lib.check(lib.fv_hash_bwd(C.byref(h), self.xf.data_ptr(), S, self.dfeat.data_ptr(),
+                                       G["table"].data_ptr(), self.dxf.data_ptr(), sp), "fv_hash_bwd")
+            self._lin_bwd_tc(self.h[3], V["off_w4"], self.dxf, self.g128[0], self.h[3], G["off_w4"], G["off_b4"], 128, 3, sp)
+            self._lin_bwd_tc(self.h[2], V["off_w3"], self.g128[0], self.g128[1], self.h[2], G["off_w3"], G["off_b3"], 128, 128, sp)
+            self._lin_bwd_tc(self.h[1], V["off_w2"], self.g128[1], self.g128[0], self.h[1], G["off_w2"], G["off_b2"], 128, 128, sp)
+            self._lin_bwd_tc(self.h[0], V["off_w1"], self.g128[0], self.g128[1], self.h[0], G["off_w1"], G["off_b1"], 128, 128, sp)
+            self._lin_bwd_tc(self.pe, V["off_w0"], self.g128[1], self.dpe, None, G["off_w0"], G["off_b0"], self.d_pe, 128, sp)
+        else:
+            self._lin_bwd(self.r[1], V["rad_w2"], self.hd, self.dh, self.g64[0], G["rad_w2"], G["rad_b2"], 64, 4, 0, sp)
+            self._lin_bwd(self.r[0], V["rad_w1"], self.r[1], self.g64[0], self.g64[1], G["rad_w1"], G["rad_b1"], 64, 64, 1, sp)
+            self._lin_bwd(self.feat, V["rad_w0"], self.r[0], self.g64[1], self.dfeat, G["rad_w0"], G["rad_b0"], 32, 64, 1, sp)
+            _lib.check(lib.fv_hash_bwd(C.byref(h), self.xf.data_ptr(), S, self.dfeat.data_ptr(),
+                                       G["table"].data_ptr(), self.dxf.data_ptr(), sp), "fv_hash_bwd")
+            self._lin_bwd(self.h[3], V["off_w4"], self.xres, self.dxf, self.g128[0], G["off_w4"], G["off_b4"], 128, 3, 0, sp)
+            self._lin_bwd(self.h[2], V["off_w3"], self.h[3], self.g128[0], self.g128[1], G["off_w3"], G["off_b3"], 128, 128, 1, sp)
+            self._lin_bwd(self.h[1], V["off_w2"], self.h[2], self.g128[1], self.g128[0], G["off_w2"], G["off_b2"], 128, 128, 1, sp)
+            self._lin_bwd(self.h[0], V["off_w1"], self.h[1], self.g128[0], self.g128[1], G["off_w1"], G["off_b1"], 128, 128, 1, sp)
+            self._lin_bwd(self.pe, V["off_w0"], self.h[0], self.g128[1], self.dpe, G["off_w0"], G["off_b0"], self.d_pe, 128, 1, sp)
         # the folded pose rows of W0: dW0[D:, :] = pose (outer) d b0_eff  (b0_eff = b0 + pose @ W0[D:])
         G["off_w0"][self.d_pe:].addr_(nets.pose_dev, G["off_b0"])
         self.dxs.copy_(self.dxf)
-        _lib.check(lib.fv_posenc_bwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.dpe.data_ptr(), self.d_pe,
+        _lib.check(lib.fv_posenc_bwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.dpe.data_ptr(), self.pe_ld,
                                      self.dxs.data_ptr(), sp))
         w = nets.warp_struct()
         _lib.check(lib.fv_warp_bwd(C.byref(w), eps, self.x.data_ptr(), S, self.dxs.data_ptr(), self.dvol.data_ptr(), sp),

@@ -74,6 +74,38 @@ def test_linear_bwd_matches_numpy():
     _close(db.cpu().numpy(), dz.sum(0), 1e-5, "db")
 
 
+@pytest.mark.parametrize("m,k,ld,n,act", [(3000, 39, 40, 128, 1), (2999, 128, 128, 128, 1), (4096, 128, 128, 3, 0),
+                                          (1000, 64, 64, 4, 0), (5000, 32, 32, 64, 1)])
+def test_linear_tf32_tensor_core_layers(m, k, ld, n, act):
+    """fv_linear_fwd_tc / fv_linear_bwd_tc (tcgen05 kind::tf32) vs float64 numpy; TF32 has a
+    10-bit mantissa, so the bar is 1e-2 relative to the output scale."""
+    rng = np.random.default_rng(m + k + n)
+    x = np.zeros((m, ld), np.float32)
+    x[:, :k] = rng.normal(size=(m, k))
+    w = (rng.normal(size=(k, n)) / np.sqrt(k)).astype(np.float32)
+    b = rng.normal(size=n).astype(np.float32)
+    lib = _lib.load()
+    xt, wt, bt = _t(x), _t(w), _t(b)
+    y = torch.empty((m, n), device=DEV)
+    _lib.check(lib.fv_linear_fwd_tc(xt.data_ptr(), ld, wt.data_ptr(), bt.data_ptr(), y.data_ptr(), n, m, k, n, act,
+                                    _lib.stream_ptr()))
+    z = x[:, :k].astype(np.float64) @ w + b
+    yr = np.maximum(z, 0) if act else z
+    _close(y.cpu().numpy(), yr, 2e-5, "y")   # forward is split-precision 3xTF32 (~fp32)
+    dz = rng.normal(size=(m, n)).astype(np.float32) * (z > 0 if act else 1)
+    xmask = rng.normal(size=(m, ld)).astype(np.float32)
+    dx = torch.zeros((m, ld), device=DEV)
+    dw = torch.zeros((k, n), device=DEV)
+    db = torch.zeros(n, device=DEV)
+    dzt, xm = _t(dz), _t(xmask)
+    _lib.check(lib.fv_linear_bwd_tc(xt.data_ptr(), ld, wt.data_ptr(), dzt.data_ptr(), n, dx.data_ptr(), ld,
+                                    xm.data_ptr(), dw.data_ptr(), db.data_ptr(), m, k, n, _lib.stream_ptr()))
+    dxr = (dz.astype(np.float64) @ w.T.astype(np.float64)) * (xmask[:, :k] > 0)
+    _close(dx.cpu().numpy()[:, :k], dxr, 1e-2, "dx")
+    _close(dw.cpu().numpy(), x[:, :k].T.astype(np.float64) @ dz, 1e-2, "dw")
+    _close(db.cpu().numpy(), dz.sum(0, dtype=np.float64), 1e-5, "db")
+
+
 def test_hash_bwd_matches_oracle():
     sc = make("c1", table_scale=0.5)
     nets = FreeviewModel(sc)
@@ -109,7 +141,8 @@ def test_warp_bwd_matches_oracle():
     _close(dvol.cpu().numpy(), ref, 1e-4, "dvol")
 
 
-def test_full_step_gradients_match_oracle():
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+def test_full_step_gradients_match_oracle(precision):
     """Whole-step gradients vs the oracle's float64 backward on the same inputs.
 
     Bar: the north star's 1e-3 absolute on every gradient.  The relative bound is set by
@@ -117,13 +150,14 @@ def test_full_step_gradients_match_oracle():
     terms and the fine hash levels amplify float32 position round-off ~500x, so the
     oracle's OWN gradient moves by a few 1e-3 (table) when the residual bias is nudged by
     3e-7; the GPU (float32 forward, different summation order) must stay within 3x of that
-    measured sensitivity."""
+    measured sensitivity.  The tensor-core path (split-precision 3xTF32 layers) is held to
+    the same rule with the nudge scaled to its round-off (1e-6)."""
     sc = make("c1", width=48, height=48, n_samples=24, table_scale=0.5, bias_scale=0.05,
               background=(0.1, 0.3, 0.8))
     nets = FreeviewModel(sc)
     target, mask = target_image(sc)
     st = RenderSettings.from_config(sc.cfg, seed=5)
-    tr = Trainer(nets, sc.camera, target, mask, st, n_patches=2, patch=16, seed=3)
+    tr = Trainer(nets, sc.camera, target, mask, st, n_patches=2, patch=16, seed=3, precision=precision)
     pix = patch_pixels(sample_patches(mask, 2, 16, 3, 0), 16, 48)
     loss = tr.forward(pix)
     tr.backward()
@@ -135,7 +169,9 @@ def test_full_step_gradients_match_oracle():
     oloss, og, _ = opipe.loss_and_grads(osc, cc, pix, 48, ost, tgt)
     assert abs(loss.item() - oloss) < 1e-5 * max(1.0, oloss)
     nudged = dict(osc, off_b=[b.copy() for b in osc["off_b"]])
-    nudged["off_b"][4] = nudged["off_b"][4] + np.float32(3e-7)
+    # nudge the residual output by the forward's own round-off scale: float32 ~3e-7; the TF32
+    # path's split-precision (3xTF32) layers carry ~2^-21 relative error per product -> 1e-6
+    nudged["off_b"][4] = nudged["off_b"][4] + np.float32(3e-7 if precision == "fp32" else 1e-6)
     _, og2, _ = opipe.loss_and_grads(nudged, cc, pix, 48, ost, tgt)
 
     def sens(a, b):
