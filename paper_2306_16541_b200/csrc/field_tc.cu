@@ -113,6 +113,46 @@ __device__ __forceinline__ void layer_mma(const uint8_t* A, const uint8_t* Wt, u
 }
 
 // TMEM row -> bias + ReLU -> fp16 -> A operand (columns [0, NC)).
+// fp16x2 helpers: (lo, hi) -> packed half2 ; relu(p * 1 + bias) in one instruction
+__device__ __forceinline__ uint32_t cvt_h2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// relu + round + pack in one conversion: (lo, hi) -> half2(max(lo,0), max(hi,0))
+__device__ __forceinline__ uint32_t cvt_relu_h2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// TMEM row -> + bias (fp32, smem) -> ReLU+fp16 pack (one cvt) -> A operand: 3 instructions
+// per pair (the FADD/FMNMX/FSETP/F2FP form spent ~40% of the kernel's issue slots)
+template <int NC>
+__device__ __forceinline__ void epi_relu_h2(uint32_t trow, const float* bias, uint8_t* A, int t) {
+#pragma unroll
+  for (int g = 0; g < NC / 16; g += 2) {
+    float v[2][16];
+    tc::tmem_ld16(trow + g * 16, v[0]);
+    tc::tmem_ld16(trow + g * 16 + 16, v[1]);
+    tc::tmem_ld_wait();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      float bb[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 b4 = *reinterpret_cast<const float4*>(bias + (g + u) * 16 + 4 * q);
+        bb[4 * q] = b4.x; bb[4 * q + 1] = b4.y; bb[4 * q + 2] = b4.z; bb[4 * q + 3] = b4.w;
+      }
+      uint32_t w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j] = cvt_relu_h2(v[u][2 * j] + bb[2 * j], v[u][2 * j + 1] + bb[2 * j + 1]);
+      *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * (g + u))) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * (g + u) + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+  }
+}
+
 template <int NC>
 __device__ __forceinline__ void epi_relu(uint32_t trow, const float* bias, uint8_t* A, int t) {
 #pragma unroll
@@ -163,6 +203,7 @@ __device__ __forceinline__ void tc_prologue_sync() {
 constexpr uint32_t OF_W = PK_RAD0 - PK_OFF0;             // 114688
 constexpr uint32_t OF_BIAS = OF_W;                       // off b1..b4: 400 floats
 constexpr uint32_t OF_B0 = OF_BIAS + 400 * 4;            // 128 floats
+
 constexpr uint32_t OF_A = (OF_B0 + 512 + 127) / 128 * 128;
 
 template <int NWG>
@@ -192,19 +233,22 @@ __global__ void __launch_bounds__(NWG * 128, 1)
     const float4 v = s < n ? xs[s] : make_float4(0.f, 0.f, 0.f, 0.f);
     const bool fg = s < n && v.w > eps_w;
     const float x0 = fg ? v.x : 0.f, x1 = fg ? v.y : 0.f, x2 = fg ? v.z : 0.f;
-    {  // posenc -> A chunks 0..5 (39 values + zero pad to 48); sin(pi x 2^k) via sincospif
+    {  // posenc -> A chunks 0..5 (39 values + zero pad to 48): sin/cos(pi x) once per coordinate,
+       // higher bands by double-angle recurrences (error 2^k ulp << fp16 resolution)
       __half pe[48];
       pe[0] = __float2half_rn(x0); pe[1] = __float2half_rn(x1); pe[2] = __float2half_rn(x2);
       const float xx[3] = {x0, x1, x2};
 #pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        const float wk = k < f.pe_bands ? f.pe_w[k] : 0.f;
+      for (int j = 0; j < 3; ++j) {
+        float sv, cv;
+        sincospif(xx[j], &sv, &cv);
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          float sv, cv;
-          sincospif(xx[j] * (float)(1 << k), &sv, &cv);
+        for (int k = 0; k < 6; ++k) {
+          const float wk = k < f.pe_bands ? f.pe_w[k] : 0.f;
           pe[3 + 6 * k + j] = __float2half_rn(wk * sv);
           pe[3 + 6 * k + 3 + j] = __float2half_rn(wk * cv);
+          const float s2 = 2.f * sv * cv, c2 = (cv - sv) * (cv + sv);
+          sv = s2; cv = c2;
         }
       }
 #pragma unroll
@@ -214,13 +258,13 @@ __global__ void __launch_bounds__(NWG * 128, 1)
         *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = *reinterpret_cast<const uint4*>(pe + 8 * c);
     }
     layer_mma<48, 128>(A, smem + (PK_OFF0 - PK_OFF0), tcol, bar, phase, t, wg);
-    epi_relu<128>(trow, sB0, A, t);
+    epi_relu_h2<128>(trow, sB0, A, t);
     layer_mma<128, 128>(A, smem + (PK_OFF1 - PK_OFF0), tcol, bar, phase, t, wg);
-    epi_relu<128>(trow, sBias + (BI_OFF1 - BI_OFF1), A, t);
+    epi_relu_h2<128>(trow, sBias, A, t);
     layer_mma<128, 128>(A, smem + (PK_OFF2 - PK_OFF0), tcol, bar, phase, t, wg);
-    epi_relu<128>(trow, sBias + (BI_OFF2 - BI_OFF1), A, t);
+    epi_relu_h2<128>(trow, sBias + 128, A, t);
     layer_mma<128, 128>(A, smem + (PK_OFF3 - PK_OFF0), tcol, bar, phase, t, wg);
-    epi_relu<128>(trow, sBias + (BI_OFF3 - BI_OFF1), A, t);
+    epi_relu_h2<128>(trow, sBias + 256, A, t);
     layer_mma<128, 16>(A, smem + (PK_OFF4 - PK_OFF0), tcol, bar, phase, t, wg);
     float o[16];
     tc::tmem_ld16(trow, o);
@@ -242,6 +286,7 @@ __global__ void __launch_bounds__(NWG * 128, 1)
 // ---- k_radiance_tc: (x_final, L) -> (c, sigma) ----------------------------------------
 constexpr uint32_t RA_W = PK_WEND - PK_RAD0;             // 14336
 constexpr uint32_t RA_BIAS = RA_W;                       // rad b0,b1,b2: 144 floats
+
 constexpr uint32_t RA_A = (RA_BIAS + 144 * 4 + 127) / 128 * 128;
 constexpr uint32_t RA_A_BYTES = 128 * 64 * 2;            // 16 KB per warpgroup
 
@@ -302,9 +347,9 @@ __global__ void __launch_bounds__(NWG * 128, 1)
       }
     }
     layer_mma<32, 64>(A, smem + (PK_RAD0 - PK_RAD0), tcol, bar, phase, t, wg);
-    epi_relu<64>(trow, sBias + (BI_RAD0 - BI_RAD0), A, t);
+    epi_relu_h2<64>(trow, sBias, A, t);
     layer_mma<64, 64>(A, smem + (PK_RAD1 - PK_RAD0), tcol, bar, phase, t, wg);
-    epi_relu<64>(trow, sBias + (BI_RAD1 - BI_RAD0), A, t);
+    epi_relu_h2<64>(trow, sBias + 64, A, t);
     layer_mma<64, 16>(A, smem + (PK_RAD2 - PK_RAD0), tcol, bar, phase, t, wg);
     float o[16];
     tc::tmem_ld16(trow, o);
