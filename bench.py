@@ -198,7 +198,8 @@ def run_ours(args, rank, world, local_rank):
     def pose_of(step):
         return sc.poses[shard.frame_of(rank, world, step, len(sc.poses))]
 
-    launches_per_step = 3 + (3 if occ_on else 0) + 1  # march, field, composite (+ occ points/field/bits) + bias fold
+    # march(+compaction), k_offset_tc, k_radiance_tc, composite, pose-bias fold; occupancy: points, 2 field, bits
+    launches_per_step = 5 + (4 if occ_on else 0)
 
     def step(i):
         nets.set_pose(pose_of(i))
@@ -262,7 +263,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- per-stage device times (same inputs, separate pass, CUDA events on this stream)
     stages = stage_times(nets, rnd, cam, st, dev, occ_on, reps=max(3, min(args.steps, 10)))
     n_samples_launch = ((n_rays + 31) // 32 * 32) * cfg.n_samples
-    roofs = stage_rooflines(stages, cfg, n_samples_launch)
+    roofs = stage_rooflines(stages, cfg, n_samples_launch, stages.get("fg_samples", n_samples_launch))
     dominant = max(roofs, key=lambda k: stages.get(k, 0.0))
     roof = dict(roofs[dominant])
 
@@ -305,8 +306,10 @@ KERNEL_UNITS = {
 }
 
 
-def stage_rooflines(stages, cfg, n_samples):
-    """Per-kernel roofline from the live CUDA-event stage times; peaks from MEASURED_PEAKS.json."""
+def stage_rooflines(stages, cfg, n_all, n_fg):
+    """Per-kernel roofline from the live CUDA-event stage times; peaks from MEASURED_PEAKS.json.
+    The march and compositor touch every sample slot; the field kernels run on the compacted
+    foreground stream (n_fg samples)."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = json.load(open(path)) if os.path.exists(path) else {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0}
     src = "MEASURED_PEAKS.json" if os.path.exists(path) else "fallback (B200_PROFILING.md)"
@@ -317,6 +320,7 @@ def stage_rooflines(stages, cfg, n_samples):
         if key not in stages or stages[key] <= 0:
             continue
         sec = stages[key] * 1e-3
+        n_samples = n_fg if key in ("offset", "radiance") else n_all
         if bound == "tensor":
             ach, pk, u = n_samples * unit / sec / 1e12, peaks.get("bf16_tflops_sustained", 1394.7), "TFLOP/s"
             psrc = src + " bf16_tflops_sustained (fp16 MMA assumed equal)"
@@ -327,7 +331,8 @@ def stage_rooflines(stages, cfg, n_samples):
             psrc = src + " hbm_gbs"
         tr = traffic.get(kname)
         out[key] = {"kernel": kname, "bound": bound, "achieved": ach, "peak": pk, "unit": u, "frac": ach / pk,
-                    "traffic": tr, "ms": stages[key], "algorithmic": algo, "peak_source": psrc}
+                    "traffic": tr, "ms": stages[key], "algorithmic": f"{algo} x {n_samples} samples/launch",
+                    "peak_source": psrc}
     return out
 
 
@@ -384,61 +389,47 @@ def train_throughput(args, rank, world, dev):
 
 
 def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5):
-    """Device time of each kernel stage of one frame (CUDA events on the launch stream)."""
+    """Device time of each stage of the actual render path (fv_render_fwd_timed: CUDA
+    events between march+warp+compaction, k_offset_tc, k_radiance_tc and the compositor),
+    median over `reps` frames; plus the occupancy rebuild."""
     import ctypes as C
     import torch
     from paper_2306_16541_b200 import _lib
     from paper_2306_16541_b200.render import camera_struct, march_struct
     lib = nets.lib
-    stream = torch.cuda.current_stream()
-    sp = stream.cuda_stream
+    sp = torch.cuda.current_stream().cuda_stream
     pix = rnd.pixel_order(cam)
     n = pix.numel()
     occ = rnd.build_occupancy(nets, st) if occ_on else None
     m, cs, w = march_struct(st, pix, occ, True), camera_struct(cam), nets.warp_struct()
     h, f = nets.hash_struct(), nets.field_struct()
-    S = (n + 31) // 32 * 32 * st.n_samples
-    xs = torch.empty((S, 4), device=dev)
-    delta = torch.empty(S, device=dev)
-    rgbs = torch.empty((S, 4), device=dev)
-    nb = lib.fv_field_workspace_bytes(S, f.precision)
-    fw = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
     rgb = torch.empty((n, 3), device=dev)
     alpha = torch.empty(n, device=dev)
     wb = lib.fv_render_workspace_bytes(n, st.n_samples, f.precision)
     work = torch.empty(wb, dtype=torch.uint8, device=dev)
-    out = {}
-
-    def timeit(fn):
+    rows, nfg = [], C.c_int64(0)
+    for _ in range(reps):
+        t = (C.c_float * 5)()
+        _lib.check(lib.fv_render_fwd_timed(C.byref(cs), C.byref(m), C.byref(w), C.byref(h), C.byref(f), n,
+                                           work.data_ptr(), wb, rgb.data_ptr(), alpha.data_ptr(), t, C.byref(nfg),
+                                           sp), "fv_render_fwd_timed")
+        rows.append(list(t))
+    med = np.median(np.array(rows), axis=0)
+    S = (n + 31) // 32 * 32 * st.n_samples
+    out = {"march_warp": float(med[0]), "offset": float(med[1]), "radiance": float(med[2]),
+           "composite": float(med[3]), "render_total": float(med[4]),
+           "field": float(med[1] + med[2]), "samples": S, "fg_samples": int(nfg.value),
+           "fg_fraction": nfg.value / S}
+    if occ_on:
         ts = []
         for _ in range(reps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fn()
-            b.record(stream)
+            a.record()
+            rnd.build_occupancy(nets, st)
+            b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
-        return float(np.median(ts))
-
-    out["march_warp"] = timeit(lambda: _lib.check(lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), n, xs.data_ptr(),
-                                                                     delta.data_ptr(), None, None, sp)))
-    out["field"] = timeit(lambda: _lib.check(lib.fv_field_fwd(C.byref(f), C.byref(h), xs.data_ptr(), S, st.eps_w,
-                                                               rgbs.data_ptr(), None, fw.data_ptr(), nb, sp)))
-    total = timeit(lambda: _lib.check(lib.fv_render_fwd(C.byref(cs), C.byref(m), C.byref(w), C.byref(h), C.byref(f), n,
-                                                         work.data_ptr(), wb, rgb.data_ptr(), alpha.data_ptr(), None, sp)))
-    out["render_total"] = total
-    out["composite"] = max(total - out["march_warp"] - out["field"], 0.0)
-    if f.precision == 1:  # time the two tensor-core kernels separately (k_offset_tc, k_radiance_tc)
-        xf = torch.empty((S, 4), device=dev)
-        f_rad = nets.field_struct(offset_enabled=False)
-        out["offset"] = timeit(lambda: _lib.check(lib.fv_residual_offset(C.byref(f), xs.data_ptr(), S, st.eps_w,
-                                                                         xf.data_ptr(), sp)))
-        out["radiance"] = timeit(lambda: _lib.check(lib.fv_field_fwd(C.byref(f_rad), C.byref(h), xf.data_ptr(), S,
-                                                                     st.eps_w, rgbs.data_ptr(), None, fw.data_ptr(),
-                                                                     nb, sp)))
-    if occ_on:
-        out["occupancy_build"] = timeit(lambda: rnd.build_occupancy(nets, st))
-    out["fg_fraction"] = float((xs[:, 3] > st.eps_w).float().mean().item())
+        out["occupancy_build"] = float(np.median(ts))
     return out
 
 

@@ -231,6 +231,14 @@ int32_t fv_render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp
                       void* d_work, size_t work_bytes, float* d_rgb, float* d_alpha,
                       int32_t* d_count, void* stream);
 
+/* fv_render_fwd with CUDA events between its stages (measurement): synchronises, writes
+ * stage_ms[5] = {march+warp+compaction, residual MLP, hash+radiance, compositor, total}
+ * and the number of foreground samples the field evaluated to *n_fg (may be NULL). */
+int32_t fv_render_fwd_timed(const fv_camera* cam, const fv_march* march, const fv_warp* warp,
+                            const fv_hash* hash, const fv_field* field, int64_t n_rays,
+                            void* d_work, size_t work_bytes, float* d_rgb, float* d_alpha,
+                            float* stage_ms, int64_t* n_fg, void* stream);
+
 /* ---- occupancy (builder-defined; PARITY UNPINNED) ------------------------------------- */
 
 /* Evaluate density at 2x2x2 sub-cell points of each of the 32^3 observation-box cells

@@ -92,6 +92,8 @@ SIGNATURES = {
     "fv_march_warp": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), i64, vp, vp, vp, vp, vp]),
     "fv_render_fwd": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), P(FvHash), P(FvField), i64, vp, sz,
                             vp, vp, vp, vp]),
+    "fv_render_fwd_timed": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), P(FvHash), P(FvField), i64, vp, sz,
+                                  vp, vp, P(f32), P(i64), vp]),
     "fv_occupancy_workspace_bytes": (sz, [i32]),
     "fv_occupancy_build": (i32, [P(FvMarch), P(FvWarp), P(FvHash), P(FvField), f32, vp, sz, vp, vp]),
     "fv_adam_step": (i32, [vp, vp, vp, vp, i64, P(i64), P(f32), i32, i32, f32, f32, f32, vp, i64, i64,

@@ -27,21 +27,34 @@ int32_t check_launch(const char* where) {
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct RenderWork {
-  float4* xs; float* delta; float4* rgbs; void* fwork; size_t fbytes;
+  float* lik; float* delta; float4* rgbs; float4* xsc; int32_t* idx; int32_t* count; float4* rgbsc;
+  void* fwork; size_t fbytes;
 };
 
+// workspace: per-sample likelihood / spacing / [c, sigma] (full ray-block-major layout),
+// the march's compacted foreground stream (x, L) + sample ids + counter, and for the fp32
+// path a compacted [c, sigma] buffer and the SIMT layer scratch.
 static size_t carve(void* base, int64_t S, int precision, RenderWork* w) {
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
-  const size_t o_xs = take((size_t)S * 16), o_d = take((size_t)S * 4), o_r = take((size_t)S * 16);
+  const size_t o_l = take((size_t)S * 4), o_d = take((size_t)S * 4), o_r = take((size_t)S * 16);
+  const size_t o_x = take((size_t)S * 16), o_i = take((size_t)S * 4), o_c = take(16);
+  const size_t o_rc = take(precision == 0 ? (size_t)S * 16 : 0);
   const size_t fb = precision == 0 ? field_f32_work_bytes(S) : 0;
   const size_t o_f = take(fb);
   if (w) {
     uint8_t* b = (uint8_t*)base;
-    w->xs = (float4*)(b + o_xs); w->delta = (float*)(b + o_d); w->rgbs = (float4*)(b + o_r);
-    w->fwork = b + o_f; w->fbytes = fb;
+    w->lik = (float*)(b + o_l); w->delta = (float*)(b + o_d); w->rgbs = (float4*)(b + o_r);
+    w->xsc = (float4*)(b + o_x); w->idx = (int32_t*)(b + o_i); w->count = (int32_t*)(b + o_c);
+    w->rgbsc = (float4*)(b + o_rc); w->fwork = b + o_f; w->fbytes = fb;
   }
   return off;
+}
+
+__global__ void k_scatter4(const float4* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                           float4* __restrict__ dst) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) dst[idx[j]] = src[j];
 }
 
 int32_t field_fwd(const fv_field* f, const fv_hash* h, const float4* xs, int64_t n, float eps_w, float4* rgbs,
@@ -121,9 +134,11 @@ extern "C" size_t fv_render_workspace_bytes(int64_t n_rays, int32_t n_samples, i
   return carve(nullptr, padded_rays(n_rays) * n_samples, precision, nullptr);
 }
 
-extern "C" int32_t fv_render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp* warp, const fv_hash* hash,
-                                 const fv_field* field, int64_t n_rays, void* d_work, size_t work_bytes, float* d_rgb,
-                                 float* d_alpha, int32_t* d_count, void* stream) {
+// ev (optional, 5 events): recorded before the march, after the march, between the two
+// tensor-core field kernels, after the field and after the compositor (stage timing).
+static int32_t render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp* warp, const fv_hash* hash,
+                          const fv_field* field, int64_t n_rays, void* d_work, size_t work_bytes, float* d_rgb,
+                          float* d_alpha, int32_t* d_count, cudaStream_t st, cudaEvent_t* ev) {
   if (!cam || !march || !warp || !hash || !field || n_rays < 0 || march->n_samples < 1)
     return set_error(FV_EDIM, "fv_render_fwd: bad arguments");
   if (int32_t e = check_hash(hash)) return e;
@@ -134,13 +149,69 @@ extern "C" int32_t fv_render_fwd(const fv_camera* cam, const fv_march* march, co
     return set_error(FV_EDIM, "fv_render_fwd: workspace too small");
   RenderWork w;
   carve(d_work, S, field->precision, &w);
-  cudaStream_t st = (cudaStream_t)stream;
-  if (int32_t e = fv_march_warp(cam, march, warp, n_rays, (float*)w.xs, w.delta, nullptr, d_count, stream)) return e;
-  if (int32_t e = field_fwd(field, hash, w.xs, S, march->eps_w, w.rgbs, nullptr, w.fwork, w.fbytes, st)) return e;
-  CompIn in{w.rgbs, w.delta, reinterpret_cast<const float*>(w.xs) + 3, 4, true};
+  if (ev) cudaEventRecord(ev[0], st);
+  if (int32_t e = march_compact(cam, march, warp, n_rays, w.lik, w.delta, w.xsc, w.idx, w.count, d_count, st)) return e;
+  if (ev) cudaEventRecord(ev[1], st);
+  if (field->precision == 1) {  // tensor-core field over the foreground stream, count stays on the device
+    if (int32_t e = field_fwd_tc(field, hash, w.xsc, S, march->eps_w, w.rgbs, nullptr, st, w.count, w.idx,
+                                 ev ? ev[2] : nullptr))
+      return e;
+  } else {                      // fp32 parity path: host needs the count for its chunked SIMT layers
+    if (ev) cudaEventRecord(ev[2], st);
+    int32_t n_fg = 0;
+    cudaMemcpyAsync(&n_fg, w.count, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("fv_render_fwd count");
+    if (n_fg > 0) {
+      if (int32_t e = field_fwd(field, hash, w.xsc, n_fg, march->eps_w, w.rgbsc, nullptr, w.fwork, w.fbytes, st))
+        return e;
+      k_scatter4<<<(unsigned)((n_fg + 255) / 256), 256, 0, st>>>(w.rgbsc, w.idx, n_fg, w.rgbs);
+    }
+  }
+  if (ev) cudaEventRecord(ev[3], st);
+  CompIn in{w.rgbs, w.delta, w.lik, 1, true, true};
   const int32_t* out_pix = march->out_by_pixel ? march->d_pix : nullptr;
   if (march->out_by_pixel && !march->d_pix) return set_error(FV_EDIM, "fv_render_fwd: out_by_pixel needs d_pix");
-  return composite_fwd(in, n_rays, N, march->bg, march->eps_w, march->eps_t, out_pix, d_rgb, d_alpha, nullptr, st);
+  const int32_t e = composite_fwd(in, n_rays, N, march->bg, march->eps_w, march->eps_t, out_pix, d_rgb, d_alpha,
+                                  nullptr, st);
+  if (ev) cudaEventRecord(ev[4], st);
+  return e;
+}
+
+extern "C" int32_t fv_render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp* warp, const fv_hash* hash,
+                                 const fv_field* field, int64_t n_rays, void* d_work, size_t work_bytes, float* d_rgb,
+                                 float* d_alpha, int32_t* d_count, void* stream) {
+  return render_fwd(cam, march, warp, hash, field, n_rays, d_work, work_bytes, d_rgb, d_alpha, d_count,
+                    (cudaStream_t)stream, nullptr);
+}
+
+// Same render with CUDA events between its stages; synchronises and returns the device
+// times (ms) of march+warp, residual MLP, hash+radiance, compositor, total in stage_ms[5]
+// and the number of foreground samples the field evaluated in *n_fg.
+extern "C" int32_t fv_render_fwd_timed(const fv_camera* cam, const fv_march* march, const fv_warp* warp,
+                                       const fv_hash* hash, const fv_field* field, int64_t n_rays, void* d_work,
+                                       size_t work_bytes, float* d_rgb, float* d_alpha, float* stage_ms,
+                                       int64_t* n_fg, void* stream) {
+  cudaEvent_t ev[5];
+  for (auto& e : ev) cudaEventCreate(&e);
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t err = render_fwd(cam, march, warp, hash, field, n_rays, d_work, work_bytes, d_rgb, d_alpha, nullptr, st, ev);
+  if (!err) {
+    cudaEventSynchronize(ev[4]);
+    float t[4];
+    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    for (int i = 0; i < 4; ++i) stage_ms[i] = t[i];
+    cudaEventElapsedTime(&stage_ms[4], ev[0], ev[4]);
+    if (n_fg) {
+      RenderWork w;
+      carve(d_work, padded_rays(n_rays) * march->n_samples, field->precision, &w);
+      int32_t c = 0;
+      cudaMemcpy(&c, w.count, sizeof(int32_t), cudaMemcpyDeviceToHost);
+      *n_fg = c;
+    }
+    err = check_launch("fv_render_fwd_timed");
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return err;
 }
 
 extern "C" size_t fv_occupancy_workspace_bytes(int32_t precision) {

@@ -26,8 +26,11 @@ __global__ void k_composite_fwd(CompIn in, int64_t n_rays, int n, float3 bg, flo
     if (eps_t > 0.f && T < eps_t) break;
     const int64_t s = sidx(in, r, i, n);
     if (trans) trans[r * (n + 1) + i] = T;
-    const float4 v = in.rgbs[s];
     const float L = in.lik[s * in.lik_stride];
+    // background samples carry sigma = 0 (abar = 0, T unchanged): with a compacted field
+    // their [c, sigma] slot was never written, so they are skipped without reading it
+    if (in.skip_bg && !(L > eps_w)) continue;
+    const float4 v = in.rgbs[s];
     const float a = __fsub_rn(1.f, expf(-__fmul_rn(v.w, in.delta[s])));
     const float gate = fminf(fmaxf(__fdiv_rn(L, eps_w), 0.f), 1.f);
     const float ab = __fmul_rn(a, gate);

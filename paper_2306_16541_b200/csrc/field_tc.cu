@@ -209,7 +209,7 @@ constexpr uint32_t OF_A = (OF_B0 + 512 + 127) / 128 * 128;
 template <int NWG>
 __global__ void __launch_bounds__(NWG * 128, 1)
     k_offset_tc(fv_field f, const float4* __restrict__ xs, int64_t n, float eps_w, float4* __restrict__ out,
-                float* __restrict__ xfinal) {
+                float* __restrict__ xfinal, const int32_t* __restrict__ d_count) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[NWG];
   __shared__ uint32_t tmem_base;
@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(NWG * 128, 1)
   const uint32_t trow = tcol + ((uint32_t)((warp & 3) * 32) << 16);
   uint64_t* bar = &bars[wg];
   uint32_t phase = 0;
+  if (d_count) n = min((int64_t)*d_count, n);   // compacted foreground stream of the march
   const int64_t ntiles = (n + 127) / 128;
   for (int64_t tile = (int64_t)blockIdx.x * NWG + wg; tile < ntiles; tile += (int64_t)gridDim.x * NWG) {
     const int64_t s = tile * 128 + t;
@@ -293,7 +294,7 @@ constexpr uint32_t RA_A_BYTES = 128 * 64 * 2;            // 16 KB per warpgroup
 template <int NWG, bool BATCH>
 __global__ void __launch_bounds__(NWG * 128, 1)
     k_radiance_tc(fv_field f, fv_hash h, const float4* __restrict__ xf, int64_t n, float eps_w,
-                  float4* __restrict__ rgbs) {
+                  float4* __restrict__ rgbs, const int32_t* __restrict__ d_count, const int32_t* __restrict__ idx) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[NWG];
   __shared__ uint32_t tmem_base;
@@ -309,6 +310,7 @@ __global__ void __launch_bounds__(NWG * 128, 1)
   const uint32_t trow = tcol + ((uint32_t)((warp & 3) * 32) << 16);
   uint64_t* bar = &bars[wg];
   uint32_t phase = 0;
+  if (d_count) n = min((int64_t)*d_count, n);
   const int64_t ntiles = (n + 127) / 128;
   for (int64_t tile = (int64_t)blockIdx.x * NWG + wg; tile < ntiles; tile += (int64_t)gridDim.x * NWG) {
     const int64_t s = tile * 128 + t;
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(NWG * 128, 1)
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           float2 fv4[4];
-          hash_4levels(h, 4 * c, xn, fv4);
+          hash_4levels_paired(h, 4 * c, xn, fv4);
           uint32_t w[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) w[q] = tc::pack_half2(fg ? fv4[q].x : 0.f, fg ? fv4[q].y : 0.f);
@@ -360,7 +362,7 @@ __global__ void __launch_bounds__(NWG * 128, 1)
       if (fg)
         r = make_float4(sigmoidf_(o[0] + b2[0]), sigmoidf_(o[1] + b2[1]), sigmoidf_(o[2] + b2[2]),
                         softplusf_(o[3] + b2[3] - 1.f));
-      rgbs[s] = r;
+      rgbs[idx ? (int64_t)idx[s] : s] = r;   // scatter back to the full sample layout
     }
   }
   tc::fence_before();
@@ -368,63 +370,59 @@ __global__ void __launch_bounds__(NWG * 128, 1)
   if (warp == 0) tc::tmem_free<TCOLS>(tmem_base);
 }
 
-template <int NWG>
+// Tuned configuration (round-1 sweeps on B200, SS4): residual MLP with 2
+// warpgroups per SM (3 leaves no L1 and runs 2x slower), hash+radiance with 4 warpgroups
+// and 4-level batched gathers.
+constexpr int OFF_NWG = 2, RAD_NWG = 4;
+
+static int sm_count() {
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  return n_sm;
+}
+
 static void launch_offset(const fv_field* f, const float4* xs, int64_t n, float eps_w, float4* out, float* xfinal,
-                          int n_sm, cudaStream_t st) {
-  const size_t smem = OF_A + NWG * A_BYTES;
-  cudaFuncSetAttribute(k_offset_tc<NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                          const int32_t* d_count, cudaStream_t st) {
+  const size_t smem = OF_A + OFF_NWG * A_BYTES;
+  cudaFuncSetAttribute(k_offset_tc<OFF_NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = (n + 127) / 128;
-  const int grid = (int)std::min<int64_t>((ntiles + NWG - 1) / NWG, n_sm);
-  k_offset_tc<NWG><<<grid, NWG * 128, smem, st>>>(*f, xs, n, eps_w, out, xfinal);
+  const int grid = (int)std::min<int64_t>((ntiles + OFF_NWG - 1) / OFF_NWG, sm_count());
+  k_offset_tc<OFF_NWG><<<grid, OFF_NWG * 128, smem, st>>>(*f, xs, n, eps_w, out, xfinal, d_count);
 }
 
-template <int NWG, bool BATCH>
 static void launch_radiance(const fv_field* f, const fv_hash* h, const float4* xf, int64_t n, float eps_w,
-                            float4* rgbs, int n_sm, cudaStream_t st) {
-  const size_t smem = RA_A + NWG * RA_A_BYTES;
-  cudaFuncSetAttribute(k_radiance_tc<NWG, BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                            float4* rgbs, const int32_t* d_count, const int32_t* idx, cudaStream_t st) {
+  const size_t smem = RA_A + RAD_NWG * RA_A_BYTES;
+  cudaFuncSetAttribute(k_radiance_tc<RAD_NWG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = (n + 127) / 128;
-  const int grid = (int)std::min<int64_t>((ntiles + NWG - 1) / NWG, n_sm);
-  k_radiance_tc<NWG, BATCH><<<grid, NWG * 128, smem, st>>>(*f, *h, xf, n, eps_w, rgbs);
+  const int grid = (int)std::min<int64_t>((ntiles + RAD_NWG - 1) / RAD_NWG, sm_count());
+  k_radiance_tc<RAD_NWG, true><<<grid, RAD_NWG * 128, smem, st>>>(*f, *h, xf, n, eps_w, rgbs, d_count, idx);
 }
 
-// x_skel -> x_final (into rgbs as scratch) -> (c, sigma) in place.
+// x_skel -> x_final -> (c, sigma).  Dense form (d_count == NULL): x_final goes to rgbs as
+// scratch and the radiance kernel overwrites it in place.  Compacted form (render path):
+// xs is the march's foreground stream of *d_count samples (<= n), x_final overwrites it in
+// place and (c, sigma) are scattered to rgbs[idx[j]] in the full sample layout.
 int32_t field_fwd_tc(const fv_field* f, const fv_hash* h, const float4* xs, int64_t n, float eps_w, float4* rgbs,
-                     float* xfinal, cudaStream_t st) {
+                     float* xfinal, cudaStream_t st, const int32_t* d_count, const int32_t* idx,
+                     cudaEvent_t mid_event) {
   if (!f->d_tc_pack) return set_error(FV_EDIM, "field tc: d_tc_pack is NULL (call fv_field_pack)");
   if (!f->d_off_b0_eff) return set_error(FV_EDIM, "field tc: d_off_b0_eff is NULL (call fv_offset_bias)");
   if (h->n_levels * h->n_feat != 32 || f->pe_bands > 6)
     return set_error(FV_EUNSUPPORTED, "field tc: needs 16x2 hash features and <= 6 PE bands");
   if (n == 0) return FV_OK;
-  int dev = 0, n_sm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  // tuning knobs (experiments only): FV_OFF_NWG in 1..3, FV_RAD_VARIANT = <1|2|4|8><b|s>
-  static const char* ov = getenv("FV_OFF_NWG");
-  static const char* rv = getenv("FV_RAD_VARIANT");
-  const int onwg = ov ? atoi(ov) : 2;
-  const int rnwg = rv ? rv[0] - '0' : 4;
-  const bool batch = rv ? rv[1] == 'b' : true;
   const float4* src = xs;
   if (f->offset_enabled) {
-    if (onwg == 1) launch_offset<1>(f, xs, n, eps_w, rgbs, xfinal, n_sm, st);
-    else if (onwg == 3) launch_offset<3>(f, xs, n, eps_w, rgbs, xfinal, n_sm, st);
-    else launch_offset<2>(f, xs, n, eps_w, rgbs, xfinal, n_sm, st);
+    float4* dst = d_count ? const_cast<float4*>(xs) : rgbs;
+    launch_offset(f, xs, n, eps_w, dst, xfinal, d_count, st);
     if (int32_t e = check_launch("k_offset_tc")) return e;
-    src = rgbs;
+    src = dst;
   } else if (xfinal) {
     return set_error(FV_EUNSUPPORTED, "field tc: x_final output needs the residual stage enabled");
   }
-  switch (rnwg * 2 + (batch ? 1 : 0)) {
-    case 2: launch_radiance<1, false>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
-    case 3: launch_radiance<1, true>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
-    case 4: launch_radiance<2, false>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
-    case 5: launch_radiance<2, true>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
-    case 8: launch_radiance<4, false>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
-    case 16: launch_radiance<8, false>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
-    case 17: launch_radiance<8, true>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
-    default: launch_radiance<4, true>(f, h, src, n, eps_w, rgbs, n_sm, st); break;
-  }
+  if (mid_event) cudaEventRecord(mid_event, st);
+  launch_radiance(f, h, src, n, eps_w, rgbs, d_count, idx, st);
   return check_launch("k_radiance_tc");
 }
 
@@ -442,10 +440,7 @@ extern "C" int32_t fv_residual_offset(const fv_field* field, const float* d_xs, 
   if (field->precision != 1 || !field->d_tc_pack || !field->d_off_b0_eff)
     return set_error(FV_EUNSUPPORTED, "fv_residual_offset: tensor-core path only (precision 1, packed weights)");
   if (n == 0) return FV_OK;
-  int dev = 0, n_sm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  launch_offset<2>(field, (const float4*)d_xs, n, eps_w, (float4*)d_out, nullptr, n_sm, (cudaStream_t)stream);
+  launch_offset(field, (const float4*)d_xs, n, eps_w, (float4*)d_out, nullptr, nullptr, (cudaStream_t)stream);
   return check_launch("fv_residual_offset");
 }
 

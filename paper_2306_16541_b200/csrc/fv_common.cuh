@@ -308,6 +308,72 @@ __device__ __forceinline__ void hash_4levels(const fv_hash& h, int l0, const flo
   }
 }
 
+// Lane-paired gathers (fp16 or fp32 table): lanes (2p, 2p+1) serve the samples of both
+// lanes; lane parity a = lane & 1 fetches the x-corner a of each sample.  A cell's two
+// x-corners differ only in low index bits (same 128-byte line ~99% of the time), so in one
+// warp instruction 16 samples x 2 corners touch 16 lines instead of 32 -- half the L1
+// wavefronts of the per-sample form at the same load count; one shuffle per feature adds the
+// partner's partial.  Accumulation order (a-partials then sum) differs from the oracle's
+// (a,b,c) order: used only where features are rounded to fp16 (tensor-core field).
+__device__ __forceinline__ void hash_4levels_paired(const fv_hash& h, int l0, const float (&xn_self)[3],
+                                                    float2 (&out)[4]) {
+  const uint32_t maskT = (1u << h.log2_T) - 1u;
+  const int lane = threadIdx.x & 31;
+  const uint32_t a = lane & 1u;
+  float xA[3], xB[3];   // A = even lane's sample, B = odd lane's sample
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float other = __shfl_xor_sync(0xffffffffu, xn_self[j], 1);
+    xA[j] = a ? other : xn_self[j];
+    xB[j] = a ? xn_self[j] : other;
+  }
+  uint32_t iA[16], iB[16];
+  float fA[4][3], fB[4][3];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int l = l0 + q < h.n_levels ? l0 + q : h.n_levels - 1;
+    HashCell cA, cB;
+    hash_level_cell(xA, h.res[l], cA);
+    hash_level_cell(xB, h.res[l], cB);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) { fA[q][j] = cA.f[j]; fB[q][j] = cB.f[j]; }
+#pragma unroll
+    for (int bc = 0; bc < 4; ++bc) {
+      iA[q * 4 + bc] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, cA.i0[0] + a, cA.i0[1] + (bc >> 1),
+                                                cA.i0[2] + (bc & 1));
+      iB[q * 4 + bc] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, cB.i0[0] + a, cB.i0[1] + (bc >> 1),
+                                                cB.i0[2] + (bc & 1));
+    }
+  }
+  float2 vA[16], vB[16];
+  if (h.table_half) {
+    const __half2* t = reinterpret_cast<const __half2*>(h.d_table);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { vA[k] = __half22float2(__ldg(t + iA[k])); vB[k] = __half22float2(__ldg(t + iB[k])); }
+  } else {
+    const float2* t = reinterpret_cast<const float2*>(h.d_table);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { vA[k] = __ldg(t + iA[k]); vB[k] = __ldg(t + iB[k]); }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float2 pA = make_float2(0.f, 0.f), pB = make_float2(0.f, 0.f);
+    const float wxA = a ? fA[q][0] : 1.f - fA[q][0], wxB = a ? fB[q][0] : 1.f - fB[q][0];
+#pragma unroll
+    for (int bc = 0; bc < 4; ++bc) {
+      const float wA = wxA * ((bc >> 1) ? fA[q][1] : 1.f - fA[q][1]) * ((bc & 1) ? fA[q][2] : 1.f - fA[q][2]);
+      const float wB = wxB * ((bc >> 1) ? fB[q][1] : 1.f - fB[q][1]) * ((bc & 1) ? fB[q][2] : 1.f - fB[q][2]);
+      pA.x = fmaf(wA, vA[q * 4 + bc].x, pA.x); pA.y = fmaf(wA, vA[q * 4 + bc].y, pA.y);
+      pB.x = fmaf(wB, vB[q * 4 + bc].x, pB.x); pB.y = fmaf(wB, vB[q * 4 + bc].y, pB.y);
+    }
+    // even lane keeps sample A: own a=0 partial of A + partner's a=1 partial of A
+    const float sx = a ? pA.x : pB.x, sy = a ? pA.y : pB.y;      // what the partner needs
+    const float rx = __shfl_xor_sync(0xffffffffu, sx, 1), ry = __shfl_xor_sync(0xffffffffu, sy, 1);
+    const float2 mine = a ? pB : pA;
+    out[q] = l0 + q < h.n_levels ? make_float2(mine.x + rx, mine.y + ry) : make_float2(0.f, 0.f);
+  }
+}
+
 // ---------------------------------------------------------------- heads
 __device__ __forceinline__ float sigmoidf_(float x) {
   if (x >= 0.f) return 1.f / (1.f + expf(-x));

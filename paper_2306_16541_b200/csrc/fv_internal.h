@@ -15,13 +15,17 @@ int32_t field_fwd_f32(const fv_field* f, const fv_hash* h, const float4* xs, int
                       float* xfinal, void* work, size_t work_bytes, cudaStream_t st);
 size_t field_f32_work_bytes(int64_t n);
 int32_t field_fwd_tc(const fv_field* f, const fv_hash* h, const float4* xs, int64_t n, float eps_w, float4* rgbs,
-                     float* xfinal, cudaStream_t st);
+                     float* xfinal, cudaStream_t st, const int32_t* d_count = nullptr, const int32_t* idx = nullptr,
+                     cudaEvent_t mid_event = nullptr);
+int32_t march_compact(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays, float* lik,
+                      float* delta, float4* xsc, int32_t* idx, int32_t* count, int32_t* ray_count, cudaStream_t st);
 struct CompIn {
   const float4* rgbs;   // [c, sigma] per sample
   const float* delta;   // per sample
   const float* lik;     // per sample, stride lik_stride floats
   int lik_stride;
   bool blocked;         // sample layout: ray-block-major (render) or ray-major [R][N]
+  bool skip_bg = false; // L <= eps_w samples are skipped (their rgbs slot is unwritten)
 };
 int32_t composite_fwd(const CompIn& in, int64_t n_rays, int n, const float* bg, float eps_w, float eps_t,
                       const int32_t* out_pix, float* rgb, float* alpha, float* trans, cudaStream_t st);

@@ -59,24 +59,39 @@ __global__ void k_warp_fwd(fv_warp w, float eps_w, const float* __restrict__ x, 
   fg[p] = L > eps_w;
 }
 
+// Compacted foreground stream written by the render march (COMPACT): fg samples only.
+struct Compact {
+  float* lik;        // [S] likelihood of every sample (0 outside box / empty cell)
+  float4* xsc;       // [<= S] (x_skel, L) of foreground samples
+  int32_t* idx;      // [<= S] their sample index
+  int32_t* count;    // device counter (zeroed before the launch)
+};
+
 // One thread per sample (ray-block-major layout).  Writes xs[s] = (x_skel, L) with L = 0
 // for samples outside the box or in empty occupancy cells, delta[s], optional x[s].
+// COMPACT: writes lik[s] instead of xs[s] and appends each foreground sample (L > eps_w)
+// to the compacted stream -- one atomicAdd per 128-thread block, warp ballots inside, so
+// a block's survivors stay contiguous (4 depths x 32 neighbouring rays) and the field
+// kernels skip background samples entirely.
+template <bool COMPACT>
 __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, fv_warp w, int64_t n_rays,
                                                     float4* __restrict__ xs_out, float* __restrict__ delta_out,
-                                                    float* __restrict__ x_out, int32_t* __restrict__ count_out) {
+                                                    float* __restrict__ x_out, int32_t* __restrict__ count_out,
+                                                    Compact cmp) {
   __shared__ float sg[FV_MAX_BONES * 12];
+  __shared__ int32_t wcount[4], wbase;
   for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
   __syncthreads();
   const int N = m.n_samples;
   const int64_t total = padded_rays(n_rays) * N;
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s >= total) return;
-  int64_t ray; int32_t i;
-  sample_coords(s, N, ray, i);
+  if (!COMPACT && s >= total) return;
+  int64_t ray = n_rays; int32_t i = 0;
+  if (s < total) sample_coords(s, N, ray, i);
   float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
   float delta = 0.f;
   bool hit = false;
-  if (ray < n_rays) {
+  if (s < total && ray < n_rays) {
     const int32_t pix = m.d_pix ? m.d_pix[ray] : (int32_t)(m.pix_offset + ray);
     const Ray r = make_ray(cam, pix);
     float t0, t1;
@@ -106,11 +121,32 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
       x_out[3 * s] = x_out[3 * s + 1] = x_out[3 * s + 2] = 0.f;
     }
     if (i == 0 && count_out) count_out[ray] = hit ? N : 0;
-  } else if (x_out) {
+  } else if (x_out && s < total) {
     x_out[3 * s] = x_out[3 * s + 1] = x_out[3 * s + 2] = 0.f;
   }
-  xs_out[s] = out;
-  delta_out[s] = delta;
+  if (!COMPACT) {
+    xs_out[s] = out;
+    delta_out[s] = delta;
+    return;
+  }
+  const bool fg = s < total && out.w > m.eps_w;
+  const uint32_t ballot = __ballot_sync(0xffffffffu, fg);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) wcount[wid] = __popc(ballot);
+  __syncthreads();
+  if (threadIdx.x == 0) wbase = atomicAdd(cmp.count, wcount[0] + wcount[1] + wcount[2] + wcount[3]);
+  __syncthreads();
+  if (s < total) {
+    cmp.lik[s] = out.w;
+    delta_out[s] = delta;
+  }
+  if (fg) {
+    int off = wbase;
+    for (int q = 0; q < wid; ++q) off += wcount[q];
+    off += __popc(ballot & ((1u << lane) - 1u));
+    cmp.xsc[off] = out;
+    cmp.idx[off] = (int32_t)s;
+  }
 }
 
 // d x_skel -> d W^c (C,G,G,G) via dw_i = <dxs, p_i - x_skel>/L and the trilinear scatter.
@@ -194,7 +230,19 @@ extern "C" int32_t fv_march_warp(const fv_camera* cam, const fv_march* march, co
   if (warp->n_bones < 1 || warp->n_bones > FV_MAX_BONES) return set_error(FV_EDIM, "fv_march_warp: bad bone count");
   if (n_rays == 0) return FV_OK;
   const int64_t total = padded_rays(n_rays) * march->n_samples;
-  k_march_warp<<<(unsigned)((total + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-      *cam, *march, *warp, n_rays, (float4*)d_xs, d_delta, d_x, d_count);
+  k_march_warp<false><<<(unsigned)((total + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      *cam, *march, *warp, n_rays, (float4*)d_xs, d_delta, d_x, d_count, Compact{});
   return check_launch("fv_march_warp");
 }
+
+namespace fv {
+// render-path march: likelihood per sample + compacted foreground stream (count zeroed here)
+int32_t march_compact(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays, float* lik,
+                      float* delta, float4* xsc, int32_t* idx, int32_t* count, int32_t* ray_count, cudaStream_t st) {
+  const int64_t total = padded_rays(n_rays) * march->n_samples;
+  cudaMemsetAsync(count, 0, sizeof(int32_t), st);
+  k_march_warp<true><<<(unsigned)((total + 127) / 128), 128, 0, st>>>(*cam, *march, *warp, n_rays, nullptr, delta,
+                                                                      nullptr, ray_count, Compact{lik, xsc, idx, count});
+  return check_launch("march_compact");
+}
+}  // namespace fv
