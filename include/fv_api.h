@@ -34,6 +34,7 @@ extern "C" {
 #define FV_EUNSUPPORTED 4
 
 #define FV_MAX_BONES 32
+#define FV_MAX_VOL_RES 128
 #define FV_MAX_LEVELS 16
 
 /* ---- parameter blocks (plain data, host memory) ----------------------------------- */
@@ -62,7 +63,7 @@ typedef struct fv_march {
 
 typedef struct fv_warp {
   int32_t n_bones;                /* K <= FV_MAX_BONES                                 */
-  int32_t vol_res;                /* G (32)                                            */
+  int32_t vol_res;                /* G (32), 2 <= G <= FV_MAX_VOL_RES                  */
   int32_t vol_half;               /* corner-packed volume dtype: 0 fp32, 1 fp16        */
   const void* d_vol_packed;       /* [K][(G+1)^3][8] corner-packed weights             */
   const float* d_g;               /* [K][12] G_i = (R row-major 9, t 3), device        */

@@ -12,9 +12,16 @@
   ``x_skel = sum_i (w_i/L) p_i`` (``weighted_sum0``, ``ad:456-467``), evaluated as
   ``(sum_i w_i p_i) / L`` (same value, the kernel's rounding order).
 
-Every function takes a ``dtype``; with float32 each elementwise operation is one
-rounded float32 op in the order the sm_100a warp kernel evaluates it, so the per-bone
-weights, the likelihood and the foreground mask compare bit-exactly with the kernel.
+Every function takes a ``dtype``.  float64 follows the reference's formulas and op order
+(``ad:748-773``, ``sk:171-172``).  float32 is the sm_100a kernel's specification: every
+op is one rounded float32 op in the kernel's order, and the kernel uses fused
+multiply-adds (one rounding) for ``p = R x + t``, ``u = (p - bmin) scale + 1``, the
+trilinear blend (written as seven lerps ``v0 + f (v1 - v0)``, the same polynomial as
+``ad:767-773``) and the ``sum_i w_i p_i`` accumulation.  ``fma32`` restates a
+single-rounded float32 FMA: the float32 product is exact in x87 extended precision (48 of
+64 mantissa bits), so only the final rounding to float32 is visible (a double-rounding
+tie needs 40 trailing bits to line up, ~2^-40 per op).  Per-bone weights, the likelihood
+and the foreground mask therefore compare bit-exactly with the kernel.
 """
 
 from __future__ import annotations
@@ -22,6 +29,21 @@ from __future__ import annotations
 import numpy as np
 
 EPS_W = 1e-4
+
+
+_XP = np.longdouble
+assert np.finfo(_XP).nmant >= 63, "fma32 needs x87 extended precision (x86-64 long double)"
+
+
+def fma32(a, b, c):
+    """float32 a*b + c with a single rounding (CUDA ``__fmaf_rn``)."""
+    return (np.asarray(a, np.float32).astype(_XP) * np.asarray(b, np.float32).astype(_XP)
+            + np.asarray(c, np.float32).astype(_XP)).astype(np.float32)
+
+
+def _lerp32(v0, v1, f):
+    """v0 + f*(v1 - v0) as the kernel evaluates it: fma(f, v1 - v0, v0)."""
+    return fma32(f, (v1 - v0).astype(np.float32), v0)
 
 
 def softmax0(a):
@@ -36,7 +58,10 @@ def softmax0_bwd(out, g):
 
 
 def _grid_coords(p, gsz, bmin, scale, dt):
-    u = (((p - bmin).astype(dt) * scale).astype(dt) + dt(1.0)).astype(dt)
+    if dt is np.float32:
+        u = fma32((p - bmin).astype(dt), np.broadcast_to(scale, p.shape), np.float32(1.0))
+    else:
+        u = (((p - bmin).astype(dt) * scale).astype(dt) + dt(1.0)).astype(dt)
     inside = np.all((u >= 0.0) & (u <= dt(gsz + 1)), axis=-1)
     i0 = np.clip(np.floor(u), 0, gsz).astype(np.int64)
     f = (u - i0.astype(dt)).astype(dt)
@@ -60,6 +85,13 @@ def sample_bone_channels(vol, pts, box_min, box_max, dtype=None):
     wy = ((dt(1.0) - f[..., 1]).astype(dt), f[..., 1])
     wz = ((dt(1.0) - f[..., 2]).astype(dt), f[..., 2])
     ix, iy, iz = i0[..., 0], i0[..., 1], i0[..., 2]
+    if dt is np.float32:
+        cv = [vp[ch, ix + a, iy + b, iz + c] for a in (0, 1) for b in (0, 1) for c in (0, 1)]
+        fx, fy, fz = f[..., 0], f[..., 1], f[..., 2]
+        c00, c01 = _lerp32(cv[0], cv[1], fz), _lerp32(cv[2], cv[3], fz)
+        c10, c11 = _lerp32(cv[4], cv[5], fz), _lerp32(cv[6], cv[7], fz)
+        out = _lerp32(_lerp32(c00, c01, fy), _lerp32(c10, c11, fy), fx)
+        return np.where(inside, out, dt(0.0)).astype(dt)
     out = np.zeros(p.shape[:2], dtype=dt)
     for a in (0, 1):
         for b in (0, 1):
@@ -115,12 +147,22 @@ def sample_bone_channels_bwd(vol_shape, pts, box_min, box_max, g, dtype=np.float
 
 
 def bone_points(x, g_r, g_t, dtype=np.float32):
-    """p_i = x @ R_i^T + t_i for every bone, (K,N,3), kernel op order."""
+    """p_i = x @ R_i^T + t_i for every bone, (K,N,3), kernel op order.
+
+    float32: ``fma(R2, x2, fma(R1, x1, R0*x0)) + t`` per row (the kernel's FMA chain).
+    """
     dt = np.dtype(dtype).type
     x = np.asarray(x, dtype=dt)
     r = np.asarray(g_r, dtype=dt)
     t = np.asarray(g_t, dtype=dt)
     out = np.empty((r.shape[0], x.shape[0], 3), dtype=dt)
+    if dt is np.float32:
+        for j in range(3):
+            acc = (r[:, j, 0][:, None] * x[None, :, 0]).astype(dt)
+            acc = fma32(r[:, j, 1][:, None], x[None, :, 1], acc)
+            acc = fma32(r[:, j, 2][:, None], x[None, :, 2], acc)
+            out[:, :, j] = (acc + t[:, j][:, None]).astype(dt)
+        return out
     for j in range(3):
         acc = (r[:, j, 0][:, None] * x[None, :, 0]).astype(dt)
         acc = (acc + (r[:, j, 1][:, None] * x[None, :, 1]).astype(dt)).astype(dt)
@@ -147,7 +189,10 @@ def skeleton_warp(x, g_r, g_t, vol, box_min, box_max, eps_w=EPS_W, dtype=np.floa
     # sum_i (w_i/L) p_i evaluated as (sum_i w_i p_i) / L -- the kernel's order
     acc = np.zeros((x.shape[0], 3), dtype=dt)
     for i in range(k):
-        acc = (acc + (w[i][:, None] * p[i]).astype(dt)).astype(dt)
+        if dt is np.float32:
+            acc = fma32(w[i][:, None], p[i], acc)
+        else:
+            acc = (acc + (w[i][:, None] * p[i]).astype(dt)).astype(dt)
     xs = (acc / safe[:, None]).astype(dt)
     xs = np.where(fg[:, None], xs, dt(0.0)).astype(dt)
     return {"x_skel": xs, "L": lik, "fg": fg, "w": w, "p": p}

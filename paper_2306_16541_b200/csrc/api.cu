@@ -66,7 +66,7 @@ int32_t field_fwd(const fv_field* f, const fv_hash* h, const float4* xs, int64_t
 
 // occupancy probe points: cell c (x-major), sub-point j in 2x2x2
 __global__ void k_occ_points(fv_march m, fv_warp w, float4* __restrict__ xs) {
-  __shared__ float sg[FV_MAX_BONES * 12];
+  __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
   for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
   __syncthreads();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -142,6 +142,7 @@ static int32_t render_fwd(const fv_camera* cam, const fv_march* march, const fv_
   if (!cam || !march || !warp || !hash || !field || n_rays < 0 || march->n_samples < 1)
     return set_error(FV_EDIM, "fv_render_fwd: bad arguments");
   if (int32_t e = check_hash(hash)) return e;
+  if (int32_t e = check_warp(warp)) return e;
   if (n_rays == 0) return FV_OK;
   const int N = march->n_samples;
   const int64_t S = padded_rays(n_rays) * N;
@@ -222,6 +223,7 @@ extern "C" int32_t fv_occupancy_build(const fv_march* march, const fv_warp* warp
                                       const fv_field* field, float threshold, void* d_work, size_t work_bytes,
                                       uint32_t* d_occ, void* stream) {
   if (!march || !warp || !hash || !field || !d_occ) return set_error(FV_EDIM, "fv_occupancy_build: null argument");
+  if (int32_t e = check_warp(warp)) return e;
   if (work_bytes < fv_occupancy_workspace_bytes(field->precision))
     return set_error(FV_EDIM, "fv_occupancy_build: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;

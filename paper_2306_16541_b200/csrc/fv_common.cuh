@@ -114,7 +114,7 @@ __device__ __forceinline__ bool warp_cell(const fv_warp& w, const float (&p)[3],
   const float gp1 = (float)(w.vol_res + 1);
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
-    const float u = __fadd_rn(__fmul_rn(__fsub_rn(p[j], w.wbox_min[j]), w.wscale[j]), 1.0f);
+    const float u = __fmaf_rn(__fsub_rn(p[j], w.wbox_min[j]), w.wscale[j], 1.0f);
     inside = inside && (u >= 0.0f) && (u <= gp1);
     float fl = floorf(u);
     fl = fl < 0.f ? 0.f : (fl > (float)w.vol_res ? (float)w.vol_res : fl);
@@ -124,32 +124,30 @@ __device__ __forceinline__ bool warp_cell(const fv_warp& w, const float (&p)[3],
   return inside;
 }
 
-__device__ __forceinline__ float trilerp8(const float (&f)[3], const float (&cv)[8]) {
-  const float wx[2] = {__fsub_rn(1.0f, f[0]), f[0]};
-  const float wy[2] = {__fsub_rn(1.0f, f[1]), f[1]};
-  const float wz[2] = {__fsub_rn(1.0f, f[2]), f[2]};
-  float acc = 0.0f;
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(__fmul_rn(wx[a], wy[b]), wz[c]), cv[a * 4 + b * 2 + c]));
-  return acc;
+// Trilinear blend of ad:767-773 as seven lerps v0 + f (v1 - v0), each one FMA
+// (oracle.warp._lerp32): z, then y, then x.
+__device__ __forceinline__ float lerp_fma(float v0, float v1, float t) {
+  return __fmaf_rn(t, __fsub_rn(v1, v0), v0);
 }
 
-// p = x @ R^T + t (row convention, sk:171-172), op order of oracle.warp.bone_points
+__device__ __forceinline__ float trilerp8(const float (&f)[3], const float (&cv)[8]) {
+  const float c00 = lerp_fma(cv[0], cv[1], f[2]), c01 = lerp_fma(cv[2], cv[3], f[2]);
+  const float c10 = lerp_fma(cv[4], cv[5], f[2]), c11 = lerp_fma(cv[6], cv[7], f[2]);
+  return lerp_fma(lerp_fma(c00, c01, f[1]), lerp_fma(c10, c11, f[1]), f[0]);
+}
+
+// p = x @ R^T + t (row convention, sk:171-172), FMA chain of oracle.warp.bone_points
 __device__ __forceinline__ void bone_point(const float* g, float x0, float x1, float x2, float (&p)[3]) {
 #pragma unroll
   for (int j = 0; j < 3; ++j)
-    p[j] = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(g[3 * j], x0), __fmul_rn(g[3 * j + 1], x1)),
-                               __fmul_rn(g[3 * j + 2], x2)), g[9 + j]);
+    p[j] = __fadd_rn(__fmaf_rn(g[3 * j + 2], x2, __fmaf_rn(g[3 * j + 1], x1, __fmul_rn(g[3 * j], x0))),
+                     g[9 + j]);
 }
 
+// <= 32 bones x 129^3 cells fits int32 (fv_warp_pack checks the volume size)
 __device__ __forceinline__ size_t vol_cell_index(int bone, int res, const int (&i0)[3]) {
   const int s = res + 1;
-  return ((size_t)(bone * s + i0[0]) * s + i0[1]) * s + i0[2];
+  return (size_t)(unsigned)(((bone * s + i0[0]) * s + i0[1]) * s + i0[2]);
 }
 
 // Full skeleton warp of one point with G in shared memory (sg: K*12 floats).
@@ -163,7 +161,12 @@ __device__ __forceinline__ float warp_point(const fv_warp& w, const float* sg, f
 #pragma unroll 4
   for (int i = 0; i < K; ++i) {
     float p[3];
-    bone_point(sg + 12 * i, x0, x1, x2, p);
+    {
+      const float4* g4 = reinterpret_cast<const float4*>(sg + 12 * i);   // 48-byte rows
+      const float4 a = g4[0], b = g4[1], c = g4[2];
+      const float g[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+      bone_point(g, x0, x1, x2, p);
+    }
     int i0[3]; float f[3];
     float wi = 0.f;
     if (warp_cell(w, p, i0, f)) {
@@ -173,9 +176,9 @@ __device__ __forceinline__ float warp_point(const fv_warp& w, const float* sg, f
     }
     if (STORE_W) w_out[(size_t)i * w_stride] = wi;
     lik = __fadd_rn(lik, wi);
-    s0 = __fadd_rn(s0, __fmul_rn(wi, p[0]));
-    s1 = __fadd_rn(s1, __fmul_rn(wi, p[1]));
-    s2 = __fadd_rn(s2, __fmul_rn(wi, p[2]));
+    s0 = __fmaf_rn(wi, p[0], s0);
+    s1 = __fmaf_rn(wi, p[1], s1);
+    s2 = __fmaf_rn(wi, p[2], s2);
   }
   if (lik > eps_w) {
     xs[0] = __fdiv_rn(s0, lik); xs[1] = __fdiv_rn(s1, lik); xs[2] = __fdiv_rn(s2, lik);

@@ -11,6 +11,8 @@ struct PeW { float w[8]; };
 int32_t set_error(int32_t code, const char* msg);
 int32_t check_launch(const char* where);
 int32_t check_hash(const fv_hash* h);
+// 1 <= K <= FV_MAX_BONES, 2 <= G <= FV_MAX_VOL_RES (packed cell index fits int32)
+int32_t check_warp(const fv_warp* w);
 int32_t field_fwd_f32(const fv_field* f, const fv_hash* h, const float4* xs, int64_t n, float eps_w, float4* rgbs,
                       float* xfinal, void* work, size_t work_bytes, cudaStream_t st);
 size_t field_f32_work_bytes(int64_t n);

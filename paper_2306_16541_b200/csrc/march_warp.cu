@@ -45,7 +45,7 @@ __global__ void k_warp_pack(const float* __restrict__ vol, int K, int G, T* __re
 __global__ void k_warp_fwd(fv_warp w, float eps_w, const float* __restrict__ x, int64_t n,
                            float* __restrict__ xskel, float* __restrict__ lik, uint8_t* __restrict__ fg,
                            float* __restrict__ wout) {
-  __shared__ float sg[FV_MAX_BONES * 12];
+  __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
   for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
   __syncthreads();
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
                                                     float4* __restrict__ xs_out, float* __restrict__ delta_out,
                                                     float* __restrict__ x_out, int32_t* __restrict__ count_out,
                                                     Compact cmp) {
-  __shared__ float sg[FV_MAX_BONES * 12];
+  __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
   __shared__ int32_t wcount[4], wbase;
   for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
   __syncthreads();
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
 // d x_skel -> d W^c (C,G,G,G) via dw_i = <dxs, p_i - x_skel>/L and the trilinear scatter.
 __global__ void k_warp_bwd(fv_warp w, float eps_w, const float* __restrict__ x, int64_t n,
                            const float* __restrict__ dxs, float* __restrict__ dvol) {
-  __shared__ float sg[FV_MAX_BONES * 12];
+  __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
   for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
   __syncthreads();
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -188,13 +188,22 @@ __global__ void k_warp_bwd(fv_warp w, float eps_w, const float* __restrict__ x, 
 
 }  // namespace fv
 
+namespace fv {
+int32_t check_warp(const fv_warp* w) {
+  if (!w) return set_error(FV_EDIM, "null fv_warp");
+  if (w->n_bones < 1 || w->n_bones > FV_MAX_BONES) return set_error(FV_EDIM, "fv_warp: bad bone count");
+  if (w->vol_res < 2 || w->vol_res > FV_MAX_VOL_RES) return set_error(FV_EDIM, "fv_warp: bad volume resolution");
+  return FV_OK;
+}
+}  // namespace fv
+
 using namespace fv;
 
 extern "C" int32_t fv_warp_pack(const float* d_vol, int32_t channels, const fv_warp* warp, void* d_vol_packed,
                                 void* stream) {
   if (!warp || !d_vol || !d_vol_packed) return set_error(FV_EDIM, "fv_warp_pack: null argument");
-  if (warp->n_bones < 1 || warp->n_bones > FV_MAX_BONES || warp->n_bones > channels || warp->vol_res < 2)
-    return set_error(FV_EDIM, "fv_warp_pack: bad bone count / resolution");
+  if (int32_t e = check_warp(warp)) return e;
+  if (warp->n_bones > channels) return set_error(FV_EDIM, "fv_warp_pack: more bones than volume channels");
   const int64_t cells = (int64_t)warp->n_bones * (warp->vol_res + 1) * (warp->vol_res + 1) * (warp->vol_res + 1);
   const int grid = (int)std::min<int64_t>((cells + 255) / 256, 148 * 16);
   cudaStream_t st = (cudaStream_t)stream;
@@ -208,7 +217,7 @@ extern "C" int32_t fv_warp_pack(const float* d_vol, int32_t channels, const fv_w
 extern "C" int32_t fv_warp_fwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n, float* d_xskel,
                                float* d_lik, uint8_t* d_fg, float* d_w, void* stream) {
   if (!warp || n < 0) return set_error(FV_EDIM, "fv_warp_fwd: bad arguments");
-  if (warp->n_bones < 1 || warp->n_bones > FV_MAX_BONES) return set_error(FV_EDIM, "fv_warp_fwd: bad bone count");
+  if (int32_t e = check_warp(warp)) return e;
   if (n == 0) return FV_OK;
   k_warp_fwd<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*warp, eps_w, d_x, n, d_xskel, d_lik,
                                                                              d_fg, d_w);
@@ -218,6 +227,7 @@ extern "C" int32_t fv_warp_fwd(const fv_warp* warp, float eps_w, const float* d_
 extern "C" int32_t fv_warp_bwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
                                const float* d_dxskel, float* d_dvol, void* stream) {
   if (!warp || n < 0) return set_error(FV_EDIM, "fv_warp_bwd: bad arguments");
+  if (int32_t e = check_warp(warp)) return e;
   if (n == 0) return FV_OK;
   k_warp_bwd<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*warp, eps_w, d_x, n, d_dxskel, d_dvol);
   return check_launch("fv_warp_bwd");
@@ -227,7 +237,7 @@ extern "C" int32_t fv_march_warp(const fv_camera* cam, const fv_march* march, co
                                  float* d_xs, float* d_delta, float* d_x, int32_t* d_count, void* stream) {
   if (!cam || !march || !warp || n_rays < 0 || march->n_samples < 1)
     return set_error(FV_EDIM, "fv_march_warp: bad arguments");
-  if (warp->n_bones < 1 || warp->n_bones > FV_MAX_BONES) return set_error(FV_EDIM, "fv_march_warp: bad bone count");
+  if (int32_t e = check_warp(warp)) return e;
   if (n_rays == 0) return FV_OK;
   const int64_t total = padded_rays(n_rays) * march->n_samples;
   k_march_warp<false><<<(unsigned)((total + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
