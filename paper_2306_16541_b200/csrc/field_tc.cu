@@ -29,30 +29,32 @@
 namespace fv {
 
 // ---- weight pack layout (bytes) ------------------------------------------------------
-constexpr uint32_t PK_OFF0 = 0;                      // [128 x 48]
-constexpr uint32_t PK_OFF1 = PK_OFF0 + 128 * 48 * 2;  // [128 x 128]
-constexpr uint32_t PK_OFF2 = PK_OFF1 + 128 * 128 * 2;
-constexpr uint32_t PK_OFF3 = PK_OFF2 + 128 * 128 * 2;
-constexpr uint32_t PK_OFF4 = PK_OFF3 + 128 * 128 * 2;  // [16 x 128]
-constexpr uint32_t PK_RAD0 = PK_OFF4 + 16 * 128 * 2;   // [64 x 32]
-constexpr uint32_t PK_RAD1 = PK_RAD0 + 64 * 32 * 2;    // [64 x 64]
-constexpr uint32_t PK_RAD2 = PK_RAD1 + 64 * 64 * 2;    // [16 x 64]
-constexpr uint32_t PK_WEND = PK_RAD2 + 16 * 64 * 2;    // 129024
+// Hidden offset layers carry their bias inside the GEMM: K = 128 activations + 16 bias
+// rows, rows 128/129 = fp16 hi/lo split of the fp32 bias (b - hi(b) in fp16: ~2^-22
+// relative), multiplied by A columns 128/129 = 1.0.  Layer 0 uses the posenc pad columns
+// 46/47 the same way for the per-frame b0' (patched into the smem copy by the kernel).
+constexpr uint32_t OF_KH = 144;                           // hidden-layer K (128 + bias group)
+constexpr uint32_t PK_OFF0 = 0;                           // [128 x 48]
+constexpr uint32_t PK_OFF1 = PK_OFF0 + 128 * 48 * 2;      // [128 x 144]
+constexpr uint32_t PK_OFF2 = PK_OFF1 + 128 * OF_KH * 2;
+constexpr uint32_t PK_OFF3 = PK_OFF2 + 128 * OF_KH * 2;
+constexpr uint32_t PK_OFF4 = PK_OFF3 + 128 * OF_KH * 2;   // [16 x 128]
+constexpr uint32_t PK_RAD0 = PK_OFF4 + 16 * 128 * 2;      // [64 x 32]
+constexpr uint32_t PK_RAD1 = PK_RAD0 + 64 * 32 * 2;       // [64 x 64]
+constexpr uint32_t PK_RAD2 = PK_RAD1 + 64 * 64 * 2;       // [16 x 64]
+constexpr uint32_t PK_WEND = PK_RAD2 + 16 * 64 * 2;       // 141312
 // fp32 biases: off b1,b2,b3 (128 each), off b4 (16), rad b0 (64), rad b1 (64), rad b2 (16)
 constexpr uint32_t BI_OFF1 = 0, BI_OFF2 = 128, BI_OFF3 = 256, BI_OFF4 = 384, BI_RAD0 = 400, BI_RAD1 = 464,
                    BI_RAD2 = 528, BI_END = 544;
-constexpr uint32_t PK_BYTES = PK_WEND + BI_END * 4;   // 131200
-constexpr uint32_t SM_B0 = PK_BYTES;                  // 128 floats (per-frame b0')
-constexpr uint32_t SM_A = SM_B0 + 512;                // 131712, 128-B aligned
-constexpr uint32_t A_BYTES = 128 * 128 * 2;           // 32 KB per warpgroup
+constexpr uint32_t PK_BYTES = PK_WEND + BI_END * 4;       // 143488
 
 struct PackLayer { uint32_t off; int N, K, n_true, k_true; };
 
 // (in,out) fp32 weight -> B operand [N rows x K] fp16, K-chunk-major (tc_sm100.cuh).
 __global__ void k_field_pack(fv_field f, uint8_t* __restrict__ pack) {
   const PackLayer L[8] = {
-      {PK_OFF0, 128, 48, 128, 3 + 6 * f.pe_bands}, {PK_OFF1, 128, 128, 128, 128}, {PK_OFF2, 128, 128, 128, 128},
-      {PK_OFF3, 128, 128, 128, 128},              {PK_OFF4, 16, 128, 3, 128},     {PK_RAD0, 64, 32, 64, 32},
+      {PK_OFF0, 128, 48, 128, 3 + 6 * f.pe_bands}, {PK_OFF1, 128, OF_KH, 128, 128}, {PK_OFF2, 128, OF_KH, 128, 128},
+      {PK_OFF3, 128, OF_KH, 128, 128},            {PK_OFF4, 16, 128, 3, 128},       {PK_RAD0, 64, 32, 64, 32},
       {PK_RAD1, 64, 64, 64, 64},                  {PK_RAD2, 16, 64, 4, 64}};
   const float* W[8] = {f.d_off_w[0], f.d_off_w[1], f.d_off_w[2], f.d_off_w[3], f.d_off_w[4],
                        f.d_rad_w[0], f.d_rad_w[1], f.d_rad_w[2]};
@@ -67,6 +69,11 @@ __global__ void k_field_pack(fv_field f, uint8_t* __restrict__ pack) {
       const int k = 8 * c + j;
       const float v = (k < pl.k_true && nrow < pl.n_true) ? W[layer][(int64_t)k * pl.n_true + nrow] : 0.f;
       hv[j] = __float2half_rn(v);
+      if (layer >= 1 && layer <= 3 && k >= 128) {   // bias rows (hi, lo) of the hidden layers
+        const float b = f.d_off_b[layer][nrow];
+        const __half hi = __float2half_rn(b);
+        hv[j] = k == 128 ? hi : (k == 129 ? __float2half_rn(b - __half2float(hi)) : __float2half_rn(0.f));
+      }
     }
     *reinterpret_cast<uint4*>(pack + pl.off + tc::op_off(pl.N, nrow, c)) = *reinterpret_cast<uint4*>(hv);
   }
@@ -88,12 +95,15 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
 }
 
-template <int K, int N>
+// One layer of a group of NTHR threads (t = index in the group): make the group's A-operand
+// stores visible to the tensor-core proxy, barrier, one thread issues K/16 MMAs + commit,
+// everyone waits for the commit.
+template <int K, int N, int NTHR = 128>
 __device__ __forceinline__ void layer_mma(const uint8_t* A, const uint8_t* Wt, uint32_t tcol, uint64_t* bar,
-                                          uint32_t& phase, int t, int wg) {
+                                          uint32_t& phase, int t, int grp) {
   tc::fence_proxy_async();
   tc::fence_before();
-  named_bar(1 + wg, 128);
+  named_bar(1 + grp, NTHR);
   if (t == 0) {
     tc::fence_after();
     constexpr uint32_t idesc = tc::idesc_f16(128, N);
@@ -153,28 +163,6 @@ __device__ __forceinline__ void epi_relu_h2(uint32_t trow, const float* bias, ui
   }
 }
 
-template <int NC>
-__device__ __forceinline__ void epi_relu(uint32_t trow, const float* bias, uint8_t* A, int t) {
-#pragma unroll
-  for (int g = 0; g < NC / 16; g += 2) {
-    float v[2][16];
-    tc::tmem_ld16(trow + g * 16, v[0]);
-    tc::tmem_ld16(trow + g * 16 + 16, v[1]);
-    tc::tmem_ld_wait();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      uint32_t w[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        w[j] = tc::pack_half2(fmaxf(v[u][2 * j] + bias[(g + u) * 16 + 2 * j], 0.f),
-                              fmaxf(v[u][2 * j + 1] + bias[(g + u) * 16 + 2 * j + 1], 0.f));
-      *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * (g + u))) = make_uint4(w[0], w[1], w[2], w[3]);
-      *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * (g + u) + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
-    }
-  }
-}
-
-
 // ---- shared prologue: copy [w_begin, w_end) of the pack and `nbias` biases into smem
 template <int NWG, uint32_t TCOLS>
 __device__ __forceinline__ void tc_prologue(const uint8_t* pack, uint32_t w_begin, uint32_t w_end, uint32_t b_begin,
@@ -200,42 +188,105 @@ __device__ __forceinline__ void tc_prologue_sync() {
 }
 
 // ---- k_offset_tc: xs (x_skel, L) -> out (x_final, L) ------------------------------------
-constexpr uint32_t OF_W = PK_RAD0 - PK_OFF0;             // 114688
-constexpr uint32_t OF_BIAS = OF_W;                       // off b1..b4: 400 floats
-constexpr uint32_t OF_B0 = OF_BIAS + 400 * 4;            // 128 floats
+// Activations never touch shared memory: each layer's A operand lives in TMEM next to its
+// accumulator (tcgen05.mma with A from TMEM), so the MMAs read only the weights from smem
+// (64 of the SM's 128 B/cycle) and the epilogue is tcgen05.ld -> ReLU+fp16 cvt ->
+// tcgen05.st.  (With A in smem, N = 128 MMAs use all of the smem bandwidth and the
+// epilogue's stores stall them: tools/tc_rate.cu measures 2175 vs 1743 cycles per layer.)
+// A team of 8 warps (two warpgroups) owns a 128-sample tile: warp w reads TMEM lane quadrant
+// w%4 and accumulator columns [64*(w/4%2), +64).  Biases ride in the GEMM (pack layout).
+// TMEM per team: D = columns [0, 128), A = [128, 200) (K = 144 fp16 pairs); 2 teams.
+constexpr uint32_t OF_W = PK_RAD0 - PK_OFF0;               // 126976
+constexpr uint32_t OF_B4 = OF_W;                           // off b4: 16 floats
+constexpr uint32_t OF_SMEM = OF_B4 + 64;
+constexpr uint32_t OF_TA = 128;                            // A-operand column offset in a team
 
-constexpr uint32_t OF_A = (OF_B0 + 512 + 127) / 128 * 128;
+// One layer of a team with A in TMEM: A stores done -> barrier -> one thread issues K/16
+// MMAs (8 A columns each) + commit -> everyone waits.
+template <int K, int N, int NTHR>
+__device__ __forceinline__ void layer_mma_ts(uint32_t tcol, const uint8_t* Wt, uint64_t* bar, uint32_t& phase,
+                                             int t, int grp) {
+  tc::tmem_st_wait();
+  tc::fence_before();
+  named_bar(1 + grp, NTHR);
+  if (t == 0) {
+    tc::fence_after();
+    constexpr uint32_t idesc = tc::idesc_f16(128, N);
+    const uint32_t b0 = tc::smem_u32(Wt);
+#pragma unroll
+    for (int k = 0; k < K / 16; ++k)
+      tc::mma_f16_ts(tcol, tcol + OF_TA + k * 8, tc::make_desc(b0 + k * 2 * N * 16, N * 16, 128), idesc,
+                     k > 0 ? 1u : 0u);
+    tc::mma_commit(bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(bar, phase);
+  phase ^= 1u;
+  tc::fence_after();
+}
 
-template <int NWG>
-__global__ void __launch_bounds__(NWG * 128, 1)
+// 64 accumulator columns -> ReLU -> fp16 pairs -> 32 A-operand columns
+__device__ __forceinline__ void epi_relu64_ts(uint32_t dsrc, uint32_t adst) {
+  float v[4][16];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) tc::tmem_ld16(dsrc + g * 16, v[g]);
+  tc::tmem_ld_wait();
+  uint32_t w[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) w[j] = cvt_relu_h2(v[j >> 3][2 * (j & 7)], v[j >> 3][2 * (j & 7) + 1]);
+  tc::tmem_st32(adst, w);
+}
+
+template <int TEAMS>
+__global__ void __launch_bounds__(TEAMS * 256, 1)
     k_offset_tc(fv_field f, const float4* __restrict__ xs, int64_t n, float eps_w, float4* __restrict__ out,
                 float* __restrict__ xfinal, const int32_t* __restrict__ d_count) {
+  static_assert(TEAMS == 1 || TEAMS == 2, "256 TMEM columns per team");
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bars[NWG];
+  __shared__ uint64_t bars[TEAMS];
   __shared__ uint32_t tmem_base;
-  constexpr uint32_t TCOLS = NWG == 1 ? 128 : (NWG == 2 ? 256 : 512);
-  float* sBias = reinterpret_cast<float*>(smem + OF_BIAS);
-  float* sB0 = reinterpret_cast<float*>(smem + OF_B0);
-  tc_prologue<NWG, TCOLS>(reinterpret_cast<const uint8_t*>(f.d_tc_pack), PK_OFF0, PK_RAD0, BI_OFF1, 400, smem,
-                          sBias, bars, &tmem_base);
-  for (int i = threadIdx.x; i < 128; i += blockDim.x) sB0[i] = f.d_off_b0_eff[i];
+  constexpr uint32_t TCOLS = TEAMS == 1 ? 256 : 512;
+  float* sB4 = reinterpret_cast<float*>(smem + OF_B4);
+  tc_prologue<TEAMS, TCOLS>(reinterpret_cast<const uint8_t*>(f.d_tc_pack), PK_OFF0, PK_RAD0, BI_OFF4, 16, smem,
+                            sB4, bars, &tmem_base);
+  // per-frame layer-0 bias b0' as weight rows K = 46 (hi) / 47 (lo) of the smem copy
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+    const float b = f.d_off_b0_eff[i];
+    const __half hi = __float2half_rn(b);
+    __half* w = reinterpret_cast<__half*>(smem + PK_OFF0 + tc::op_off(128, i, 5));
+    w[6] = hi;
+    w[7] = __float2half_rn(b - __half2float(hi));
+  }
   tc_prologue_sync();
 
-  const int warp = threadIdx.x >> 5, wg = threadIdx.x >> 7, t = threadIdx.x & 127;
-  uint8_t* A = smem + OF_A + wg * A_BYTES;
-  const uint32_t tcol = tmem_base + wg * 128;
-  const uint32_t trow = tcol + ((uint32_t)((warp & 3) * 32) << 16);
-  uint64_t* bar = &bars[wg];
+  const int warp = threadIdx.x >> 5, team = threadIdx.x >> 8, tt = threadIdx.x & 255;
+  const int quad = warp & 3, half = (warp >> 2) & 1;
+  const int row = quad * 32 + (threadIdx.x & 31);
+  const uint32_t tcol = tmem_base + team * 256;
+  const uint32_t lane = (uint32_t)(quad * 32) << 16;
+  const uint32_t dsrc = tcol + lane + half * 64;              // this thread's accumulator columns
+  const uint32_t adst = tcol + lane + OF_TA + half * 32;      // ... and its A-operand columns
+  if (half == 0) {   // constant bias group of the hidden layers: A columns 64..71 = (1, 1), 0, ...
+    const uint32_t ones[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    tc::tmem_st8(tcol + lane + OF_TA + 64, ones);
+  }
+  uint64_t* bar = &bars[team];
   uint32_t phase = 0;
   if (d_count) n = min((int64_t)*d_count, n);   // compacted foreground stream of the march
   const int64_t ntiles = (n + 127) / 128;
-  for (int64_t tile = (int64_t)blockIdx.x * NWG + wg; tile < ntiles; tile += (int64_t)gridDim.x * NWG) {
-    const int64_t s = tile * 128 + t;
-    const float4 v = s < n ? xs[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t tstep = (int64_t)gridDim.x * TEAMS;
+  int64_t tile = (int64_t)blockIdx.x * TEAMS + team;
+  float4 vnext = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (tile * 128 + row < n) vnext = xs[tile * 128 + row];
+  for (; tile < ntiles; tile += tstep) {
+    const int64_t s = tile * 128 + row;
+    const float4 v = vnext;
+    if (s + tstep * 128 < n) vnext = xs[s + tstep * 128];   // prefetch the team's next tile
     const bool fg = s < n && v.w > eps_w;
     const float x0 = fg ? v.x : 0.f, x1 = fg ? v.y : 0.f, x2 = fg ? v.z : 0.f;
-    {  // posenc -> A chunks 0..5 (39 values + zero pad to 48): sin/cos(pi x) once per coordinate,
-       // higher bands by double-angle recurrences (error 2^k ulp << fp16 resolution)
+    {  // posenc -> A columns [12*half, +12) of 0..23 (39 values, zero pad, ones at k = 46/47):
+       // sin/cos(pi x) once per coordinate, higher bands by double-angle recurrences
+       // (error 2^k ulp << fp16 resolution)
       __half pe[48];
       pe[0] = __float2half_rn(x0); pe[1] = __float2half_rn(x1); pe[2] = __float2half_rn(x2);
       const float xx[3] = {x0, x1, x2};
@@ -253,29 +304,36 @@ __global__ void __launch_bounds__(NWG * 128, 1)
         }
       }
 #pragma unroll
-      for (int j = 39; j < 48; ++j) pe[j] = __float2half_rn(0.f);
-#pragma unroll
-      for (int c = 0; c < 6; ++c)
-        *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = *reinterpret_cast<const uint4*>(pe + 8 * c);
+      for (int j = 39; j < 46; ++j) pe[j] = __float2half_rn(0.f);
+      pe[46] = pe[47] = __float2half_rn(1.f);
+      const uint32_t* pw = reinterpret_cast<const uint32_t*>(pe);
+      if (half == 0) {
+        tc::tmem_st8(tcol + lane + OF_TA, pw);
+        tc::tmem_st4(tcol + lane + OF_TA + 8, pw + 8);
+      } else {
+        tc::tmem_st8(tcol + lane + OF_TA + 12, pw + 12);
+        tc::tmem_st4(tcol + lane + OF_TA + 20, pw + 20);
+      }
     }
-    layer_mma<48, 128>(A, smem + (PK_OFF0 - PK_OFF0), tcol, bar, phase, t, wg);
-    epi_relu_h2<128>(trow, sB0, A, t);
-    layer_mma<128, 128>(A, smem + (PK_OFF1 - PK_OFF0), tcol, bar, phase, t, wg);
-    epi_relu_h2<128>(trow, sBias, A, t);
-    layer_mma<128, 128>(A, smem + (PK_OFF2 - PK_OFF0), tcol, bar, phase, t, wg);
-    epi_relu_h2<128>(trow, sBias + 128, A, t);
-    layer_mma<128, 128>(A, smem + (PK_OFF3 - PK_OFF0), tcol, bar, phase, t, wg);
-    epi_relu_h2<128>(trow, sBias + 256, A, t);
-    layer_mma<128, 16>(A, smem + (PK_OFF4 - PK_OFF0), tcol, bar, phase, t, wg);
-    float o[16];
-    tc::tmem_ld16(trow, o);
-    tc::tmem_ld_wait();
-    if (s < n) {
-      const float* b4 = sBias + (BI_OFF4 - BI_OFF1);
-      const float y0 = x0 + (o[0] + b4[0]), y1 = x1 + (o[1] + b4[1]), y2 = x2 + (o[2] + b4[2]);
-      out[s] = fg ? make_float4(y0, y1, y2, v.w) : make_float4(0.f, 0.f, 0.f, v.w);
-      if (xfinal) {
-        xfinal[3 * s] = fg ? y0 : 0.f; xfinal[3 * s + 1] = fg ? y1 : 0.f; xfinal[3 * s + 2] = fg ? y2 : 0.f;
+    layer_mma_ts<48, 128, 256>(tcol, smem + PK_OFF0, bar, phase, tt, team);
+    epi_relu64_ts(dsrc, adst);
+    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF1, bar, phase, tt, team);
+    epi_relu64_ts(dsrc, adst);
+    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF2, bar, phase, tt, team);
+    epi_relu64_ts(dsrc, adst);
+    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF3, bar, phase, tt, team);
+    epi_relu64_ts(dsrc, adst);
+    layer_mma_ts<128, 16, 256>(tcol, smem + PK_OFF4, bar, phase, tt, team);
+    if (half == 0) {
+      float o[16];
+      tc::tmem_ld16(dsrc, o);
+      tc::tmem_ld_wait();
+      if (s < n) {
+        const float y0 = x0 + (o[0] + sB4[0]), y1 = x1 + (o[1] + sB4[1]), y2 = x2 + (o[2] + sB4[2]);
+        out[s] = fg ? make_float4(y0, y1, y2, v.w) : make_float4(0.f, 0.f, 0.f, v.w);
+        if (xfinal) {
+          xfinal[3 * s] = fg ? y0 : 0.f; xfinal[3 * s + 1] = fg ? y1 : 0.f; xfinal[3 * s + 2] = fg ? y2 : 0.f;
+        }
       }
     }
   }
@@ -371,9 +429,9 @@ __global__ void __launch_bounds__(NWG * 128, 1)
 }
 
 // Tuned configuration (round-1 sweeps on B200, SS4): residual MLP with 2
-// warpgroups per SM (3 leaves no L1 and runs 2x slower), hash+radiance with 4 warpgroups
-// and 4-level batched gathers.
-constexpr int OFF_NWG = 2, RAD_NWG = 4;
+// 8-warp teams per SM (all 512 TMEM columns; 124 KB of weights in smem), hash+radiance
+// with 4 warpgroups and 4-level batched gathers.
+constexpr int OFF_TEAMS = 2, RAD_NWG = 4;
 
 static int sm_count() {
   int dev = 0, n_sm = 148;
@@ -384,11 +442,11 @@ static int sm_count() {
 
 static void launch_offset(const fv_field* f, const float4* xs, int64_t n, float eps_w, float4* out, float* xfinal,
                           const int32_t* d_count, cudaStream_t st) {
-  const size_t smem = OF_A + OFF_NWG * A_BYTES;
-  cudaFuncSetAttribute(k_offset_tc<OFF_NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = OF_SMEM;
+  cudaFuncSetAttribute(k_offset_tc<OFF_TEAMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = (n + 127) / 128;
-  const int grid = (int)std::min<int64_t>((ntiles + OFF_NWG - 1) / OFF_NWG, sm_count());
-  k_offset_tc<OFF_NWG><<<grid, OFF_NWG * 128, smem, st>>>(*f, xs, n, eps_w, out, xfinal, d_count);
+  const int grid = (int)std::min<int64_t>((ntiles + OFF_TEAMS - 1) / OFF_TEAMS, sm_count());
+  k_offset_tc<OFF_TEAMS><<<grid, OFF_TEAMS * 256, smem, st>>>(*f, xs, n, eps_w, out, xfinal, d_count);
 }
 
 static void launch_radiance(const fv_field* f, const fv_hash* h, const float4* xf, int64_t n, float eps_w,
