@@ -29,24 +29,26 @@
 namespace fv {
 
 // ---- weight pack layout (bytes) ------------------------------------------------------
-// Hidden offset layers carry their bias inside the GEMM: K = 128 activations + 16 bias
-// rows, rows 128/129 = fp16 hi/lo split of the fp32 bias (b - hi(b) in fp16: ~2^-22
-// relative), multiplied by A columns 128/129 = 1.0.  Layer 0 uses the posenc pad columns
-// 46/47 the same way for the per-frame b0' (patched into the smem copy by the kernel).
+// Every tensor-core layer except the offset MLP's last carries its bias inside the GEMM:
+// K = activations + a 16-row bias group whose first two rows are the fp16 hi/lo split of
+// the fp32 bias (b - hi(b) in fp16: ~2^-22 relative), multiplied by A columns = 1.0.
+// Offset layer 0 uses the posenc pad columns 46/47 for the per-frame b0' (patched into the
+// smem copy by the kernel).
 constexpr uint32_t OF_KH = 144;                           // hidden-layer K (128 + bias group)
 constexpr uint32_t PK_OFF0 = 0;                           // [128 x 48]
 constexpr uint32_t PK_OFF1 = PK_OFF0 + 128 * 48 * 2;      // [128 x 144]
 constexpr uint32_t PK_OFF2 = PK_OFF1 + 128 * OF_KH * 2;
 constexpr uint32_t PK_OFF3 = PK_OFF2 + 128 * OF_KH * 2;
 constexpr uint32_t PK_OFF4 = PK_OFF3 + 128 * OF_KH * 2;   // [16 x 128]
-constexpr uint32_t PK_RAD0 = PK_OFF4 + 16 * 128 * 2;      // [64 x 32]
-constexpr uint32_t PK_RAD1 = PK_RAD0 + 64 * 32 * 2;       // [64 x 64]
-constexpr uint32_t PK_RAD2 = PK_RAD1 + 64 * 64 * 2;       // [16 x 64]
-constexpr uint32_t PK_WEND = PK_RAD2 + 16 * 64 * 2;       // 141312
+constexpr uint32_t RA_K0 = 48, RA_KH = 80;                // radiance K incl. the bias group
+constexpr uint32_t PK_RAD0 = PK_OFF4 + 16 * 128 * 2;      // [64 x 48]  (32 features + bias group)
+constexpr uint32_t PK_RAD1 = PK_RAD0 + 64 * RA_K0 * 2;    // [64 x 80]  (64 hidden + bias group)
+constexpr uint32_t PK_RAD2 = PK_RAD1 + 64 * RA_KH * 2;    // [16 x 80]
+constexpr uint32_t PK_WEND = PK_RAD2 + 16 * RA_KH * 2;    // 148480
 // fp32 biases: off b1,b2,b3 (128 each), off b4 (16), rad b0 (64), rad b1 (64), rad b2 (16)
 constexpr uint32_t BI_OFF1 = 0, BI_OFF2 = 128, BI_OFF3 = 256, BI_OFF4 = 384, BI_RAD0 = 400, BI_RAD1 = 464,
                    BI_RAD2 = 528, BI_END = 544;
-constexpr uint32_t PK_BYTES = PK_WEND + BI_END * 4;       // 143488
+constexpr uint32_t PK_BYTES = PK_WEND + BI_END * 4;       // 150656
 
 struct PackLayer { uint32_t off; int N, K, n_true, k_true; };
 
@@ -54,8 +56,8 @@ struct PackLayer { uint32_t off; int N, K, n_true, k_true; };
 __global__ void k_field_pack(fv_field f, uint8_t* __restrict__ pack) {
   const PackLayer L[8] = {
       {PK_OFF0, 128, 48, 128, 3 + 6 * f.pe_bands}, {PK_OFF1, 128, OF_KH, 128, 128}, {PK_OFF2, 128, OF_KH, 128, 128},
-      {PK_OFF3, 128, OF_KH, 128, 128},            {PK_OFF4, 16, 128, 3, 128},       {PK_RAD0, 64, 32, 64, 32},
-      {PK_RAD1, 64, 64, 64, 64},                  {PK_RAD2, 16, 64, 4, 64}};
+      {PK_OFF3, 128, OF_KH, 128, 128},            {PK_OFF4, 16, 128, 3, 128},       {PK_RAD0, 64, RA_K0, 64, 32},
+      {PK_RAD1, 64, RA_KH, 64, 64},               {PK_RAD2, 16, RA_KH, 4, 64}};
   const float* W[8] = {f.d_off_w[0], f.d_off_w[1], f.d_off_w[2], f.d_off_w[3], f.d_off_w[4],
                        f.d_rad_w[0], f.d_rad_w[1], f.d_rad_w[2]};
   const int layer = blockIdx.y;
@@ -69,10 +71,10 @@ __global__ void k_field_pack(fv_field f, uint8_t* __restrict__ pack) {
       const int k = 8 * c + j;
       const float v = (k < pl.k_true && nrow < pl.n_true) ? W[layer][(int64_t)k * pl.n_true + nrow] : 0.f;
       hv[j] = __float2half_rn(v);
-      if (layer >= 1 && layer <= 3 && k >= 128) {   // bias rows (hi, lo) of the hidden layers
-        const float b = f.d_off_b[layer][nrow];
+      if (layer != 0 && layer != 4 && k >= pl.k_true) {   // bias group: rows (hi, lo, 0 ...)
+        const float b = nrow >= pl.n_true ? 0.f : (layer < 4 ? f.d_off_b[layer][nrow] : f.d_rad_b[layer - 5][nrow]);
         const __half hi = __float2half_rn(b);
-        hv[j] = k == 128 ? hi : (k == 129 ? __float2half_rn(b - __half2float(hi)) : __float2half_rn(0.f));
+        hv[j] = k == pl.k_true ? hi : (k == pl.k_true + 1 ? __float2half_rn(b - __half2float(hi)) : __float2half_rn(0.f));
       }
     }
     *reinterpret_cast<uint4*>(pack + pl.off + tc::op_off(pl.N, nrow, c)) = *reinterpret_cast<uint4*>(hv);
@@ -134,33 +136,6 @@ __device__ __forceinline__ uint32_t cvt_relu_h2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
-}
-
-// TMEM row -> + bias (fp32, smem) -> ReLU+fp16 pack (one cvt) -> A operand: 3 instructions
-// per pair (the FADD/FMNMX/FSETP/F2FP form spent ~40% of the kernel's issue slots)
-template <int NC>
-__device__ __forceinline__ void epi_relu_h2(uint32_t trow, const float* bias, uint8_t* A, int t) {
-#pragma unroll
-  for (int g = 0; g < NC / 16; g += 2) {
-    float v[2][16];
-    tc::tmem_ld16(trow + g * 16, v[0]);
-    tc::tmem_ld16(trow + g * 16 + 16, v[1]);
-    tc::tmem_ld_wait();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      float bb[16];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 b4 = *reinterpret_cast<const float4*>(bias + (g + u) * 16 + 4 * q);
-        bb[4 * q] = b4.x; bb[4 * q + 1] = b4.y; bb[4 * q + 2] = b4.z; bb[4 * q + 3] = b4.w;
-      }
-      uint32_t w[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) w[j] = cvt_relu_h2(v[u][2 * j] + bb[2 * j], v[u][2 * j + 1] + bb[2 * j + 1]);
-      *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * (g + u))) = make_uint4(w[0], w[1], w[2], w[3]);
-      *reinterpret_cast<uint4*>(A + tc::op_off(128, t, 2 * (g + u) + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
-    }
-  }
 }
 
 // ---- shared prologue: copy [w_begin, w_end) of the pack and `nbias` biases into smem
@@ -343,83 +318,100 @@ __global__ void __launch_bounds__(TEAMS * 256, 1)
 }
 
 // ---- k_radiance_tc: (x_final, L) -> (c, sigma) ----------------------------------------
-constexpr uint32_t RA_W = PK_WEND - PK_RAD0;             // 14336
-constexpr uint32_t RA_BIAS = RA_W;                       // rad b0,b1,b2: 144 floats
+// Hash features and hidden activations live in TMEM (tcgen05.st; MMAs take A from TMEM)
+// and the biases ride in the GEMM, so the only shared-memory traffic is the tensor core
+// reading the 17 KB of weights: the L1 data pipe is left to the table gathers, which
+// bound this kernel.  (The smem-A version spent ~25% of the pipe's wavefronts on the
+// MLP's STS/LDS.)  TMEM per warpgroup: D = columns [0, 64), A = [64, 104): features
+// (words 0..15) or hidden activations (words 0..31), then the shared bias group
+// (words 32..39 = (1, 1), 0, ...) that every layer's last K step reads.
+constexpr uint32_t RA_SMEM = PK_WEND - PK_RAD0;          // 19456 B of weights
+constexpr uint32_t RA_TA = 64;                           // A-operand column offset
+constexpr uint32_t RA_TCOLS_WG = 128;                    // TMEM columns per warpgroup (104 used)
 
-constexpr uint32_t RA_A = (RA_BIAS + 144 * 4 + 127) / 128 * 128;
-constexpr uint32_t RA_A_BYTES = 128 * 64 * 2;            // 16 KB per warpgroup
+// K_ACT activations (K_ACT/16 steps from A words 0..) + the bias step (A words 32..39).
+template <int K_ACT, int N>
+__device__ __forceinline__ void layer_mma_rad(uint32_t tcol, const uint8_t* Wt, uint64_t* bar, uint32_t& phase,
+                                              int t, int wg) {
+  tc::tmem_st_wait();
+  tc::fence_before();
+  named_bar(1 + wg, 128);
+  if (t == 0) {
+    tc::fence_after();
+    constexpr uint32_t idesc = tc::idesc_f16(128, N);
+    const uint32_t b0 = tc::smem_u32(Wt);
+#pragma unroll
+    for (int k = 0; k <= K_ACT / 16; ++k) {
+      const uint32_t a = tcol + RA_TA + (k < K_ACT / 16 ? k * 8 : 32);
+      tc::mma_f16_ts(tcol, a, tc::make_desc(b0 + k * 2 * N * 16, N * 16, 128), idesc, k > 0 ? 1u : 0u);
+    }
+    tc::mma_commit(bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(bar, phase);
+  phase ^= 1u;
+  tc::fence_after();
+}
 
-template <int NWG, bool BATCH>
+template <int NWG>
 __global__ void __launch_bounds__(NWG * 128, 1)
     k_radiance_tc(fv_field f, fv_hash h, const float4* __restrict__ xf, int64_t n, float eps_w,
                   float4* __restrict__ rgbs, const int32_t* __restrict__ d_count, const int32_t* __restrict__ idx) {
+  static_assert(NWG * RA_TCOLS_WG <= 512, "TMEM");
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[NWG];
   __shared__ uint32_t tmem_base;
-  constexpr uint32_t TCOLS = NWG <= 2 ? 128 : (NWG <= 4 ? 256 : 512);
-  float* sBias = reinterpret_cast<float*>(smem + RA_BIAS);
-  tc_prologue<NWG, TCOLS>(reinterpret_cast<const uint8_t*>(f.d_tc_pack), PK_RAD0, PK_WEND, BI_RAD0, 144, smem,
-                          sBias, bars, &tmem_base);
+  constexpr uint32_t TCOLS = NWG * RA_TCOLS_WG <= 256 ? 256 : 512;
+  tc_prologue<NWG, TCOLS>(reinterpret_cast<const uint8_t*>(f.d_tc_pack), PK_RAD0, PK_WEND, 0, 0, smem, nullptr,
+                          bars, &tmem_base);
   tc_prologue_sync();
 
   const int warp = threadIdx.x >> 5, wg = threadIdx.x >> 7, t = threadIdx.x & 127;
-  uint8_t* A = smem + RA_A + wg * RA_A_BYTES;
-  const uint32_t tcol = tmem_base + wg * 64;
-  const uint32_t trow = tcol + ((uint32_t)((warp & 3) * 32) << 16);
+  const uint32_t tcol = tmem_base + wg * RA_TCOLS_WG;
+  const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t trow = tcol + lane;              // this thread's accumulator row
+  const uint32_t arow = tcol + lane + RA_TA;      // ... and its A-operand row
+  {
+    const uint32_t ones[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    tc::tmem_st8(arow + 32, ones);
+  }
   uint64_t* bar = &bars[wg];
   uint32_t phase = 0;
   if (d_count) n = min((int64_t)*d_count, n);
   const int64_t ntiles = (n + 127) / 128;
-  for (int64_t tile = (int64_t)blockIdx.x * NWG + wg; tile < ntiles; tile += (int64_t)gridDim.x * NWG) {
+  const int64_t tstep = (int64_t)gridDim.x * NWG;
+  int64_t tile = (int64_t)blockIdx.x * NWG + wg;
+  float4 vnext = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (tile * 128 + t < n) vnext = xf[tile * 128 + t];
+  for (; tile < ntiles; tile += tstep) {
     const int64_t s = tile * 128 + t;
-    const float4 v = s < n ? xf[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 v = vnext;
+    if (s + tstep * 128 < n) vnext = xf[s + tstep * 128];   // prefetch the warpgroup's next tile
     const bool fg = s < n && v.w > eps_w;
-    {  // hash-grid features -> A chunks 0..3
+    {  // hash-grid features -> A words 0..15 (4 levels = 4 words per batch)
       float xn[3]; bool msk[3];
       hash_norm(h, fg ? v.x : 0.f, fg ? v.y : 0.f, fg ? v.z : 0.f, xn, msk);
-      if (BATCH) {
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          float2 fv4[4];
-          hash_4levels_paired(h, 4 * c, xn, fv4);
-          uint32_t w[4];
+      for (int c = 0; c < 4; ++c) {
+        float2 fv4[4];
+        hash_4levels_paired(h, 4 * c, xn, fv4);
+        uint32_t w[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) w[q] = tc::pack_half2(fg ? fv4[q].x : 0.f, fg ? fv4[q].y : 0.f);
-          *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t w[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int l = 4 * c + q;
-            float2 fv2 = make_float2(0.f, 0.f);
-            if (l < h.n_levels) {
-              HashCell cell;
-              hash_level_cell(xn, h.res[l], cell);
-              fv2 = hash_level_feat(h, l, cell);
-            }
-            w[q] = tc::pack_half2(fg ? fv2.x : 0.f, fg ? fv2.y : 0.f);
-          }
-          *reinterpret_cast<uint4*>(A + tc::op_off(128, t, c)) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
+        for (int q = 0; q < 4; ++q) w[q] = tc::pack_half2(fg ? fv4[q].x : 0.f, fg ? fv4[q].y : 0.f);
+        tc::tmem_st4(arow + 4 * c, w);
       }
     }
-    layer_mma<32, 64>(A, smem + (PK_RAD0 - PK_RAD0), tcol, bar, phase, t, wg);
-    epi_relu_h2<64>(trow, sBias, A, t);
-    layer_mma<64, 64>(A, smem + (PK_RAD1 - PK_RAD0), tcol, bar, phase, t, wg);
-    epi_relu_h2<64>(trow, sBias + 64, A, t);
-    layer_mma<64, 16>(A, smem + (PK_RAD2 - PK_RAD0), tcol, bar, phase, t, wg);
+    layer_mma_rad<32, 64>(tcol, smem + (PK_RAD0 - PK_RAD0), bar, phase, t, wg);
+    epi_relu64_ts(trow, arow);
+    layer_mma_rad<64, 64>(tcol, smem + (PK_RAD1 - PK_RAD0), bar, phase, t, wg);
+    epi_relu64_ts(trow, arow);
+    layer_mma_rad<64, 16>(tcol, smem + (PK_RAD2 - PK_RAD0), bar, phase, t, wg);
     float o[16];
     tc::tmem_ld16(trow, o);
     tc::tmem_ld_wait();
     if (s < n) {
-      const float* b2 = sBias + (BI_RAD2 - BI_RAD0);
       float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (fg)
-        r = make_float4(sigmoidf_(o[0] + b2[0]), sigmoidf_(o[1] + b2[1]), sigmoidf_(o[2] + b2[2]),
-                        softplusf_(o[3] + b2[3] - 1.f));
+      if (fg) r = make_float4(sigmoidf_(o[0]), sigmoidf_(o[1]), sigmoidf_(o[2]), softplusf_(o[3] - 1.f));
       rgbs[idx ? (int64_t)idx[s] : s] = r;   // scatter back to the full sample layout
     }
   }
@@ -451,11 +443,11 @@ static void launch_offset(const fv_field* f, const float4* xs, int64_t n, float 
 
 static void launch_radiance(const fv_field* f, const fv_hash* h, const float4* xf, int64_t n, float eps_w,
                             float4* rgbs, const int32_t* d_count, const int32_t* idx, cudaStream_t st) {
-  const size_t smem = RA_A + RAD_NWG * RA_A_BYTES;
-  cudaFuncSetAttribute(k_radiance_tc<RAD_NWG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = RA_SMEM;
+  cudaFuncSetAttribute(k_radiance_tc<RAD_NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = (n + 127) / 128;
   const int grid = (int)std::min<int64_t>((ntiles + RAD_NWG - 1) / RAD_NWG, sm_count());
-  k_radiance_tc<RAD_NWG, true><<<grid, RAD_NWG * 128, smem, st>>>(*f, *h, xf, n, eps_w, rgbs, d_count, idx);
+  k_radiance_tc<RAD_NWG><<<grid, RAD_NWG * 128, smem, st>>>(*f, *h, xf, n, eps_w, rgbs, d_count, idx);
 }
 
 // x_skel -> x_final -> (c, sigma).  Dense form (d_count == NULL): x_final goes to rgbs as
