@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(NWG * 128, 1)
     tc::tmem_ld_wait();
     if (s < n) {
       float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (fg) r = make_float4(sigmoidf_(o[0]), sigmoidf_(o[1]), sigmoidf_(o[2]), softplusf_(o[3] - 1.f));
+      if (fg) r = make_float4(sigmoid_fast(o[0]), sigmoid_fast(o[1]), sigmoid_fast(o[2]), softplus_fast(o[3] - 1.f));
       rgbs[idx ? (int64_t)idx[s] : s] = r;   // scatter back to the full sample layout
     }
   }

@@ -268,106 +268,99 @@ __device__ __forceinline__ float2 hash_level_feat(const fv_hash& h, int l, const
   return acc;
 }
 
-// Four levels at once: 32 independent gathers in flight per thread before any is consumed
-// (the serial per-level form stalls on long-scoreboard for every level).
-__device__ __forceinline__ void hash_4levels(const fv_hash& h, int l0, const float (&xn)[3], float2 (&out)[4]) {
-  const uint32_t maskT = (1u << h.log2_T) - 1u;
-  uint32_t gidx[32];
-  float f[4][3];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int l = l0 + q < h.n_levels ? l0 + q : h.n_levels - 1;
-    HashCell c;
-    hash_level_cell(xn, h.res[l], c);
-    f[q][0] = c.f[0]; f[q][1] = c.f[1]; f[q][2] = c.f[2];
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      gidx[q * 8 + k] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + ((k >> 2) & 1),
-                                                  c.i0[1] + ((k >> 1) & 1), c.i0[2] + (k & 1));
-  }
-  float2 v[32];
-  if (h.table_half) {
-    const __half2* t = reinterpret_cast<const __half2*>(h.d_table);
-#pragma unroll
-    for (int k = 0; k < 32; ++k) v[k] = __half22float2(__ldg(t + gidx[k]));
-  } else {
-    const float2* t = reinterpret_cast<const float2*>(h.d_table);
-#pragma unroll
-    for (int k = 0; k < 32; ++k) v[k] = __ldg(t + gidx[k]);
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float wx[2] = {__fsub_rn(1.0f, f[q][0]), f[q][0]};
-    const float wy[2] = {__fsub_rn(1.0f, f[q][1]), f[q][1]};
-    const float wz[2] = {__fsub_rn(1.0f, f[q][2]), f[q][2]};
-    float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float wgt = __fmul_rn(__fmul_rn(wx[(k >> 2) & 1], wy[(k >> 1) & 1]), wz[k & 1]);
-      acc.x = __fadd_rn(acc.x, __fmul_rn(wgt, v[q * 8 + k].x));
-      acc.y = __fadd_rn(acc.y, __fmul_rn(wgt, v[q * 8 + k].y));
-    }
-    out[q] = l0 + q < h.n_levels ? acc : make_float2(0.f, 0.f);
-  }
-}
-
-// Lane-paired gathers (fp16 or fp32 table): lanes (2p, 2p+1) serve the samples of both
-// lanes; lane parity a = lane & 1 fetches the x-corner a of each sample.  A cell's two
-// x-corners differ only in low index bits (same 128-byte line ~99% of the time), so in one
-// warp instruction 16 samples x 2 corners touch 16 lines instead of 32 -- half the L1
-// wavefronts of the per-sample form at the same load count; one shuffle per feature adds the
-// partner's partial.  Accumulation order (a-partials then sum) differs from the oracle's
-// (a,b,c) order: used only where features are rounded to fp16 (tensor-core field).
+// Lane-paired gathers of four levels (fp16 or fp32 table): lanes (2p, 2p+1) serve the
+// samples of both lanes; lane parity a = lane & 1 fetches the x-corner a of each sample.  A
+// cell's two x-corners differ only in low index bits (same 128-byte line ~99% of the time),
+// so in one warp instruction 16 samples x 2 corners touch 16 lines instead of 32 -- half
+// the L1 wavefronts of the per-sample form at the same load count.  32 independent gathers
+// are in flight per thread before any is consumed.  Corner indices are strength-reduced
+// (y+1 -> +PRIME_Y or +s, z+1 -> +PRIME_Z or +s^2, same uint32 arithmetic as hash_index)
+// and each lane blends its four corners as lerps (z, then y) scaled by its x weight; one
+// shuffle per feature adds the partner's partial.  The blend order differs from the
+// oracle's (a,b,c) sum by fp32 rounding only: used where features are rounded to fp16.
 __device__ __forceinline__ void hash_4levels_paired(const fv_hash& h, int l0, const float (&xn_self)[3],
                                                     float2 (&out)[4]) {
   const uint32_t maskT = (1u << h.log2_T) - 1u;
-  const int lane = threadIdx.x & 31;
-  const uint32_t a = lane & 1u;
-  float xA[3], xB[3];   // A = even lane's sample, B = odd lane's sample
+  const uint32_t a = threadIdx.x & 1u;
+  // A = the even lane's sample, B = the odd lane's, for both lanes of a pair: each load
+  // instruction then has the pair fetching the two x-corners of the same sample
+  float xA[3], xB[3];
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
     const float other = __shfl_xor_sync(0xffffffffu, xn_self[j], 1);
     xA[j] = a ? other : xn_self[j];
     xB[j] = a ? xn_self[j] : other;
   }
+  const float wsgn = a ? 1.f : -1.f, wbase = a ? 0.f : 1.f;   // w_x(a) = wbase + wsgn * f_x
   uint32_t iA[16], iB[16];
+  uint32_t lofs[4];
   float fA[4][3], fB[4][3];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int l = l0 + q < h.n_levels ? l0 + q : h.n_levels - 1;
+    const int res = h.res[l];
+    lofs[q] = h.offset[l];
     HashCell cA, cB;
-    hash_level_cell(xA, h.res[l], cA);
-    hash_level_cell(xB, h.res[l], cB);
+    hash_level_cell(xA, res, cA);
+    hash_level_cell(xB, res, cB);
 #pragma unroll
     for (int j = 0; j < 3; ++j) { fA[q][j] = cA.f[j]; fB[q][j] = cB.f[j]; }
-#pragma unroll
-    for (int bc = 0; bc < 4; ++bc) {
-      iA[q * 4 + bc] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, cA.i0[0] + a, cA.i0[1] + (bc >> 1),
-                                                cA.i0[2] + (bc & 1));
-      iB[q * 4 + bc] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, cB.i0[0] + a, cB.i0[1] + (bc >> 1),
-                                                cB.i0[2] + (bc & 1));
+    const uint32_t xa = (uint32_t)cA.i0[0] + a, xb = (uint32_t)cB.i0[0] + a;
+    if (h.dense[l]) {
+      const uint32_t sy = (uint32_t)res + 1u, sz = sy * sy;
+      const uint32_t bA = xa + (uint32_t)cA.i0[1] * sy + (uint32_t)cA.i0[2] * sz;
+      const uint32_t bB = xb + (uint32_t)cB.i0[1] * sy + (uint32_t)cB.i0[2] * sz;
+      iA[q * 4 + 0] = bA; iA[q * 4 + 1] = bA + sz; iA[q * 4 + 2] = bA + sy; iA[q * 4 + 3] = bA + sy + sz;
+      iB[q * 4 + 0] = bB; iB[q * 4 + 1] = bB + sz; iB[q * 4 + 2] = bB + sy; iB[q * 4 + 3] = bB + sy + sz;
+    } else {
+      const uint32_t yA0 = (uint32_t)cA.i0[1] * PRIME_Y, yA1 = yA0 + PRIME_Y;
+      const uint32_t zA0 = (uint32_t)cA.i0[2] * PRIME_Z, zA1 = zA0 + PRIME_Z;
+      const uint32_t yB0 = (uint32_t)cB.i0[1] * PRIME_Y, yB1 = yB0 + PRIME_Y;
+      const uint32_t zB0 = (uint32_t)cB.i0[2] * PRIME_Z, zB1 = zB0 + PRIME_Z;
+      iA[q * 4 + 0] = (xa ^ yA0 ^ zA0) & maskT; iA[q * 4 + 1] = (xa ^ yA0 ^ zA1) & maskT;
+      iA[q * 4 + 2] = (xa ^ yA1 ^ zA0) & maskT; iA[q * 4 + 3] = (xa ^ yA1 ^ zA1) & maskT;
+      iB[q * 4 + 0] = (xb ^ yB0 ^ zB0) & maskT; iB[q * 4 + 1] = (xb ^ yB0 ^ zB1) & maskT;
+      iB[q * 4 + 2] = (xb ^ yB1 ^ zB0) & maskT; iB[q * 4 + 3] = (xb ^ yB1 ^ zB1) & maskT;
     }
   }
   float2 vA[16], vB[16];
   if (h.table_half) {
-    const __half2* t = reinterpret_cast<const __half2*>(h.d_table);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) { vA[k] = __half22float2(__ldg(t + iA[k])); vB[k] = __half22float2(__ldg(t + iB[k])); }
+    for (int q = 0; q < 4; ++q) {
+      const __half2* t = reinterpret_cast<const __half2*>(h.d_table) + lofs[q];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        vA[q * 4 + k] = __half22float2(__ldg(t + iA[q * 4 + k]));
+        vB[q * 4 + k] = __half22float2(__ldg(t + iB[q * 4 + k]));
+      }
+    }
   } else {
-    const float2* t = reinterpret_cast<const float2*>(h.d_table);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) { vA[k] = __ldg(t + iA[k]); vB[k] = __ldg(t + iB[k]); }
+    for (int q = 0; q < 4; ++q) {
+      const float2* t = reinterpret_cast<const float2*>(h.d_table) + lofs[q];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { vA[q * 4 + k] = __ldg(t + iA[q * 4 + k]); vB[q * 4 + k] = __ldg(t + iB[q * 4 + k]); }
+    }
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    float2 pA = make_float2(0.f, 0.f), pB = make_float2(0.f, 0.f);
-    const float wxA = a ? fA[q][0] : 1.f - fA[q][0], wxB = a ? fB[q][0] : 1.f - fB[q][0];
-#pragma unroll
-    for (int bc = 0; bc < 4; ++bc) {
-      const float wA = wxA * ((bc >> 1) ? fA[q][1] : 1.f - fA[q][1]) * ((bc & 1) ? fA[q][2] : 1.f - fA[q][2]);
-      const float wB = wxB * ((bc >> 1) ? fB[q][1] : 1.f - fB[q][1]) * ((bc & 1) ? fB[q][2] : 1.f - fB[q][2]);
-      pA.x = fmaf(wA, vA[q * 4 + bc].x, pA.x); pA.y = fmaf(wA, vA[q * 4 + bc].y, pA.y);
-      pB.x = fmaf(wB, vB[q * 4 + bc].x, pB.x); pB.y = fmaf(wB, vB[q * 4 + bc].y, pB.y);
+    // corners k = 2b + c of this lane's x-corner a: lerp in z (c), then y (b), scale by w_x(a)
+    const float2* va = vA + q * 4;
+    const float2* vb = vB + q * 4;
+    float2 pA, pB;
+    {
+      const float fy = fA[q][1], fz = fA[q][2];
+      const float c0x = fmaf(fz, va[1].x - va[0].x, va[0].x), c0y = fmaf(fz, va[1].y - va[0].y, va[0].y);
+      const float c1x = fmaf(fz, va[3].x - va[2].x, va[2].x), c1y = fmaf(fz, va[3].y - va[2].y, va[2].y);
+      const float wx = fmaf(wsgn, fA[q][0], wbase);
+      pA = make_float2(wx * fmaf(fy, c1x - c0x, c0x), wx * fmaf(fy, c1y - c0y, c0y));
+    }
+    {
+      const float fy = fB[q][1], fz = fB[q][2];
+      const float c0x = fmaf(fz, vb[1].x - vb[0].x, vb[0].x), c0y = fmaf(fz, vb[1].y - vb[0].y, vb[0].y);
+      const float c1x = fmaf(fz, vb[3].x - vb[2].x, vb[2].x), c1y = fmaf(fz, vb[3].y - vb[2].y, vb[2].y);
+      const float wx = fmaf(wsgn, fB[q][0], wbase);
+      pB = make_float2(wx * fmaf(fy, c1x - c0x, c0x), wx * fmaf(fy, c1y - c0y, c0y));
     }
     // even lane keeps sample A: own a=0 partial of A + partner's a=1 partial of A
     const float sx = a ? pA.x : pB.x, sy = a ? pA.y : pB.y;      // what the partner needs
@@ -384,5 +377,9 @@ __device__ __forceinline__ float sigmoidf_(float x) {
   return e / (1.f + e);
 }
 __device__ __forceinline__ float softplusf_(float x) { return log1pf(expf(-fabsf(x))) + fmaxf(x, 0.f); }
+
+// MUFU forms for the fp16 tensor-core field (absolute error ~1e-7, far inside its 1e-3 bar)
+__device__ __forceinline__ float sigmoid_fast(float x) { return __frcp_rn(1.f + __expf(-x)); }
+__device__ __forceinline__ float softplus_fast(float x) { return __logf(1.f + __expf(-fabsf(x))) + fmaxf(x, 0.f); }
 
 }  // namespace fv
