@@ -17,6 +17,8 @@
 #include "fv_common.cuh"
 #include "fv_internal.h"
 #include "tc_sm100.cuh"
+#include "gemm_tf32x3.h"
+#include <cstdlib>
 
 namespace fv {
 
@@ -365,6 +367,12 @@ int32_t lin_dw_tc(const DwArgs& a0, float* db, cudaStream_t st) {
 
 static int pad(int x, int m) { return (x + m - 1) / m * m; }
 
+// FV_LEGACY_LIN=1 selects the round-1 per-CTA kernels (A/B timing only)
+static bool legacy() {
+  static const int v = [] { const char* e = std::getenv("FV_LEGACY_LIN"); return e && e[0] == '1' ? 1 : 0; }();
+  return v != 0;
+}
+
 }  // namespace fv
 
 using namespace fv;
@@ -378,6 +386,10 @@ extern "C" int32_t fv_linear_fwd_tc(const float* d_x, int64_t ldx, const float* 
   if (m == 0) return FV_OK;
   // forward activations feed the next layer and, through x_final, the hash-cell positions,
   // so the forward runs split-precision 3xTF32 (~fp32); backward GEMMs are plain TF32
+  if (!legacy()) {
+    g3::RowsArgs r{d_x, ldx, k_in, d_w, 1, n_out, n_out, d_b, act, nullptr, 0, d_y, ldy, m};
+    return g3::rows_gemm(r, (cudaStream_t)stream);
+  }
   LinArgs a{d_x, ldx, k_in, d_w, 1, n_out, n_out, pad(k_in, KC), pad(n_out, 16), d_b, act, nullptr, 0, d_y, ldy, m, 1};
   return lin_tc(a, (cudaStream_t)stream);
 }
@@ -395,13 +407,23 @@ extern "C" int32_t fv_linear_bwd_tc(const float* d_x, int64_t ldx, const float* 
   cudaStream_t st = (cudaStream_t)stream;
   if (d_dx) {
     // dx[m, k] = sum_n dz[m, n] W[k, n]  : K' = n_out, N' = k_in, B(n'=k, k'=n) = W[k*n_out + n]
-    LinArgs a{d_dz, ldz, n_out, d_w, n_out, 1, k_in, pad(n_out, KC), pad(k_in, 16), nullptr, 0, d_xmask, ldx,
-              d_dx, lddx, m, 1};   // dx feeds the rest of the backward chain: 3xTF32 too
-    if (int32_t e = lin_tc(a, st)) return e;
+    if (!legacy()) {
+      g3::RowsArgs r{d_dz, ldz, n_out, d_w, n_out, 1, k_in, nullptr, 0, d_xmask, ldx, d_dx, lddx, m};
+      if (int32_t e = g3::rows_gemm(r, st)) return e;
+    } else {
+      LinArgs a{d_dz, ldz, n_out, d_w, n_out, 1, k_in, pad(n_out, KC), pad(k_in, 16), nullptr, 0, d_xmask, ldx,
+                d_dx, lddx, m, 1};   // dx feeds the rest of the backward chain: 3xTF32 too
+      if (int32_t e = lin_tc(a, st)) return e;
+    }
   }
   if (d_dw) {
-    DwArgs a{d_x, ldx, k_in, d_dz, ldz, n_out, pad(n_out, 16), d_dw, m, 0};
-    if (int32_t e = lin_dw_tc(a, d_db, st)) return e;
+    if (!legacy()) {
+      g3::DwArgs3 w{d_x, ldx, k_in, d_dz, ldz, n_out, d_dw, d_db, m};
+      if (int32_t e = g3::dw_gemm(w, st)) return e;
+    } else {
+      DwArgs a{d_x, ldx, k_in, d_dz, ldz, n_out, pad(n_out, 16), d_dw, m, 0};
+      if (int32_t e = lin_dw_tc(a, d_db, st)) return e;
+    }
   }
   return FV_OK;
 }
