@@ -312,6 +312,9 @@ __global__ void __launch_bounds__(384, 1) k_rows(RowsArgs a, const __grid_consta
 }
 
 // ============================================================================ k_dw
+// Stage layout (smem): Z raw [4 boxes] | X hi [nxb + 1 boxes] | X lo [nxb + 1]; the split
+// dZ^T operand lives in TMEM (A stage t at columns 256 + 64t: hi 32 columns, lo 32), the
+// accumulator D = dW^T (+ db column) in columns [0, 32*nxb + 16).
 constexpr int kDwS = 32;                  // samples per stage (4 MMA k-steps of 8)
 constexpr int kBox = kDwS * 128;          // bytes of one 32-feature x 32-sample swizzled box
 
@@ -324,19 +327,17 @@ __global__ void __launch_bounds__(256, 1) k_dw(DwArgs3 a, const __grid_constant_
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ST = a.stages;
   const int nxb1 = a.nxb + 1;                               // X boxes + the ones box
-  // stage layout: Z hi [4 boxes] | Z lo [4] | X hi [nxb1] | X lo [nxb1]
-  const uint32_t stage_bytes = (uint32_t)(8 + 2 * nxb1) * kBox;
-  auto zhi = [&](int s) { return sm + s * stage_bytes; };
-  auto zlo = [&](int s) { return sm + s * stage_bytes + 4 * kBox; };
-  auto xhi = [&](int s) { return sm + s * stage_bytes + 8 * kBox; };
-  auto xlo = [&](int s) { return sm + s * stage_bytes + (8 + nxb1) * kBox; };
+  const uint32_t stage_bytes = (uint32_t)(4 + 2 * nxb1) * kBox;
+  auto zraw = [&](int s) { return sm + s * stage_bytes; };
+  auto xhi = [&](int s) { return sm + s * stage_bytes + 4 * kBox; };
+  auto xlo = [&](int s) { return sm + s * stage_bytes + (4 + nxb1) * kBox; };
 
-  // zero every stage (unused Z boxes, X padding); the ones box is 1.0 everywhere (hi = 1,
-  // lo = 0), so each of its columns of D is colsum(dZ) whatever the swizzle
+  // zero every stage (Z boxes TMA never writes, X padding); the ones box is 1.0 everywhere
+  // (hi = 1, lo = 0), so each of its columns of D is colsum(dZ) whatever the swizzle
   for (uint32_t i = tid; i < ST * stage_bytes / 16; i += blockDim.x) {
-    const uint32_t s = i / (stage_bytes / 16), o = i % (stage_bytes / 16);
-    const bool ones = o >= (8 + a.nxb) * kBox / 16 && o < (8 + nxb1) * kBox / 16;
-    const float v = (ones && s < (uint32_t)ST) ? 1.f : 0.f;
+    const uint32_t o = i % (stage_bytes / 16);
+    const bool ones = o >= (4 + a.nxb) * kBox / 16 && o < (4 + nxb1) * kBox / 16;
+    const float v = ones ? 1.f : 0.f;
     reinterpret_cast<float4*>(sm)[i] = make_float4(v, v, v, v);
   }
   if (tid == 0) {
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(256, 1) k_dw(DwArgs3 a, const __grid_constant_
     tc::mbar_init(&tfull, 1);
     tc::mbar_fence_init();
   }
-  if (warp == 1) tc::tmem_alloc<256>(&tmem_base);
+  if (warp == 1) tc::tmem_alloc<512>(&tmem_base);
   tc::fence_proxy_async();
   tc::fence_before();
   __syncthreads();
@@ -364,69 +365,89 @@ __global__ void __launch_bounds__(256, 1) k_dw(DwArgs3 a, const __grid_constant_
         tc::mbar_wait(&empty[s], ((g / ST) & 1) ^ 1);
         if (bytes) mbar_expect_tx(&full[s], bytes); else mbar_arrive(&full[s]);
         if (a.tmaZ)
-          for (int b = 0; b < a.nzb; ++b) tma_load_2d(zhi(s) + b * kBox, &tmZ, &full[s], 32 * b, row);
+          for (int b = 0; b < a.nzb; ++b) tma_load_2d(zraw(s) + b * kBox, &tmZ, &full[s], 32 * b, row);
         if (a.tmaX)
           for (int b = 0; b < a.nxb; ++b) tma_load_2d(xhi(s) + b * kBox, &tmX, &full[s], 32 * b, row);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t id = idesc_tf32(128, nprime, 1, 1);
+      const uint32_t id = idesc_tf32(128, nprime, 0, 1);      // A = dZ^T K-major in TMEM, B MN-major
       for (int g = 0; g < nchunk; ++g) {
         const int s = g % ST;
         tc::mbar_wait(&conv[s], (g / ST) & 1);
         tc::fence_after();
-        const uint32_t ah = tc::smem_u32(zhi(s)), al = tc::smem_u32(zlo(s));
+        const uint32_t ah = tbase + 256 + 64 * s, al = ah + 32;
         const uint32_t bh = tc::smem_u32(xhi(s)), bl = tc::smem_u32(xlo(s));
 #pragma unroll
         for (int j = 0; j < kDwS / 8; ++j) {
           // MN-major, 32-byte-chunk swizzle: 4-sample k-groups 512 B apart, 32-feature groups kBox apart
-          const uint64_t dah = desc_sw128<1>(ah + j * 1024, kBox, 512), dal = desc_sw128<1>(al + j * 1024, kBox, 512);
           const uint64_t dbh = desc_sw128<1>(bh + j * 1024, kBox, 512), dbl = desc_sw128<1>(bl + j * 1024, kBox, 512);
-          mma_tf32(tbase, dal, dbh, id, (g | j) ? 1u : 0u);
-          mma_tf32(tbase, dah, dbl, id, 1u);
-          mma_tf32(tbase, dah, dbh, id, 1u);
+          mma_tf32_ts(tbase, al + 8 * j, dbh, id, (g | j) ? 1u : 0u);
+          mma_tf32_ts(tbase, ah + 8 * j, dbl, id, 1u);
+          mma_tf32_ts(tbase, ah + 8 * j, dbh, id, 1u);
         }
         tc::mma_commit(&empty[s]);
       }
       tc::mma_commit(&tfull);
     }
   } else if (warp >= 4) {
-    const int ct = tid - 128;
-    const bool vz = (a.ldz % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.Z) & 15) == 0);
+    const int ct = tid - 128, quarter = warp & 3;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const bool vx = (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
+    const int n = ct;                                         // this thread's TMEM lane = output neuron
     for (int g = 0; g < nchunk; ++g) {
       const int s = g % ST;
       const int64_t row0 = r0 + (int64_t)g * kDwS;
       tc::mbar_wait(&full[s], (g / ST) & 1);
-      // one pass per operand: 256 16-byte units per box, unit q -> (sample q/8, unit q%8)
-      for (int op = 0; op < 2; ++op) {
-        const bool isz = op == 0;
-        const int nb = isz ? a.nzb : a.nxb;
-        float4* h4 = reinterpret_cast<float4*>(isz ? zhi(s) : xhi(s));
-        float4* l4 = reinterpret_cast<float4*>(isz ? zlo(s) : xlo(s));
-        if (isz ? a.tmaZ : a.tmaX) {
-          for (int q = ct; q < nb * (kBox / 16); q += 128) {
-            float4 h, l;
-            split4(h4[q], h, l);
-            h4[q] = h;
-            l4[q] = l;
-          }
-        } else {
-          const float* base = isz ? a.Z : a.X;
-          const int64_t ld = isz ? a.ldz : a.ldx;
-          const int ncol = isz ? a.N : a.K;
-          for (int q = ct; q < nb * (kBox / 16); q += 128) {
-            const int b = q / (kBox / 16), r = (q / 8) % kDwS, u = q % 8;
-            const int64_t row = row0 + r;
-            float4 h, l;
-            split4(load4(base + row * ld, 32 * b + 4 * u, ncol, isz ? vz : vx, row < r1), h, l);
-            const uint32_t off = (b * kBox + sw32_off(r, u)) >> 4;
-            h4[off] = h;
-            l4[off] = l;
-          }
+      // dZ^T row n (32 samples) -> hi/lo -> TMEM lane n
+      uint32_t hi[32], lo[32];
+      if (a.tmaZ) {
+        const uint8_t* zb = zraw(s) + (n >> 5) * kBox;
+        const uint32_t nb = (uint32_t)(n & 31) * 4;
+#pragma unroll
+        for (int r = 0; r < kDwS; ++r) {
+          const float v = *reinterpret_cast<const float*>(zb + r * 128 + (nb ^ ((r & 3u) << 5)));
+          const float h = rna_tf32(v);
+          hi[r] = __float_as_uint(h);
+          lo[r] = __float_as_uint(v - h);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < kDwS; ++r) {
+          const int64_t row = row0 + r;
+          const float v = (n < a.N && row < r1) ? __ldg(a.Z + row * a.ldz + n) : 0.f;
+          const float h = rna_tf32(v);
+          hi[r] = __float_as_uint(h);
+          lo[r] = __float_as_uint(v - h);
         }
       }
+      const uint32_t ta = tbase + lane_off + 256 + 64 * s;
+      tc::tmem_st32(ta, hi);
+      tc::tmem_st32(ta + 32, lo);
+      // X -> hi (in place) / lo tiles in smem
+      float4* h4 = reinterpret_cast<float4*>(xhi(s));
+      float4* l4 = reinterpret_cast<float4*>(xlo(s));
+      if (a.tmaX) {
+        for (int q = ct; q < a.nxb * (kBox / 16); q += 128) {
+          float4 h, l;
+          split4(h4[q], h, l);
+          h4[q] = h;
+          l4[q] = l;
+        }
+      } else {
+        for (int q = ct; q < a.nxb * (kBox / 16); q += 128) {
+          const int b = q / (kBox / 16), r = (q / 8) % kDwS, u = q % 8;
+          const int64_t row = row0 + r;
+          float4 h, l;
+          split4(load4(a.X + row * a.ldx, 32 * b + 4 * u, a.K, vx, row < r1), h, l);
+          const uint32_t off = (b * kBox + sw32_off(r, u)) >> 4;
+          h4[off] = h;
+          l4[off] = l;
+        }
+      }
+      tc::tmem_st_wait();
+      tc::fence_before();
       tc::fence_proxy_async();
       mbar_arrive(&conv[s]);
     }
@@ -434,8 +455,7 @@ __global__ void __launch_bounds__(256, 1) k_dw(DwArgs3 a, const __grid_constant_
     if (nchunk > 0) {
       tc::mbar_wait(&tfull, 0);
       tc::fence_after();
-      const int n = ct, quarter = warp & 3;
-      const uint32_t taddr = tbase + ((uint32_t)(quarter * 32) << 16);
+      const uint32_t taddr = tbase + lane_off;
       for (int c0 = 0; c0 < nprime; c0 += 16) {
         float v[16];
         tc::tmem_ld16(taddr + c0, v);
@@ -454,7 +474,7 @@ __global__ void __launch_bounds__(256, 1) k_dw(DwArgs3 a, const __grid_constant_
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_free<256>(tbase);
+  if (warp == 1) tc::tmem_free<512>(tbase);
 }
 
 // ============================================================================ host side
@@ -535,7 +555,7 @@ int32_t dw_gemm(DwArgs3 a, cudaStream_t st) {
   const int ncta = num_sms();
   a.rows_per_cta = ((a.M + ncta - 1) / ncta + kDwS - 1) / kDwS * kDwS;
   const int grid = (int)((a.M + a.rows_per_cta - 1) / a.rows_per_cta);
-  const int stage_bytes = (8 + 2 * (a.nxb + 1)) * kBox;
+  const int stage_bytes = (4 + 2 * (a.nxb + 1)) * kBox;
   a.stages = std::min(4, (kSmemMax - 1024) / stage_bytes);
   const size_t smem = 1024 + (size_t)a.stages * stage_bytes;
   cudaFuncSetAttribute(k_dw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

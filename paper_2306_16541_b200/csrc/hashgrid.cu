@@ -27,21 +27,33 @@ __global__ void __launch_bounds__(128) k_hash_fwd(fv_hash h, const float* __rest
 }
 
 // dtable += w_corner * dfeat (float2 vector atomics); dx = sum_l d feat_l / d x.
+// Warp aggregation: a warp holds 32 neighbouring rays at one depth, so at the coarse levels
+// many lanes share a cell.  Lanes are grouped by (level cell) with __match_any_sync; a
+// group's lowest lane sums the members' 8 corner contributions through shared memory and
+// issues one float2 atomic per corner (singletons -- most lanes at the fine levels -- add
+// directly).  Summation order inside a group differs from a per-sample scatter by fp32
+// rounding only (the reference's gather0 scatter-add, ad:335-344, is order-free).
 __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __restrict__ x, int64_t n,
                                                   const float* __restrict__ dfeat, float* __restrict__ dtable,
                                                   float* __restrict__ dx) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= n) return;
+  __shared__ float2 scratch[4][8][33];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t p0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool valid = p0 < n;
+  const int64_t p = valid ? p0 : n - 1;
   float xn[3]; bool mask[3];
   hash_norm(h, x[3 * p], x[3 * p + 1], x[3 * p + 2], xn, mask);
   const uint32_t maskT = (1u << h.log2_T) - 1u;
+  float2* dt2 = reinterpret_cast<float2*>(dtable);
   float gx = 0.f, gy = 0.f, gz = 0.f;
   for (int l = 0; l < h.n_levels; ++l) {
-    const float g0 = dfeat[p * (2 * h.n_levels) + 2 * l];
-    const float g1 = dfeat[p * (2 * h.n_levels) + 2 * l + 1];
+    const float g0 = valid ? dfeat[p * (2 * h.n_levels) + 2 * l] : 0.f;
+    const float g1 = valid ? dfeat[p * (2 * h.n_levels) + 2 * l + 1] : 0.f;
     HashCell c;
     hash_level_cell(xn, h.res[l], c);
     const float wx[2] = {1.f - c.f[0], c.f[0]}, wy[2] = {1.f - c.f[1], c.f[1]}, wz[2] = {1.f - c.f[2], c.f[2]};
+    uint32_t gi[8];
+    float2 v[8];
     float px = 0.f, py = 0.f, pz = 0.f;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -49,16 +61,15 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
       for (int b = 0; b < 2; ++b)
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
-          const uint32_t gi = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + a, c.i0[1] + b,
-                                                       c.i0[2] + cc);
+          const int q = a * 4 + b * 2 + cc;
+          gi[q] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + a, c.i0[1] + b, c.i0[2] + cc);
           const float wgt = wx[a] * wy[b] * wz[cc];
-          if (g0 != 0.f || g1 != 0.f)
-            atomicAdd(reinterpret_cast<float2*>(dtable) + gi, make_float2(wgt * g0, wgt * g1));
+          v[q] = make_float2(wgt * g0, wgt * g1);
           if (dx) {
-            float2 v;
-            if (h.table_half) v = __half22float2(__ldg(reinterpret_cast<const __half2*>(h.d_table) + gi));
-            else v = __ldg(reinterpret_cast<const float2*>(h.d_table) + gi);
-            const float gv = g0 * v.x + g1 * v.y;
+            float2 t;
+            if (h.table_half) t = __half22float2(__ldg(reinterpret_cast<const __half2*>(h.d_table) + gi[q]));
+            else t = __ldg(reinterpret_cast<const float2*>(h.d_table) + gi[q]);
+            const float gv = g0 * t.x + g1 * t.y;
             px += (a ? 1.f : -1.f) * wy[b] * wz[cc] * gv;
             py += wx[a] * (b ? 1.f : -1.f) * wz[cc] * gv;
             pz += wx[a] * wy[b] * (cc ? 1.f : -1.f) * gv;
@@ -66,8 +77,40 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
         }
     const float rf = (float)h.res[l];
     gx += px * rf; gy += py * rf; gz += pz * rf;
+    const bool any = valid && (g0 != 0.f || g1 != 0.f);
+    const uint64_t key = any ? ((uint64_t)(uint32_t)c.i0[0] | ((uint64_t)(uint32_t)c.i0[1] << 21) |
+                                ((uint64_t)(uint32_t)c.i0[2] << 42))
+                             : (~0ull - (uint64_t)lane);
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    const unsigned multi = __ballot_sync(0xffffffffu, grp != (1u << lane));
+    if (grp == (1u << lane)) {
+      if (any) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) atomicAdd(dt2 + gi[q], v[q]);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) scratch[wib][q][lane] = v[q];
+      __syncwarp(multi);
+      if (lane == __ffs(grp) - 1 && any) {
+        unsigned rest = grp & (grp - 1);
+        while (rest) {
+          const int o = __ffs(rest) - 1;
+          rest &= rest - 1;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float2 w = scratch[wib][q][o];
+            v[q].x += w.x;
+            v[q].y += w.y;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) atomicAdd(dt2 + gi[q], v[q]);
+      }
+      __syncwarp(multi);
+    }
   }
-  if (dx) {
+  if (dx && valid) {
     dx[3 * p] = mask[0] ? gx * h.cinv[0] : 0.f;
     dx[3 * p + 1] = mask[1] ? gy * h.cinv[1] : 0.f;
     dx[3 * p + 2] = mask[2] ? gz * h.cinv[2] : 0.f;

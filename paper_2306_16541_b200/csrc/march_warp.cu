@@ -150,39 +150,68 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
 }
 
 // d x_skel -> d W^c (C,G,G,G) via dw_i = <dxs, p_i - x_skel>/L and the trilinear scatter.
-__global__ void k_warp_bwd(fv_warp w, float eps_w, const float* __restrict__ x, int64_t n,
-                           const float* __restrict__ dxs, float* __restrict__ dvol) {
+// dvol[i, corner] += trilinear weight * dL/dw_i (ad:778-789 bincount scatter); dL/dw_i =
+// dL/dx_skel . (G_i(x) - x_skel) / L.  Warp-aggregated like k_hash_bwd: lanes sharing a
+// bone cell (a warp = 32 neighbouring rays at one depth, ~8 rays per 1/32-box cell) sum
+// their 8 corner terms in shared memory and the group's lowest lane issues the atomics.
+__global__ void __launch_bounds__(128) k_warp_bwd(fv_warp w, float eps_w, const float* __restrict__ x, int64_t n,
+                                                  const float* __restrict__ dxs, float* __restrict__ dvol) {
   __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
+  __shared__ float scratch[4][8][33];
   for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
   __syncthreads();
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= n) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool live = q0 < n;
+  const int64_t q = live ? q0 : n - 1;
   const float g0 = dxs[3 * q], g1 = dxs[3 * q + 1], g2 = dxs[3 * q + 2];
-  if (g0 == 0.f && g1 == 0.f && g2 == 0.f) return;
+  live = live && !(g0 == 0.f && g1 == 0.f && g2 == 0.f);
+  if (!__any_sync(0xffffffffu, live)) return;
   const float x0 = x[3 * q], x1 = x[3 * q + 1], x2 = x[3 * q + 2];
   float xsk[3];
   const float L = warp_point<false>(w, sg, eps_w, x0, x1, x2, xsk);
-  if (!(L > eps_w)) return;
-  const float invL = 1.f / L;
+  live = live && (L > eps_w);
+  const float invL = live ? 1.f / L : 0.f;
   const int G = w.vol_res;
   for (int i = 0; i < w.n_bones; ++i) {
     float p[3];
     bone_point(sg + 12 * i, x0, x1, x2, p);
     int i0[3]; float f[3];
-    if (!warp_cell(w, p, i0, f)) continue;
+    const bool in = warp_cell(w, p, i0, f);
     const float dw = (g0 * (p[0] - xsk[0]) + g1 * (p[1] - xsk[1]) + g2 * (p[2] - xsk[2])) * invL;
-    if (dw == 0.f) continue;
+    const bool any = live && in && dw != 0.f;
     const float wx[2] = {1.f - f[0], f[0]}, wy[2] = {1.f - f[1], f[1]}, wz[2] = {1.f - f[2], f[2]};
+    float v[8];
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int c = 0; c < 8; ++c) v[c] = wx[c >> 2] * wy[(c >> 1) & 1] * wz[c & 1] * dw;
+    const uint32_t key = any ? (uint32_t)vol_cell_index(i, G, i0) : (0xFFFFFFFFu - (uint32_t)lane);
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    const unsigned multi = __ballot_sync(0xffffffffu, grp != (1u << lane));
+    bool lead = any;
+    if (grp != (1u << lane)) {
 #pragma unroll
-      for (int b = 0; b < 2; ++b)
+      for (int c = 0; c < 8; ++c) scratch[wib][c][lane] = v[c];
+      __syncwarp(multi);
+      lead = any && lane == __ffs(grp) - 1;
+      if (lead) {
+        unsigned rest = grp & (grp - 1);
+        while (rest) {
+          const int o = __ffs(rest) - 1;
+          rest &= rest - 1;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int vx = i0[0] + a - 1, vy = i0[1] + b - 1, vz = i0[2] + c - 1;
-          if (vx < 0 || vx >= G || vy < 0 || vy >= G || vz < 0 || vz >= G) continue;
-          atomicAdd(dvol + (((int64_t)i * G + vx) * G + vy) * G + vz, wx[a] * wy[b] * wz[c] * dw);
+          for (int c = 0; c < 8; ++c) v[c] += scratch[wib][c][o];
         }
+      }
+      __syncwarp(multi);
+    }
+    if (lead) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int vx = i0[0] + (c >> 2) - 1, vy = i0[1] + ((c >> 1) & 1) - 1, vz = i0[2] + (c & 1) - 1;
+        if (vx < 0 || vx >= G || vy < 0 || vy >= G || vz < 0 || vz >= G) continue;
+        atomicAdd(dvol + (((int64_t)i * G + vx) * G + vy) * G + vz, v[c]);
+      }
+    }
   }
 }
 
