@@ -193,6 +193,16 @@ int32_t fv_linear_bwd_tc(const float* d_x, int64_t ldx, const float* d_w, const 
                          int64_t ldz, float* d_dx, int64_t lddx, const float* d_xmask,
                          float* d_dw, float* d_db, int64_t m, int32_t k_in, int32_t n_out,
                          void* stream);
+/* Same layer ops with the ReLU mask as bits: the forward writes bit (y > 0) of every output
+ * ([m][ceil(n_out/32)] uint32 words, bit j of word w <-> column 32w + j; d_relu_bits may be
+ * NULL) and the backward masks dx with such bits of the layer input ([m][ceil(k_in/32)]). */
+int32_t fv_linear_fwd_tc_bits(const float* d_x, int64_t ldx, const float* d_w, const float* d_b,
+                              float* d_y, int64_t ldy, int64_t m, int32_t k_in, int32_t n_out,
+                              int32_t act, uint32_t* d_relu_bits, void* stream);
+int32_t fv_linear_bwd_tc_bits(const float* d_x, int64_t ldx, const float* d_w, const float* d_dz,
+                              int64_t ldz, float* d_dx, int64_t lddx, const uint32_t* d_xmask_bits,
+                              float* d_dw, float* d_db, int64_t m, int32_t k_in, int32_t n_out,
+                              void* stream);
 int32_t fv_posenc_bwd(const float* d_xs, int64_t n, float eps_w, int32_t bands, const float* w,
                       const float* d_dpe, int64_t ld, float* d_dx, void* stream);
 /* x_final = x_skel + x_res on foreground rows; d_xres may be NULL. */

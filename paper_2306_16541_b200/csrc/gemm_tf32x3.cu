@@ -67,6 +67,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(tc::smem_u32(src)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory"); }
+
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
 }
@@ -112,7 +121,8 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_
                :: "r"(d), "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
 }
 
-__global__ void __launch_bounds__(384, 1) k_rows(RowsArgs a, const __grid_constant__ CUtensorMap tmA) {
+__global__ void __launch_bounds__(384, 1) k_rows(RowsArgs a, const __grid_constant__ CUtensorMap tmA,
+                                                const __grid_constant__ CUtensorMap tmO) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[8], empty[8], aready[kAStages], afree[kAStages], tfull[2], tempty[2];
@@ -242,69 +252,154 @@ __global__ void __launch_bounds__(384, 1) k_rows(RowsArgs a, const __grid_consta
     }
   } else if (warp >= 8) {
     // ------------------------------------------------------------ epilogue
+    // Row et of the tile per thread, 32-column groups; the TMEM load of group cg+1 is in
+    // flight while group cg is processed.  Output: each warp stages its 32 rows x 32
+    // columns in a 128B-swizzled smem buffer (double-buffered per warp) and one lane issues
+    // a TMA bulk-tensor store; direct row stores when TMA cannot address the output.
+    // ReLU bits in/out: one uint32 per 32 columns per row.
     const int et = tid - 256, quarter = warp & 3;
     const bool vout = (a.ldo % 4 == 0) && (a.N % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0) &&
                       (!a.mask || ((a.ldm % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.mask) & 15) == 0)));
-    uint32_t it = 0;
+    const int ngroups = (a.Np + 31) / 32, nw = (a.N + 31) / 32;
+    uint8_t* wbuf = sRaw + ST * kStageA + quarter * 2 * 4096;
+    uint32_t it = 0, wcount = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t acc = it & 1;
+      const int64_t m = tile * 128 + et;
+      const bool rowok = m < a.M;
+      uint32_t mb[4] = {~0u, ~0u, ~0u, ~0u};
+      if (a.bits_in && rowok) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          if (w < nw) mb[w] = __ldg(a.bits_in + m * nw + w);
+      }
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after();
-      const int64_t m = tile * 128 + et;
       const uint32_t taddr = tbase + acc * 128 + ((uint32_t)(quarter * 32) << 16);
-      auto emit = [&](int n0, float (&v)[16], const float4 (&mk)[4]) {
-        if (m >= a.M) return;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          v[j] += sbias[(n0 + j) & 127];
-          if (a.act == 1) v[j] = fmaxf(v[j], 0.f);
+      float va[16], vb[16];
+      tc::tmem_ld16(taddr, va);
+      if (16 < a.Np) tc::tmem_ld16(taddr + 16, vb);
+      tc::tmem_ld_wait();
+      for (int cg = 0; cg < ngroups; ++cg) {
+        const int n0 = 32 * cg;
+        const bool more = cg + 1 < ngroups;
+        float na[16], nb[16];
+        if (more) {
+          tc::tmem_ld16(taddr + n0 + 32, na);
+          if (n0 + 48 < a.Np) tc::tmem_ld16(taddr + n0 + 48, nb);
+        } else {                          // accumulator fully read: the MMA may reuse it
+          tc::fence_before();
+          mbar_arrive(&tempty[acc]);
         }
-        if (vout) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int n = n0 + 4 * q;
-            if (n >= a.N) break;
-            float4 y = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            if (a.mask) {
-              y.x = mk[q].x > 0.f ? y.x : 0.f; y.y = mk[q].y > 0.f ? y.y : 0.f;
-              y.z = mk[q].z > 0.f ? y.z : 0.f; y.w = mk[q].w > 0.f ? y.w : 0.f;
-            }
-            *reinterpret_cast<float4*>(a.out + m * a.ldo + n) = y;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = n0 + j;
-            if (n < a.N) {
-              float y = v[j];
-              if (a.mask && !(__ldg(a.mask + m * a.ldm + n) > 0.f)) y = 0.f;
-              a.out[m * a.ldo + n] = y;
-            }
-          }
-        }
-      };
-      for (int n0 = 0; n0 < a.Np; n0 += 32) {   // two 16-column TMEM loads per wait
-        float va[16], vb[16];
-        float4 ma[4], mb[4];
-        const bool two = n0 + 16 < a.Np;
-        if (a.mask && vout && m < a.M) {   // issue the mask loads (L2 hits) before the TMEM wait
+        float4 ma[4], mbf[4];
+        if (a.mask && vout && rowok) {   // float mask (legacy form)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             ma[q] = n0 + 4 * q < a.N ? __ldg(reinterpret_cast<const float4*>(a.mask + m * a.ldm + n0 + 4 * q))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-            mb[q] = n0 + 16 + 4 * q < a.N ? __ldg(reinterpret_cast<const float4*>(a.mask + m * a.ldm + n0 + 16 + 4 * q))
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            mbf[q] = n0 + 16 + 4 * q < a.N
+                         ? __ldg(reinterpret_cast<const float4*>(a.mask + m * a.ldm + n0 + 16 + 4 * q))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
-        tc::tmem_ld16(taddr + n0, va);
-        if (two) tc::tmem_ld16(taddr + n0 + 16, vb);
-        tc::tmem_ld_wait();
-        emit(n0, va, ma);
-        if (two) emit(n0 + 16, vb, mb);
+        uint32_t bits = 0;
+        const uint32_t mw = cg == 0 ? mb[0] : cg == 1 ? mb[1] : cg == 2 ? mb[2] : mb[3];
+        // bias of the 32 columns as 8 broadcast float4 shared loads
+        float bias[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 b4 = *reinterpret_cast<const float4*>(sbias + ((n0 + 4 * q) & 127));
+          bias[4 * q] = b4.x; bias[4 * q + 1] = b4.y; bias[4 * q + 2] = b4.z; bias[4 * q + 3] = b4.w;
+        }
+        const uint32_t live = a.N - n0 >= 32 ? 0xFFFFFFFFu : ((1u << (a.N - n0)) - 1u);   // columns < N
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float y = va[j] + bias[j];
+          if (a.act == 1) y = fmaxf(y, 0.f);
+          va[j] = y;
+          float z = vb[j] + bias[16 + j];
+          if (a.act == 1) z = fmaxf(z, 0.f);
+          vb[j] = z;
+        }
+        if (a.bits_in) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            va[j] = (mw >> j) & 1u ? va[j] : 0.f;
+            vb[j] = (mw >> (16 + j)) & 1u ? vb[j] : 0.f;
+          }
+        }
+        if (a.mask) {   // legacy float-mask form
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (vout) {
+              const float4 x = ma[q], z = mbf[q];
+              va[4 * q] = x.x > 0.f ? va[4 * q] : 0.f;     va[4 * q + 1] = x.y > 0.f ? va[4 * q + 1] : 0.f;
+              va[4 * q + 2] = x.z > 0.f ? va[4 * q + 2] : 0.f; va[4 * q + 3] = x.w > 0.f ? va[4 * q + 3] : 0.f;
+              vb[4 * q] = z.x > 0.f ? vb[4 * q] : 0.f;     vb[4 * q + 1] = z.y > 0.f ? vb[4 * q + 1] : 0.f;
+              vb[4 * q + 2] = z.z > 0.f ? vb[4 * q + 2] : 0.f; vb[4 * q + 3] = z.w > 0.f ? vb[4 * q + 3] : 0.f;
+            } else if (rowok) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int n = n0 + 4 * q + e;
+                if (n < a.N && !(__ldg(a.mask + m * a.ldm + n) > 0.f)) va[4 * q + e] = 0.f;
+                if (n + 16 < a.N && !(__ldg(a.mask + m * a.ldm + n + 16) > 0.f)) vb[4 * q + e] = 0.f;
+              }
+            }
+          }
+        }
+        if (a.bits_out) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            bits |= (va[j] > 0.f ? 1u : 0u) << j;
+            bits |= (vb[j] > 0.f ? 1u : 0u) << (16 + j);
+          }
+          bits &= live;
+        }
+        if (a.bits_out && rowok) a.bits_out[m * nw + cg] = bits;
+        if (a.tma_out) {
+          uint8_t* ob = wbuf + (wcount & 1) * 4096;
+          if (lane == 0) bulk_wait_read<1>();      // the store that used this buffer has read it
+          __syncwarp();
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<float4*>(ob + sw_off(lane, u)) = make_float4(va[4 * u], va[4 * u + 1], va[4 * u + 2], va[4 * u + 3]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<float4*>(ob + sw_off(lane, 4 + u)) =
+                make_float4(vb[4 * u], vb[4 * u + 1], vb[4 * u + 2], vb[4 * u + 3]);
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmO, ob, n0, (int)(tile * 128 + quarter * 32));
+            bulk_commit();
+          }
+          ++wcount;
+        } else if (rowok) {
+          auto store16 = [&](const float (&v)[16], int nb0) {
+            if (vout) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int n = nb0 + 4 * q;
+                if (n >= a.N) break;
+                *reinterpret_cast<float4*>(a.out + m * a.ldo + n) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (nb0 + j < a.N) a.out[m * a.ldo + nb0 + j] = v[j];
+            }
+          };
+          store16(va, n0);
+          if (n0 + 16 < a.Np) store16(vb, n0 + 16);
+        }
+        if (more) {
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) { va[j] = na[j]; vb[j] = nb[j]; }
+        }
       }
-      tc::fence_before();
-      mbar_arrive(&tempty[acc]);
     }
+    if (a.tma_out && lane == 0) bulk_wait_read<0>();
   }
   tc::fence_before();
   __syncthreads();
@@ -531,16 +626,21 @@ int32_t rows_gemm(RowsArgs a, cudaStream_t st) {
   a.nkc = (a.K + 31) / 32;
   a.nsteps = (a.K + 7) / 8;
   if (a.M == 0) return FV_OK;
-  CUtensorMap tm{};
+  CUtensorMap tm{}, to{};
   a.tma = make_tmap(&tm, a.A, a.K, a.M, a.lda, 128) ? 1 : 0;
+  static const int dbg = [] { const char* e = std::getenv("FV_G3_DBG"); return e ? atoi(e) : 0; }();
+  a.dbg = dbg;
+  static const bool no_out = [] { const char* e = std::getenv("FV_G3_NOTMAOUT"); return e && e[0] == '1'; }();
+  a.tma_out = !no_out && make_tmap(&to, a.out, a.N, a.M, a.ldo, 32) ? 1 : 0;
   const int bbytes = 2 * a.nkc * a.Np * 128;
-  a.stages = std::min(8, (kSmemMax - 2048 - bbytes) / kStageA);
+  const int obytes = a.tma_out ? 2 * kStageA : 0;
+  a.stages = std::min(6, (kSmemMax - 2048 - bbytes - obytes) / kStageA);
   if (a.stages < 2) return set_error(FV_EDIM, "rows_gemm: B operand too large for shared memory");
-  const size_t smem = 1024 + bbytes + (size_t)a.stages * kStageA;
+  const size_t smem = 1024 + bbytes + (size_t)a.stages * kStageA + obytes;
   cudaFuncSetAttribute(k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = (a.M + 127) / 128;
   const int grid = (int)std::min<int64_t>(ntiles, num_sms());
-  k_rows<<<grid, 384, smem, st>>>(a, tm);
+  k_rows<<<grid, 384, smem, st>>>(a, tm, to);
   return check_launch("k_rows");
 }
 

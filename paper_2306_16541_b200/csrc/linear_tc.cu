@@ -427,3 +427,37 @@ extern "C" int32_t fv_linear_bwd_tc(const float* d_x, int64_t ldx, const float* 
   }
   return FV_OK;
 }
+
+// Bit-mask forms (training path): the forward also writes the ReLU mask as bits
+// (bit j of word w of row m <-> output column 32w + j is > 0, [m][ceil(n_out/32)] words),
+// and the backward applies such bits to dx instead of reading the float activations.
+extern "C" int32_t fv_linear_fwd_tc_bits(const float* d_x, int64_t ldx, const float* d_w, const float* d_b,
+                                         float* d_y, int64_t ldy, int64_t m, int32_t k_in, int32_t n_out,
+                                         int32_t act, uint32_t* d_relu_bits, void* stream) {
+  if (m < 0 || k_in < 1 || k_in > 256 || n_out < 1 || n_out > 128 || ldx < k_in || ldy < n_out)
+    return set_error(FV_EDIM, "fv_linear_fwd_tc_bits: bad shape");
+  if (m == 0) return FV_OK;
+  g3::RowsArgs r{d_x, ldx, k_in, d_w, 1, n_out, n_out, d_b, act, nullptr, 0, d_y, ldy, m};
+  r.bits_out = d_relu_bits;
+  return g3::rows_gemm(r, (cudaStream_t)stream);
+}
+
+extern "C" int32_t fv_linear_bwd_tc_bits(const float* d_x, int64_t ldx, const float* d_w, const float* d_dz,
+                                         int64_t ldz, float* d_dx, int64_t lddx, const uint32_t* d_xmask_bits,
+                                         float* d_dw, float* d_db, int64_t m, int32_t k_in, int32_t n_out,
+                                         void* stream) {
+  if (m < 0 || k_in < 1 || k_in > 128 || n_out < 1 || n_out > 128 || ldx < k_in || ldz < n_out)
+    return set_error(FV_EDIM, "fv_linear_bwd_tc_bits: bad shape");
+  if (m == 0) return FV_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (d_dx) {
+    g3::RowsArgs r{d_dz, ldz, n_out, d_w, n_out, 1, k_in, nullptr, 0, nullptr, 0, d_dx, lddx, m};
+    r.bits_in = d_xmask_bits;
+    if (int32_t e = g3::rows_gemm(r, st)) return e;
+  }
+  if (d_dw) {
+    g3::DwArgs3 w{d_x, ldx, k_in, d_dz, ldz, n_out, d_dw, d_db, m};
+    if (int32_t e = g3::dw_gemm(w, st)) return e;
+  }
+  return FV_OK;
+}

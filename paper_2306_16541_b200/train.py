@@ -87,6 +87,10 @@ class Trainer:
         self.x = torch.empty((S, 3), **f32)
         self.pe = torch.empty((S, self.pe_ld), **f32)
         self.h = [torch.empty((S, 128), **f32) for _ in range(4)]
+        # ReLU masks of the hidden activations as bits (tensor-core path): 1 uint32 per 32 units
+        i32 = dict(device=dev, dtype=torch.int32)
+        self.hbits = [torch.empty((S, 4), **i32) for _ in range(4)] if self.tc else [None] * 4
+        self.rbits = [torch.empty((S, 2), **i32) for _ in range(2)] if self.tc else [None] * 2
         self.xres = torch.empty((S, 3), **f32)
         self.xf = torch.empty((S, 3), **f32)
         self.feat = torch.empty((S, 32), **f32)
@@ -123,23 +127,25 @@ class Trainer:
         self.table_elems = nets.views["table"].numel()
 
     # ------------------------------------------------------------------------------------
-    def _lin(self, x, w, b, y, k, n, act, sp):
+    def _lin(self, x, w, b, y, k, n, act, sp, bits=None):
         bp = b.data_ptr() if b is not None else None
         if self.tc:
-            _lib.check(self.lib.fv_linear_fwd_tc(x.data_ptr(), x.shape[1], w.data_ptr(), bp, y.data_ptr(), y.shape[1],
-                                                 self.S, k, n, act, sp), "fv_linear_fwd_tc")
+            _lib.check(self.lib.fv_linear_fwd_tc_bits(x.data_ptr(), x.shape[1], w.data_ptr(), bp, y.data_ptr(),
+                                                      y.shape[1], self.S, k, n, act,
+                                                      bits.data_ptr() if bits is not None else None, sp),
+                       "fv_linear_fwd_tc_bits")
         else:
             _lib.check(self.lib.fv_linear_fwd(x.data_ptr(), w.data_ptr(), bp, y.data_ptr(), self.S, k, n, act, sp),
                        "fv_linear_fwd")
 
-    def _lin_bwd_tc(self, x, w, dz, dx, xmask, dw, db, k, n, sp):
-        """dz = masked pre-activation gradient of this layer; dx gets (dz W^T) * (xmask > 0),
-        i.e. the masked dz of the previous layer when xmask is that layer's ReLU output."""
-        _lib.check(self.lib.fv_linear_bwd_tc(x.data_ptr(), x.shape[1], w.data_ptr(), dz.data_ptr(), dz.shape[1],
-                                             dx.data_ptr() if dx is not None else None,
-                                             dx.shape[1] if dx is not None else 0,
-                                             xmask.data_ptr() if xmask is not None else None, dw.data_ptr(),
-                                             db.data_ptr(), self.S, k, n, sp), "fv_linear_bwd_tc")
+    def _lin_bwd_tc(self, x, w, dz, dx, xbits, dw, db, k, n, sp):
+        """dz = masked pre-activation gradient of this layer; dx gets (dz W^T) * xbits, the
+        previous layer's ReLU bits -> the masked dz of that layer."""
+        _lib.check(self.lib.fv_linear_bwd_tc_bits(x.data_ptr(), x.shape[1], w.data_ptr(), dz.data_ptr(), dz.shape[1],
+                                                  dx.data_ptr() if dx is not None else None,
+                                                  dx.shape[1] if dx is not None else 0,
+                                                  xbits.data_ptr() if xbits is not None else None, dw.data_ptr(),
+                                                  db.data_ptr(), self.S, k, n, sp), "fv_linear_bwd_tc_bits")
 
     def _lin_bwd(self, x, w, y, dy, dx, dw, db, k, n, act, sp):
         _lib.check(self.lib.fv_linear_bwd(x.data_ptr(), w.data_ptr(), y.data_ptr(), dy.data_ptr(),
@@ -161,14 +167,14 @@ class Trainer:
         V = nets.views
         _lib.check(lib.fv_posenc_fwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.pe.data_ptr(), self.pe_ld,
                                      sp))
-        self._lin(self.pe, V["off_w0"], nets.b0_eff, self.h[0], self.d_pe, 128, 1, sp)
+        self._lin(self.pe, V["off_w0"], nets.b0_eff, self.h[0], self.d_pe, 128, 1, sp, self.hbits[0])
         for i in range(1, 4):
-            self._lin(self.h[i - 1], V[f"off_w{i}"], V[f"off_b{i}"], self.h[i], 128, 128, 1, sp)
+            self._lin(self.h[i - 1], V[f"off_w{i}"], V[f"off_b{i}"], self.h[i], 128, 128, 1, sp, self.hbits[i])
         self._lin(self.h[3], V["off_w4"], V["off_b4"], self.xres, 128, 3, 0, sp)
         _lib.check(lib.fv_xfinal(self.xs.data_ptr(), self.xres.data_ptr(), S, eps, self.xf.data_ptr(), sp))
         _lib.check(lib.fv_hash_fwd(C.byref(h), self.xf.data_ptr(), S, self.feat.data_ptr(), None, sp), "fv_hash_fwd")
-        self._lin(self.feat, V["rad_w0"], V["rad_b0"], self.r[0], 32, 64, 1, sp)
-        self._lin(self.r[0], V["rad_w1"], V["rad_b1"], self.r[1], 64, 64, 1, sp)
+        self._lin(self.feat, V["rad_w0"], V["rad_b0"], self.r[0], 32, 64, 1, sp, self.rbits[0])
+        self._lin(self.r[0], V["rad_w1"], V["rad_b1"], self.r[1], 64, 64, 1, sp, self.rbits[1])
         self._lin(self.r[1], V["rad_w2"], V["rad_b2"], self.hd, 64, 4, 0, sp)
         _lib.check(lib.fv_heads_fwd(self.xs.data_ptr(), self.hd.data_ptr(), S, eps, self.rgbs.data_ptr(), sp))
         _lib.check(lib.fv_composite_fwd(self.rgbs.data_ptr(), self.delta.data_ptr(), self.xs[:, 3:].data_ptr(), 4, 1,
@@ -191,15 +197,15 @@ class Trainer:
                                     self.dh.data_ptr(), sp))
         h = nets.hash_struct()
         if self.tc:  # dz-form: each dx epilogue applies the previous layer's ReLU mask
-            self._lin_bwd_tc(self.r[1], V["rad_w2"], self.dh, self.g64[0], self.r[1], G["rad_w2"], G["rad_b2"], 64, 4, sp)
-            self._lin_bwd_tc(self.r[0], V["rad_w1"], self.g64[0], self.g64[1], self.r[0], G["rad_w1"], G["rad_b1"], 64, 64, sp)
+            self._lin_bwd_tc(self.r[1], V["rad_w2"], self.dh, self.g64[0], self.rbits[1], G["rad_w2"], G["rad_b2"], 64, 4, sp)
+            self._lin_bwd_tc(self.r[0], V["rad_w1"], self.g64[0], self.g64[1], self.rbits[0], G["rad_w1"], G["rad_b1"], 64, 64, sp)
             self._lin_bwd_tc(self.feat, V["rad_w0"], self.g64[1], self.dfeat, None, G["rad_w0"], G["rad_b0"], 32, 64, sp)
             _lib.check(lib.fv_hash_bwd(C.byref(h), self.xf.data_ptr(), S, self.dfeat.data_ptr(),
                                        G["table"].data_ptr(), self.dxf.data_ptr(), sp), "fv_hash_bwd")
-            self._lin_bwd_tc(self.h[3], V["off_w4"], self.dxf, self.g128[0], self.h[3], G["off_w4"], G["off_b4"], 128, 3, sp)
-            self._lin_bwd_tc(self.h[2], V["off_w3"], self.g128[0], self.g128[1], self.h[2], G["off_w3"], G["off_b3"], 128, 128, sp)
-            self._lin_bwd_tc(self.h[1], V["off_w2"], self.g128[1], self.g128[0], self.h[1], G["off_w2"], G["off_b2"], 128, 128, sp)
-            self._lin_bwd_tc(self.h[0], V["off_w1"], self.g128[0], self.g128[1], self.h[0], G["off_w1"], G["off_b1"], 128, 128, sp)
+            self._lin_bwd_tc(self.h[3], V["off_w4"], self.dxf, self.g128[0], self.hbits[3], G["off_w4"], G["off_b4"], 128, 3, sp)
+            self._lin_bwd_tc(self.h[2], V["off_w3"], self.g128[0], self.g128[1], self.hbits[2], G["off_w3"], G["off_b3"], 128, 128, sp)
+            self._lin_bwd_tc(self.h[1], V["off_w2"], self.g128[1], self.g128[0], self.hbits[1], G["off_w2"], G["off_b2"], 128, 128, sp)
+            self._lin_bwd_tc(self.h[0], V["off_w1"], self.g128[0], self.g128[1], self.hbits[0], G["off_w1"], G["off_b1"], 128, 128, sp)
             self._lin_bwd_tc(self.pe, V["off_w0"], self.g128[1], self.dpe, None, G["off_w0"], G["off_b0"], self.d_pe, 128, sp)
         else:
             self._lin_bwd(self.r[1], V["rad_w2"], self.hd, self.dh, self.g64[0], G["rad_w2"], G["rad_b2"], 64, 4, 0, sp)

@@ -106,6 +106,50 @@ def test_linear_tf32_tensor_core_layers(m, k, ld, n, act):
     _close(db.cpu().numpy(), dz.sum(0, dtype=np.float64), 1e-5, "db")
 
 
+@pytest.mark.parametrize("m,k,n", [(3000, 39, 128), (2999, 128, 128), (5000, 32, 64), (777, 64, 40)])
+def test_linear_tc_relu_bits(m, k, n):
+    """fv_linear_fwd_tc_bits writes bit (y > 0) per output; fv_linear_bwd_tc_bits masks dx
+    with such bits exactly as the float-mask form does (bit-exact outputs)."""
+    rng = np.random.default_rng(m + n)
+    x = rng.normal(size=(m, k)).astype(np.float32)
+    w = (rng.normal(size=(k, n)) / np.sqrt(k)).astype(np.float32)
+    b = rng.normal(size=n).astype(np.float32)
+    lib = _lib.load()
+    xt, wt, bt = _t(x), _t(w), _t(b)
+    nw = (n + 31) // 32
+    y = torch.empty((m, n), device=DEV)
+    bits = torch.full((m, nw), -1, device=DEV, dtype=torch.int32)
+    _lib.check(lib.fv_linear_fwd_tc_bits(xt.data_ptr(), k, wt.data_ptr(), bt.data_ptr(), y.data_ptr(), n, m, k, n, 1,
+                                         bits.data_ptr(), _lib.stream_ptr()))
+    yn = y.cpu().numpy()
+    bn = bits.cpu().numpy().view(np.uint32)
+    ref_bits = np.zeros((m, nw), np.uint32)
+    for j in range(n):
+        ref_bits[:, j // 32] |= (yn[:, j] > 0).astype(np.uint32) << np.uint32(j % 32)
+    assert np.array_equal(bn, ref_bits)
+    # backward of the NEXT layer (input = y, width n) with bits vs float mask
+    n2 = 48
+    w2 = (rng.normal(size=(n, n2)) / np.sqrt(n)).astype(np.float32)
+    dz = rng.normal(size=(m, n2)).astype(np.float32)
+    w2t, dzt = _t(w2), _t(dz)
+    outs = []
+    for form in ("bits", "float"):
+        dx = torch.zeros((m, n), device=DEV)
+        dw = torch.zeros((n, n2), device=DEV)
+        db = torch.zeros(n2, device=DEV)
+        if form == "bits":
+            _lib.check(lib.fv_linear_bwd_tc_bits(y.data_ptr(), n, w2t.data_ptr(), dzt.data_ptr(), n2, dx.data_ptr(), n,
+                                                 bits.data_ptr(), dw.data_ptr(), db.data_ptr(), m, n, n2,
+                                                 _lib.stream_ptr()))
+        else:
+            _lib.check(lib.fv_linear_bwd_tc(y.data_ptr(), n, w2t.data_ptr(), dzt.data_ptr(), n2, dx.data_ptr(), n,
+                                            y.data_ptr(), dw.data_ptr(), db.data_ptr(), m, n, n2, _lib.stream_ptr()))
+        outs.append(dx.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    dxr = (dz.astype(np.float64) @ w2.T.astype(np.float64)) * (yn > 0)
+    _close(outs[0], dxr, 2e-5, "dx(bits)")
+
+
 def test_hash_bwd_matches_oracle():
     sc = make("c1", table_scale=0.5)
     nets = FreeviewModel(sc)

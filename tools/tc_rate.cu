@@ -42,7 +42,9 @@ __global__ void __launch_bounds__(128) k_rate(int reps, long long* cycles) {
   tc::fence_after();
   const uint32_t tb = tmem_base;
   const uint32_t sA = tc::smem_u32(smem), sB = sA + 128 * 128 * 2;
-  constexpr uint32_t idesc = tc::idesc_f16(128, N);
+  constexpr uint32_t idesc = MODE >= 3 ? ((1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+                                          ((uint32_t)(128 >> 4) << 24))
+                                       : tc::idesc_f16(128, N);
   if (t == 0) {
     long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
@@ -55,8 +57,18 @@ __global__ void __launch_bounds__(128) k_rate(int reps, long long* cycles) {
           const uint32_t kb = (k & 3) * 32 + (k >> 2) * 128 * 128;
           tc::mma_f16(tb, desc_sw(sA + kb, 16, 1024, 2), desc_sw(sB + (k & 3) * 32 + (k >> 2) * N * 128, 16, 1024, 2),
                       idesc, 1u);
-        } else {                  // A in TMEM columns [256, 320): K=16 fp16 = 8 columns per MMA
+        } else if (MODE == 2) {   // A in TMEM columns [256, 320): K=16 fp16 = 8 columns per MMA
           mma_ts(tb, tb + 256 + k * 8, tc::make_desc(sB + k * 2 * N * 16, N * 16, 128), idesc, 1u);
+        } else if (MODE == 3) {   // kind::tf32, A in TMEM (K=8 = 8 columns), B SW128 K-major
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                       :: "r"(tb), "r"(tb + 256 + k * 8), "l"(desc_sw(sB + (k & 3) * 32 + (k >> 2) * N * 128, 16, 1024, 2)),
+                          "r"(idesc), "r"(1u));
+        } else {                  // kind::tf32, A and B SW128 K-major in smem
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+                       :: "r"(tb), "l"(desc_sw(sA + (k & 3) * 32 + (k >> 2) * 128 * 128, 16, 1024, 2)),
+                          "l"(desc_sw(sB + (k & 3) * 32 + (k >> 2) * N * 128, 16, 1024, 2)), "r"(idesc), "r"(1u));
         }
       }
     }
@@ -296,6 +308,14 @@ int main() {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   long long* d;
   cudaMalloc(&d, 512 * sizeof(long long));
+  if (getenv("TF32")) {
+    run<2, 128>("f16_ts", d, nsm);
+    run<3, 128>("tf32_ts", d, nsm);
+    run<4, 128>("tf32_ss", d, nsm);
+    run<3, 144>("tf32_ts", d, nsm);
+    run<3, 64>("tf32_ts", d, nsm);
+    return 0;
+  }
   if (getenv("FULL")) {
   run<0, 128>("ss_none", d, nsm);
   run<1, 128>("ss_128b", d, nsm);
