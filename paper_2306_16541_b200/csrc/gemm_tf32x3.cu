@@ -80,10 +80,10 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
 }
 
+// round-to-nearest (ties away) to tf32 = cvt.rna.tf32.f32 for finite inputs, as 2 integer
+// ops on the bit pattern (the cvt is emulated with an extra inf/nan guard we do not need)
 __device__ __forceinline__ float rna_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 __device__ __forceinline__ void split4(const float4 v, float4& hi, float4& lo) {
   hi = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(384, 1) k_rows(RowsArgs a, const __grid_consta
 constexpr int kDwS = 32;                  // samples per stage (4 MMA k-steps of 8)
 constexpr int kBox = kDwS * 128;          // bytes of one 32-feature x 32-sample swizzled box
 
-__global__ void __launch_bounds__(256, 1) k_dw(DwArgs3 a, const __grid_constant__ CUtensorMap tmX,
+__global__ void __launch_bounds__(384, 1) k_dw(DwArgs3 a, const __grid_constant__ CUtensorMap tmX,
                                                const __grid_constant__ CUtensorMap tmZ) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -436,7 +436,9 @@ __global__ void __launch_bounds__(256, 1) k_dw(DwArgs3 a, const __grid_constant_
     reinterpret_cast<float4*>(sm)[i] = make_float4(v, v, v, v);
   }
   if (tid == 0) {
-    for (int s = 0; s < 4; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&conv[s], 128); tc::mbar_init(&empty[s], 1); }
+    // narrow unaligned dZ: the producer warp's 32 lanes also arrive (cp.async completion)
+    const uint32_t nfull = (!a.tmaZ && a.N <= 16) ? 33u : 1u;
+    for (int s = 0; s < 4; ++s) { tc::mbar_init(&full[s], nfull); tc::mbar_init(&conv[s], 256); tc::mbar_init(&empty[s], 1); }
     tc::mbar_init(&tfull, 1);
     tc::mbar_fence_init();
   }
@@ -452,17 +454,34 @@ __global__ void __launch_bounds__(256, 1) k_dw(DwArgs3 a, const __grid_constant_
   const int nprime = 32 * a.nxb + 16;
 
   if (warp == 0) {
-    if (lane == 0) {
-      const uint32_t bytes = (uint32_t)((a.tmaZ ? a.nzb : 0) + (a.tmaX ? a.nxb : 0)) * kBox;
-      for (int g = 0; g < nchunk; ++g) {
-        const int s = g % ST;
-        const int row = (int)(r0 + (int64_t)g * kDwS);
-        tc::mbar_wait(&empty[s], ((g / ST) & 1) ^ 1);
+    // producer: TMA boxes (lane 0); a narrow unaligned dZ (N <= 16, e.g. the 3-wide residual
+    // output) is gathered by all 32 lanes with 4-byte cp.async straight into the swizzled
+    // zraw box, completion tracked by the same full barrier (cp.async.mbarrier.arrive.noinc)
+    const bool zcoop = !a.tmaZ && a.N <= 16;
+    const uint32_t bytes = (uint32_t)((a.tmaZ ? a.nzb : 0) + (a.tmaX ? a.nxb : 0)) * kBox;
+    for (int g = 0; g < nchunk; ++g) {
+      const int s = g % ST;
+      const int64_t row0 = r0 + (int64_t)g * kDwS;
+      if (zcoop || lane == 0) tc::mbar_wait(&empty[s], ((g / ST) & 1) ^ 1);
+      if (zcoop) {
+        for (int e = lane; e < kDwS * a.N; e += 32) {
+          const int r = e / a.N, nn = e % a.N;
+          uint8_t* dst = zraw(s) + r * 128 + ((nn * 4) ^ ((r & 3) << 5));
+          if (row0 + r < r1) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(tc::smem_u32(dst)),
+                         "l"(a.Z + (row0 + r) * a.ldz + nn) : "memory");
+          } else {
+            *reinterpret_cast<float*>(dst) = 0.f;
+          }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(tc::smem_u32(&full[s])) : "memory");
+      }
+      if (lane == 0) {
         if (bytes) mbar_expect_tx(&full[s], bytes); else mbar_arrive(&full[s]);
         if (a.tmaZ)
-          for (int b = 0; b < a.nzb; ++b) tma_load_2d(zraw(s) + b * kBox, &tmZ, &full[s], 32 * b, row);
+          for (int b = 0; b < a.nzb; ++b) tma_load_2d(zraw(s) + b * kBox, &tmZ, &full[s], 32 * b, (int)row0);
         if (a.tmaX)
-          for (int b = 0; b < a.nxb; ++b) tma_load_2d(xhi(s) + b * kBox, &tmX, &full[s], 32 * b, row);
+          for (int b = 0; b < a.nxb; ++b) tma_load_2d(xhi(s) + b * kBox, &tmX, &full[s], 32 * b, (int)row0);
       }
     }
   } else if (warp == 1) {
@@ -487,51 +506,55 @@ __global__ void __launch_bounds__(256, 1) k_dw(DwArgs3 a, const __grid_constant_
       tc::mma_commit(&tfull);
     }
   } else if (warp >= 4) {
-    const int ct = tid - 128, quarter = warp & 3;
+    // two converter warpgroups: half h owns samples [16h, 16h + 16) of every chunk (TMEM
+    // columns) and every other X unit; both see all 128 TMEM lanes (warp quarter = lanes)
+    const int t256 = tid - 128, half = t256 >> 7, ct = t256 & 127, quarter = warp & 3;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const bool vx = (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
     const int n = ct;                                         // this thread's TMEM lane = output neuron
+    const bool zcoop = !a.tmaZ && a.N <= 16;          // dZ gathered into zraw by the producer
     for (int g = 0; g < nchunk; ++g) {
       const int s = g % ST;
       const int64_t row0 = r0 + (int64_t)g * kDwS;
       tc::mbar_wait(&full[s], (g / ST) & 1);
-      // dZ^T row n (32 samples) -> hi/lo -> TMEM lane n
-      uint32_t hi[32], lo[32];
-      if (a.tmaZ) {
+      // dZ^T row n, samples [16h, 16h+16) -> hi/lo -> TMEM lane n
+      uint32_t hi[16], lo[16];
+      if (a.tmaZ || zcoop) {
         const uint8_t* zb = zraw(s) + (n >> 5) * kBox;
         const uint32_t nb = (uint32_t)(n & 31) * 4;
 #pragma unroll
-        for (int r = 0; r < kDwS; ++r) {
+        for (int j = 0; j < 16; ++j) {
+          const int r = 16 * half + j;
           const float v = *reinterpret_cast<const float*>(zb + r * 128 + (nb ^ ((r & 3u) << 5)));
           const float h = rna_tf32(v);
-          hi[r] = __float_as_uint(h);
-          lo[r] = __float_as_uint(v - h);
+          hi[j] = __float_as_uint(h);
+          lo[j] = __float_as_uint(v - h);
         }
       } else {
 #pragma unroll
-        for (int r = 0; r < kDwS; ++r) {
-          const int64_t row = row0 + r;
+        for (int j = 0; j < 16; ++j) {
+          const int64_t row = row0 + 16 * half + j;
           const float v = (n < a.N && row < r1) ? __ldg(a.Z + row * a.ldz + n) : 0.f;
           const float h = rna_tf32(v);
-          hi[r] = __float_as_uint(h);
-          lo[r] = __float_as_uint(v - h);
+          hi[j] = __float_as_uint(h);
+          lo[j] = __float_as_uint(v - h);
         }
       }
-      const uint32_t ta = tbase + lane_off + 256 + 64 * s;
-      tc::tmem_st32(ta, hi);
-      tc::tmem_st32(ta + 32, lo);
+      const uint32_t ta = tbase + lane_off + 256 + 64 * s + 16 * half;
+      tc::tmem_st16(ta, hi);
+      tc::tmem_st16(ta + 32, lo);
       // X -> hi (in place) / lo tiles in smem
       float4* h4 = reinterpret_cast<float4*>(xhi(s));
       float4* l4 = reinterpret_cast<float4*>(xlo(s));
       if (a.tmaX) {
-        for (int q = ct; q < a.nxb * (kBox / 16); q += 128) {
+        for (int q = t256; q < a.nxb * (kBox / 16); q += 256) {
           float4 h, l;
           split4(h4[q], h, l);
           h4[q] = h;
           l4[q] = l;
         }
       } else {
-        for (int q = ct; q < a.nxb * (kBox / 16); q += 128) {
+        for (int q = t256; q < a.nxb * (kBox / 16); q += 256) {
           const int b = q / (kBox / 16), r = (q / 8) % kDwS, u = q % 8;
           const int64_t row = row0 + r;
           float4 h, l;
@@ -546,12 +569,13 @@ __global__ void __launch_bounds__(256, 1) k_dw(DwArgs3 a, const __grid_constant_
       tc::fence_proxy_async();
       mbar_arrive(&conv[s]);
     }
-    // epilogue: TMEM lane n = output neuron, column k = input feature (column 32*nxb = db)
+    // epilogue: TMEM lane n = output neuron, column k = input feature (column 32*nxb = db);
+    // half h reads the 16-column blocks 2i + h
     if (nchunk > 0) {
       tc::mbar_wait(&tfull, 0);
       tc::fence_after();
       const uint32_t taddr = tbase + lane_off;
-      for (int c0 = 0; c0 < nprime; c0 += 16) {
+      for (int c0 = 16 * half; c0 < nprime; c0 += 32) {
         float v[16];
         tc::tmem_ld16(taddr + c0, v);
         tc::tmem_ld_wait();
@@ -659,7 +683,7 @@ int32_t dw_gemm(DwArgs3 a, cudaStream_t st) {
   a.stages = std::min(4, (kSmemMax - 1024) / stage_bytes);
   const size_t smem = 1024 + (size_t)a.stages * stage_bytes;
   cudaFuncSetAttribute(k_dw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_dw<<<grid, 256, smem, st>>>(a, tx, tz);
+  k_dw<<<grid, 384, smem, st>>>(a, tx, tz);
   return check_launch("k_dw");
 }
 
