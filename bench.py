@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--skip-cpu-baseline", action="store_true")
     p.add_argument("--no-train", action="store_true", help="skip the config-3 training-step measurement")
     p.add_argument("--train-steps", type=int, default=20)
+    p.add_argument("--no-scene", action="store_true", help="skip the config-5 multi-subject measurement")
     return p.parse_args()
 
 
@@ -268,6 +269,7 @@ def run_ours(args, rank, world, local_rank):
     roof = dict(roofs[dominant])
 
     train = None if args.no_train else train_throughput(args, rank, world, dev)
+    multi = None if args.no_scene else scene_throughput(args, rank, world, dev)
 
     cpu = None
     if rank == 0 and not args.skip_cpu_baseline:
@@ -288,6 +290,7 @@ def run_ours(args, rank, world, local_rank):
                     "d2h_bytes_per_step": d2h, "frames_per_s": world / (e2e_ms / 1000.0)},
             "gpu_launches": launches_per_step * args.steps,
             "train": train,
+            "multi_subject": multi,
             "stages_ms": stages,
             "roofline": roof,
             "stage_rooflines": roofs,
@@ -386,6 +389,75 @@ def train_throughput(args, rank, world, dev):
             "workload": "c3: 6 x 32x32 patches of a 512^2 target, 128 samples/ray, fwd + full bwd + Adam"
                         + (f", NCCL all-reduce over {world} GPUs" if world > 1 else ""),
             "final_loss": float(tr.loss.item())}
+
+
+def scene_throughput(args, rank, world, dev):
+    """Config 5: 4 independently posed subjects (own T=2^19 grids, skeletons, MLPs) in a 4 m
+    scene, one 1024x1024 frame, 192 jittered samples per ray inside each subject box,
+    occupancy per subject pose, depth-ordered joint compositing.  Sharded by image tile:
+    rank r renders the interleaved 4-row tile bands r, r+N, ... (strong scaling; the
+    frame time is the max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2306_16541_b200 import scene as psc
+    from paper_2306_16541_b200 import shard
+    from paper_2306_16541_b200.model import FreeviewModel
+    from paper_2306_16541_b200.render import SceneRenderer, scene_settings
+    ms = psc.make_multi_scene(psc.config("c5"))
+    nets = [FreeviewModel(s, device=str(dev)) for s in ms.subjects]
+    if world > 1:
+        for n in nets:
+            dist.broadcast(n.flat, src=0)
+            n.refresh()
+    cam = ms.camera
+    rows = shard.row_bands_for_rank(rank, world, cam.height) if world > 1 else None
+    r = SceneRenderer(len(nets), str(dev))
+    st = scene_settings(ms)
+    bg = tuple(ms.cfg.background)
+    poses = [s.poses[0] for s in ms.subjects]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(3, args.warmup)):
+        r.render_scene(nets, ms, st, bg, poses=poses, rows=rows)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    steps = max(3, min(args.steps, 10))
+    times = []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        r.render_scene(nets, ms, st, bg, poses=poses, rows=rows)
+        b.record(stream)
+        times.append((a, b))
+    torch.cuda.synchronize()
+    ms_frame = float(np.mean([a.elapsed_time(b) for a, b in times]))
+    # e2e: host poses in, host image + alpha out (pinned) every frame
+    host = torch.empty((cam.height * cam.width, 4), dtype=torch.float32, pin_memory=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        img, alpha = r.render_scene(nets, ms, st, bg, poses=poses, rows=rows)
+        host[:, :3].copy_(img.view(-1, 3), non_blocking=True)
+        host[:, 3].copy_(alpha.view(-1), non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms_frame, e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_frame, e2e_ms = float(t[0]), float(t[1])
+    n_rays = cam.width * cam.height
+    marched = sum(len(r.subject_pix(s, ms.subject_camera(s), st[s], rows)) for s in range(len(nets)))
+    return {"metric": "rays_per_s", "value": n_rays / (ms_frame / 1000.0), "unit": "rays/s",
+            "frames_per_s": 1000.0 / ms_frame, "ms_per_frame": ms_frame, "e2e_frames_per_s": 1000.0 / e2e_ms,
+            "scaling": "strong", "subjects": len(nets), "subject_rays_marched_rank0": marched,
+            "samples_per_ray_per_subject": ms.cfg.n_samples,
+            "workload": "c5: 4 subjects (own T=2^19 grids/skeletons/MLPs) at seeded offsets in a 4 m scene, "
+                        "1024x1024, 192 jittered samples/ray per subject box, occupancy per pose, fp16 tcgen05 "
+                        "MLPs, depth-ordered joint compositing" + (f", tile bands over {world} GPUs" if world > 1 else ""),
+            "l2": "flushed (256 MB write) before every timed frame"}
 
 
 def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5):

@@ -36,6 +36,7 @@ extern "C" {
 #define FV_MAX_BONES 32
 #define FV_MAX_VOL_RES 128
 #define FV_MAX_LEVELS 16
+#define FV_MAX_SUBJECTS 8
 
 /* ---- parameter blocks (plain data, host memory) ----------------------------------- */
 
@@ -71,6 +72,17 @@ typedef struct fv_warp {
   float wscale[3];                /* float32((G-1)/(wbox_max-wbox_min))  (ad:746)      */
 } fv_warp;
 
+/* Multi-subject scene (BASELINE config 5; builder-defined, parity unpinned): per-subject
+ * renders over disjoint boxes merged front to back in entry-depth order. */
+typedef struct fv_scene_merge {
+  int32_t n_subjects;                      /* 1..FV_MAX_SUBJECTS                         */
+  fv_camera cam[FV_MAX_SUBJECTS];          /* subject-local cameras (world cam - offset) */
+  float box_min[3], box_max[3];            /* subject box in subject-local coordinates   */
+  const float* d_rgb[FV_MAX_SUBJECTS];     /* [n_pix][3] premultiplied, background 0     */
+  const float* d_alpha[FV_MAX_SUBJECTS];   /* [n_pix]                                    */
+  float bg[3];                             /* scene background                           */
+} fv_scene_merge;
+
 typedef struct fv_hash {
   int32_t n_levels, n_feat, log2_T;
   int32_t res[FV_MAX_LEVELS];
@@ -98,7 +110,7 @@ typedef struct fv_field {
 int32_t fv_version(void);                       /* ABI version (100 = 1.0)            */
 const char* fv_last_error(void);                /* thread-local message of last error */
 int32_t fv_device_sm(void);                     /* SM count of the current device     */
-/* sizeof of the 5 parameter structs (camera, march, warp, hash, field) -> out[5];
+/* sizeof of the 6 parameter structs (camera, march, warp, hash, field, scene_merge) -> out[6];
  * lets a binding verify its struct layout without a GPU. */
 void fv_struct_sizes(int64_t* out);
 
@@ -241,6 +253,13 @@ int32_t fv_render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp
                       const fv_hash* hash, const fv_field* field, int64_t n_rays,
                       void* d_work, size_t work_bytes, float* d_rgb, float* d_alpha,
                       int32_t* d_count, void* stream);
+
+/* Joint compositing of per-subject renders for pixel ids pix0 .. pix0+n_pix-1 (subject and
+ * output buffers image-sized, indexed by pixel id):
+ * rgb = sum_s (prod_{j before s} T_j) C_s + (prod T) bg, alpha = 1 - prod T, subjects ordered
+ * by ray entry depth (same float32 slab as fv_march_warp). */
+int32_t fv_scene_composite(const fv_scene_merge* m, int64_t pix0, int64_t n_pix, float* d_rgb,
+                           float* d_alpha, void* stream);
 
 /* fv_render_fwd with CUDA events between its stages (measurement): synchronises, writes
  * stage_ms[5] = {march+warp+compaction, residual MLP, hash+radiance, compositor, total}

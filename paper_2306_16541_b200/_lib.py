@@ -34,6 +34,14 @@ class FvMarch(C.Structure):
                 ("out_by_pixel", C.c_int32)]
 
 
+MAX_SUBJECTS = 8
+
+
+class FvSceneMerge(C.Structure):
+    _fields_ = [("n_subjects", C.c_int32), ("cam", FvCamera * MAX_SUBJECTS), ("box_min", f3), ("box_max", f3),
+                ("d_rgb", vp * MAX_SUBJECTS), ("d_alpha", vp * MAX_SUBJECTS), ("bg", f3)]
+
+
 class FvWarp(C.Structure):
     _fields_ = [("n_bones", C.c_int32), ("vol_res", C.c_int32), ("vol_half", C.c_int32),
                 ("d_vol_packed", vp), ("d_g", vp), ("wbox_min", f3), ("wscale", f3)]
@@ -52,7 +60,7 @@ class FvField(C.Structure):
                 ("d_rad_w", vp * 3), ("d_rad_b", vp * 3), ("d_off_b0_eff", vp), ("d_tc_pack", vp)]
 
 
-STRUCTS = (FvCamera, FvMarch, FvWarp, FvHash, FvField)
+STRUCTS = (FvCamera, FvMarch, FvWarp, FvHash, FvField, FvSceneMerge)
 
 P = C.POINTER
 i32, i64, f32, sz = C.c_int32, C.c_int64, C.c_float, C.c_size_t
@@ -92,6 +100,7 @@ SIGNATURES = {
     "fv_mse_loss": (i32, [vp, vp, vp, i64, vp, vp, vp]),
     "fv_render_workspace_bytes": (sz, [i64, i32, i32]),
     "fv_march_warp": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), i64, vp, vp, vp, vp, vp]),
+    "fv_scene_composite": (i32, [P(FvSceneMerge), i64, i64, vp, vp, vp]),
     "fv_render_fwd": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), P(FvHash), P(FvField), i64, vp, sz,
                             vp, vp, vp, vp]),
     "fv_render_fwd_timed": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), P(FvHash), P(FvField), i64, vp, sz,
@@ -116,7 +125,7 @@ def load() -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        sizes = (C.c_int64 * 5)()
+        sizes = (C.c_int64 * len(STRUCTS))()
         lib.fv_struct_sizes(sizes)
         want = [C.sizeof(s) for s in STRUCTS]
         if list(sizes) != want:

@@ -36,6 +36,15 @@ class CameraModel:
     def center(self) -> np.ndarray:
         return -self.rotation.T @ self.world_to_camera[:3, 3]
 
+    def translated(self, offset) -> "CameraModel":
+        """The same camera seen from a frame whose origin sits at world point ``offset``
+        (a subject placed at ``offset``, config 5): x_local = x_world - offset, so the centre
+        moves by -offset and t = R offset is added to the translation; depths along a ray
+        are unchanged."""
+        w2c = self.world_to_camera.copy()
+        w2c[:3, 3] = w2c[:3, 3] + self.rotation @ np.asarray(offset, dtype=np.float64)
+        return CameraModel(self.intrinsics.copy(), w2c, self.width, self.height)
+
     def kernel_consts(self):
         """float32 (K^-1, R, centre) exactly as fv_camera carries them."""
         return (np.linalg.inv(self.intrinsics).astype(np.float32), self.rotation.astype(np.float32),

@@ -108,7 +108,7 @@ extern "C" int32_t fv_version(void) { return 100; }
 extern "C" const char* fv_last_error(void) { return g_err; }
 extern "C" void fv_struct_sizes(int64_t* out) {
   out[0] = sizeof(fv_camera); out[1] = sizeof(fv_march); out[2] = sizeof(fv_warp);
-  out[3] = sizeof(fv_hash); out[4] = sizeof(fv_field);
+  out[3] = sizeof(fv_hash); out[4] = sizeof(fv_field); out[5] = sizeof(fv_scene_merge);
 }
 extern "C" int32_t fv_device_sm(void) {
   int dev = 0, n = 0;

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
-from typing import Optional, Tuple
+from typing import List, Optional, Tuple
 
 import numpy as np
 import torch
@@ -224,3 +224,121 @@ def composite(sigma: torch.Tensor, color: torch.Tensor, delta: torch.Tensor, lik
                                     likelihood.float().contiguous().data_ptr(), 1, 0, r, n, bg, eps_w, eps_t,
                                     rgb.data_ptr(), alpha.data_ptr(), None, _lib.stream_ptr()), "fv_composite_fwd")
     return rgb, alpha
+
+
+# ----------------------------------------------------------------------- config 5: scenes
+
+def subject_pixels(cam: CameraModel, box_min, box_max, rows=None) -> np.ndarray:
+    """Pixel ids (8x4-tiled order) of every tile that the projection of the box touches,
+    optionally restricted to the image row bands ``rows`` ([(r0, r1), ...]): a superset of the pixels whose ray hits
+    the box, so a subject is only marched where it can be seen.  All pixels if a box
+    corner is behind the camera."""
+    w, h = cam.width, cam.height
+    corners = np.array([[x, y, z] for x in (box_min[0], box_max[0]) for y in (box_min[1], box_max[1])
+                        for z in (box_min[2], box_max[2])], np.float64)
+    pc = corners @ cam.rotation.T + cam.world_to_camera[:3, 3]
+    order = tiled_pixel_order(w, h)
+    if np.any(pc[:, 2] <= 1e-6):
+        sel = order
+    else:
+        uv = pc @ cam.intrinsics.T
+        u, v = uv[:, 0] / uv[:, 2], uv[:, 1] / uv[:, 2]
+        x0, x1 = int(np.floor(u.min())) - 1, int(np.ceil(u.max())) + 1
+        y0, y1 = int(np.floor(v.min())) - 1, int(np.ceil(v.max())) + 1
+        if w % 8 == 0 and h % 4 == 0:     # whole 8x4 tiles (32-ray blocks stay spatially coherent)
+            x0, x1 = x0 // 8 * 8, (x1 + 8) // 8 * 8
+            y0, y1 = y0 // 4 * 4, (y1 + 4) // 4 * 4
+        px, py = order % w, order // w
+        sel = order[(px >= x0) & (px < x1) & (py >= y0) & (py < y1)]
+    if rows is not None:
+        py = sel // w
+        keep = np.zeros(len(sel), bool)
+        for r0, r1 in rows:
+            keep |= (py >= r0) & (py < r1)
+        sel = sel[keep]
+    return np.ascontiguousarray(sel, dtype=np.int32)
+
+
+class SceneRenderer:
+    """Config 5: every subject through the single-subject path (its own pose, occupancy
+    grid and jitter seed, camera shifted into its frame, background 0) over the pixels its
+    box can cover, then ``fv_scene_composite`` merges them front to back."""
+
+    def __init__(self, n_subjects: int, device: str = "cuda"):
+        if n_subjects < 1 or n_subjects > _lib.MAX_SUBJECTS:
+            raise DimensionError(f"1..{_lib.MAX_SUBJECTS} subjects")
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        self.renderers = [Renderer(device) for _ in range(n_subjects)]
+        shared = self.renderers[0]
+        for r in self.renderers[1:]:
+            r.workspace = shared.workspace          # one workspace, subjects render in turn
+        self._pix = {}
+        self._bufs = None
+
+    def _buffers(self, n_pix):
+        if self._bufs is None or self._bufs[1].shape[1] != n_pix:
+            s = len(self.renderers)
+            self._bufs = (torch.zeros((s, n_pix, 3), dtype=torch.float32, device=self.device),
+                          torch.zeros((s, n_pix), dtype=torch.float32, device=self.device))
+        return self._bufs
+
+    def subject_pix(self, s: int, cam: CameraModel, settings: RenderSettings, rows=None) -> torch.Tensor:
+        key = (s, cam.world_to_camera.tobytes(), cam.width, cam.height, settings.box_min, settings.box_max, rows)
+        if key not in self._pix:
+            self._pix[key] = torch.from_numpy(subject_pixels(cam, settings.box_min, settings.box_max, rows)).to(self.device)
+        return self._pix[key]
+
+    def render_scene(self, subject_nets, scene, settings: List[RenderSettings], background, poses=None,
+                     rows=None, out_rgb=None, out_alpha=None, stream=None):
+        """(image (H,W,3), alpha (H,W)); with ``rows`` = [(r0, r1), ...] only those image row
+        bands are produced (tile sharding across ranks; other rows are left undefined).
+        ``settings[s]`` must carry background 0."""
+        if rows is not None:
+            rows = tuple((int(a), int(b)) for a, b in rows)
+        cam = scene.camera
+        n_pix = cam.width * cam.height
+        rgb_s, alpha_s = self._buffers(n_pix)
+        if out_rgb is None:
+            out_rgb = torch.empty((n_pix, 3), dtype=torch.float32, device=self.device)
+        if out_alpha is None:
+            out_alpha = torch.empty(n_pix, dtype=torch.float32, device=self.device)
+        m = _lib.FvSceneMerge()
+        m.n_subjects = len(subject_nets)
+        for s, (nets, st) in enumerate(zip(subject_nets, settings)):
+            if any(b != 0.0 for b in st.background):
+                raise DimensionError("subject settings must use background 0 (the scene background is merged once)")
+            r = self.renderers[s]
+            cam_s = scene.subject_camera(s)
+            if poses is not None:
+                nets.set_pose(poses[s], stream)
+            occ = r.build_occupancy(nets, st, stream) if st.occupancy else None
+            pix = self.subject_pix(s, cam_s, st, rows)
+            if pix.numel():
+                r.render_pixels(nets, cam_s, pix, st, rgb_s[s], alpha_s[s], by_pixel=True, occ=occ, stream=stream)
+            m.cam[s] = camera_struct(cam_s)
+            m.d_rgb[s] = rgb_s[s].data_ptr()
+            m.d_alpha[s] = alpha_s[s].data_ptr()
+        _lib.farr(m.box_min, np.asarray(settings[0].box_min, np.float32))
+        _lib.farr(m.box_max, np.asarray(settings[0].box_max, np.float32))
+        _lib.farr(m.bg, background)
+        p0, p1 = (0, n_pix) if rows is None else (min(a for a, _ in rows) * cam.width, max(b for _, b in rows) * cam.width)
+        _lib.check(self.lib.fv_scene_composite(C.byref(m), p0, p1 - p0, out_rgb.data_ptr(), out_alpha.data_ptr(),
+                                               _lib.stream_ptr(stream)), "fv_scene_composite")
+        return out_rgb.view(cam.height, cam.width, 3), out_alpha.view(cam.height, cam.width)
+
+
+def scene_settings(scene, **kw) -> List[RenderSettings]:
+    """Per-subject render settings of a MultiScene: config samples/jitter/occupancy, the
+    subject's own jitter seed, background 0."""
+    return [RenderSettings.from_config(scene.cfg, seed=sub.jitter_seed, background=(0.0, 0.0, 0.0), **kw)
+            for sub in scene.subjects]
+
+
+def render_scene(subject_nets, scene, poses=None, settings: Optional[List[RenderSettings]] = None):
+    """Config 5 public entry: joint image of all subjects over the scene background."""
+    key = ("scene", str(subject_nets[0].device), len(subject_nets))
+    if key not in _DEFAULT:
+        _DEFAULT[key] = SceneRenderer(len(subject_nets), subject_nets[0].device)
+    st = settings if settings is not None else scene_settings(scene)
+    return _DEFAULT[key].render_scene(subject_nets, scene, st, tuple(scene.cfg.background), poses)

@@ -12,6 +12,10 @@ table / weight volume / tensor-core MLPs with fp32 accumulation, 32^3 occupancy 
 Config 3 ("c3"): config-2 model trained on 6 random 32x32 patches of a seeded smooth
 512x512 target (foreground = projected body-box ellipsoid), fp16 grid with fp32 master.
 Config 4 ("c4"): 8 poses ~N(0, 0.3), otherwise config 2.
+Config 5 ("c5"): 4 independently posed subjects (own seeded skeleton, pose, weight volume,
+MLPs and T = 2^19 hash table each) at seeded offsets in a shared 4 m scene, 1024x1024,
+192 jittered samples per ray inside each subject's box, depth-ordered joint compositing
+over a constant background (``make_multi_scene``; builder-defined, SS3).
 
 Every tensor comes from its own child of ``np.random.SeedSequence(seed)``.
 """
@@ -99,6 +103,9 @@ CONFIGS = {
     "c4": SceneConfig(name="c4", width=512, height=512, n_samples=128, jitter=True,
                       hash=HashGridConfig(log2_T=19, max_res=2048), half=True, occupancy=True,
                       pose_sigma=0.3, n_poses=8),
+    "c5": SceneConfig(name="c5", width=1024, height=1024, n_samples=192, jitter=True,
+                      hash=HashGridConfig(log2_T=19, max_res=2048), half=True, occupancy=True,
+                      radius=8.0, background=(0.2, 0.2, 0.2)),
 }
 
 
@@ -196,3 +203,42 @@ def target_image(scene: Scene, seed: int = 7):
     mask = b * b - 4 * a * cc > 0
     out = np.where(mask[..., None], np.clip(img, 0, 1), np.asarray(cfg.background)[None, None, :])
     return out.astype(np.float32), mask
+
+
+@dataclass
+class MultiScene:
+    """Config 5: subjects (each a full single-subject Scene in its own frame) placed at
+    world offsets; ``camera`` is the world camera, subject s is rendered through
+    ``camera.translated(offsets[s])``."""
+    cfg: SceneConfig
+    subjects: List[Scene]
+    offsets: np.ndarray             # (S, 3) world position of each subject frame's origin
+    camera: CameraModel
+
+    def subject_camera(self, s: int) -> CameraModel:
+        return self.camera.translated(self.offsets[s])
+
+
+def place_subjects(rng, n: int, extent: float, box: float = 2.0, margin: float = 0.05,
+                   tries: int = 10000) -> np.ndarray:
+    """Seeded subject positions on the ground plane (y = 0): x, z ~ U(-extent/2, extent/2),
+    rejection-sampled until every pair of boxes is separated along x or z by >= box + margin,
+    i.e. the boxes are disjoint (what makes the depth-ordered merge exact)."""
+    half = extent / 2.0
+    for _ in range(tries):
+        xz = rng.uniform(-half, half, (n, 2))
+        ok = all(max(abs(xz[i, 0] - xz[j, 0]), abs(xz[i, 1] - xz[j, 1])) >= box + margin
+                 for i in range(n) for j in range(i))
+        if ok:
+            return np.stack([xz[:, 0], np.zeros(n), xz[:, 1]], 1)
+    raise ValueError(f"could not place {n} disjoint {box} m boxes in a {extent} m square")
+
+
+def make_multi_scene(cfg: SceneConfig, n_subjects: int = 4, extent: float = 4.0, pitch_deg: float = 20.0) -> MultiScene:
+    """Config 5 stand-in: every subject from its own child seed (its own hash table,
+    skeleton, pose, weight volume and MLPs), positions from another child."""
+    ch = np.random.SeedSequence(cfg.seed).spawn(n_subjects + 1)
+    subjects = [make_scene(replace(cfg, seed=int(c.generate_state(1)[0]))) for c in ch[:n_subjects]]
+    offsets = place_subjects(np.random.default_rng(ch[n_subjects]), n_subjects, extent)
+    cam = orbit_camera((0.0, 0.0, 0.0), 0.0, pitch_deg, cfg.radius, cfg.fov_deg, cfg.width, cfg.height)
+    return MultiScene(cfg=cfg, subjects=subjects, offsets=offsets, camera=cam)

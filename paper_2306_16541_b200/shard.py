@@ -30,6 +30,13 @@ def tiles_for_rank(rank: int, world: int, n_tiles: int) -> List[int]:
     return list(range(rank, n_tiles, world))
 
 
+def row_bands_for_rank(rank: int, world: int, height: int, band: int = 4):
+    """Image-tile sharding for config 5: interleaved bands of ``band`` rows (one 8x4 tile
+    row each), rank r taking bands r, r + world, ... (subject coverage is uneven, the
+    interleave balances it)."""
+    return [(y, min(y + band, height)) for y in range(band * rank, height, band * world)]
+
+
 def broadcast_params(flat: torch.Tensor, src: int = 0, group=None) -> None:
     """Identical weights on every rank: one broadcast of the flat master buffer."""
     import torch.distributed as dist

@@ -30,7 +30,7 @@ def test_binding_covers_header():
 def test_struct_layout_and_version_without_gpu():
     lib = _lib.load()  # checks ctypes struct sizes against sizeof() in C
     assert lib.fv_version() == 100
-    sizes = (ctypes.c_int64 * 5)()
+    sizes = (ctypes.c_int64 * len(_lib.STRUCTS))()
     lib.fv_struct_sizes(sizes)
     assert all(s > 0 for s in sizes)
 
