@@ -105,3 +105,13 @@ def test_frame_schedule_covers_each_frame_once_per_round(world):
     assert seen == list(range(n))
     tiles = sorted(t for r in range(world) for t in shard.tiles_for_rank(r, world, 64))
     assert tiles == list(range(64))
+
+
+@pytest.mark.parametrize("world,height", [(1, 64), (2, 1024), (3, 64), (8, 1024), (8, 20)])
+def test_row_bands_partition_the_image(world, height):
+    from paper_2306_16541_b200.shard import row_bands_for_rank
+    rows = np.zeros(height, int)
+    for r in range(world):
+        for a, b in row_bands_for_rank(r, world, height):
+            rows[a:b] += 1
+    assert np.all(rows == 1)
