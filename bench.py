@@ -388,7 +388,7 @@ def train_throughput(args, rank, world, dev):
             "samples_per_iter_per_gpu": tr.S, "n_params": nets.n_params,
             "workload": "c3: 6 x 32x32 patches of a 512^2 target, 128 samples/ray, fwd + full bwd + Adam"
                         + (f", NCCL all-reduce over {world} GPUs" if world > 1 else ""),
-            "final_loss": float(tr.loss.item())}
+            "final_loss": float(tr.loss[0].item())}
 
 
 def scene_throughput(args, rank, world, dev):

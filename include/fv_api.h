@@ -230,6 +230,13 @@ int32_t fv_softmax0_fwd(const float* d_a, int32_t channels, int64_t voxels, floa
                         void* stream);
 int32_t fv_softmax0_bwd(const float* d_out, const float* d_g, int32_t channels, int64_t voxels,
                         float* d_da, void* stream);
+/* SPEC compute_loss on patches: rgb rows are G patches of size x size pixels,
+ * each row-major; target gathered by d_pix.  loss[0..2] = (lam_mse*MSE + lam_perc*GD, MSE,
+ * GD) with GD the multi-scale gradient-difference proxy of the perceptual term;
+ * d_drgb = d loss[0] / d rgb. */
+int32_t fv_patch_loss(const float* d_rgb, const float* d_target, const int32_t* d_pix, int32_t n_patches,
+                      int32_t size, float lam_mse, float lam_perc, float* d_loss, float* d_drgb,
+                      void* stream);
 /* L2 loss over rays (target gathered at pixel ids, or row r when d_pix is NULL):
  * *d_loss = mean((rgb - t)^2) (device scalar), d_drgb = its gradient. */
 int32_t fv_mse_loss(const float* d_rgb, const float* d_target, const int32_t* d_pix,

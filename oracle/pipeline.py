@@ -83,17 +83,26 @@ def render_rays(scene, cc, pix, width, settings, dtype=np.float32):
             "lik": lik.reshape(-1, n), "rgb": res["rgb"], "alpha": res["alpha"], "comp": res}
 
 
-def loss_and_grads(scene, cc, pix, width, settings, target, dtype=np.float32):
-    """MSE loss over the rays and float64 gradients of every trainable block.
+def loss_and_grads(scene, cc, pix, width, settings, target, dtype=np.float32, patch=None):
+    """MSE loss over the rays (or, with ``patch = (size, lam_mse, lam_perc)`` and patch-major
+    rays, the SPEC patch loss ``oracle.loss.patch_loss``) and float64 gradients of
+    every trainable block.
 
     Blocks: ``table``; ``off_w[i]``/``off_b[i]``; ``rad_w[i]``/``rad_b[i]``; ``vol`` (the
     softmaxed weight volume; chain into logits with ``warp.softmax0_bwd``).
     """
     r = render_rays(scene, cc, pix, width, settings, dtype)
     rgb = r["rgb"].astype(np.float64)
-    diff = rgb - np.asarray(target, np.float64)
-    loss = float(np.mean(diff * diff))
-    d_rgb = 2.0 * diff / diff.size
+    if patch is None:
+        diff = rgb - np.asarray(target, np.float64)
+        loss = float(np.mean(diff * diff))
+        d_rgb = 2.0 * diff / diff.size
+    else:
+        from . import loss as oloss
+        size, lam_mse, lam_perc = patch
+        shp = (-1, size, size, 3)
+        loss, _, _, g = oloss.patch_loss(rgb.reshape(shp), np.asarray(target, np.float64).reshape(shp), lam_mse, lam_perc)
+        d_rgb = g.reshape(-1, 3)
     d_alpha = np.zeros(len(rgb))
     n = settings["n_samples"]
     d_sigma, d_color = comp.composite_bwd(r["comp"], r["sigma"], r["color"], r["delta"], r["lik"],

@@ -100,6 +100,7 @@ SIGNATURES = {
     "fv_mse_loss": (i32, [vp, vp, vp, i64, vp, vp, vp]),
     "fv_render_workspace_bytes": (sz, [i64, i32, i32]),
     "fv_march_warp": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), i64, vp, vp, vp, vp, vp]),
+    "fv_patch_loss": (i32, [vp, vp, vp, i32, i32, f32, f32, vp, vp, vp]),
     "fv_scene_composite": (i32, [P(FvSceneMerge), i64, i64, vp, vp, vp]),
     "fv_render_fwd": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), P(FvHash), P(FvField), i64, vp, sz,
                             vp, vp, vp, vp]),

@@ -202,6 +202,100 @@ extern "C" int32_t fv_softmax0_bwd(const float* d_out, const float* d_g, int32_t
   return check_launch("fv_softmax0_bwd");
 }
 
+// SPEC compute_loss on S x S patches: lam_mse * mean((r - t)^2) + lam_perc *
+// multi-scale gradient difference (sum over scales 1, 2 of mean |d_x e| + mean |d_y e|,
+// e = r - t, scale 2 = 2x2 average pooling; oracle/loss.py restates the reference ops
+// diff_axis ad:844, avgpool2 ad:862, absval ad:243).  One CTA per patch; e and its pooled
+// copy in shared memory; loss[0..2] = (total, mse, perc) accumulated with atomics.
+__device__ __forceinline__ float sgnf(float d) { return (float)((d > 0.f) - (d < 0.f)); }
+
+__global__ void k_patch_loss(const float* __restrict__ rgb, const float* __restrict__ target,
+                             const int32_t* __restrict__ pix, int S, float lam_mse, float lam_perc, float inv_mse,
+                             float inv_d1, float inv_d2, float* __restrict__ loss, float* __restrict__ drgb) {
+  extern __shared__ float sh[];
+  float* e = sh;                       // [S][S][3]
+  float* e2 = sh + S * S * 3;          // [S/2][S/2][3]
+  __shared__ float red[3][32];
+  const int S2 = S / 2;
+  const int64_t base = (int64_t)blockIdx.x * S * S;
+  for (int i = threadIdx.x; i < S * S * 3; i += blockDim.x) {
+    const int64_t r = base + i / 3;
+    const int64_t q = pix ? pix[r] : r;
+    e[i] = rgb[3 * r + i % 3] - target[3 * q + i % 3];
+  }
+  __syncthreads();
+  if (lam_perc != 0.f) {
+    for (int i = threadIdx.x; i < S2 * S2 * 3; i += blockDim.x) {
+      const int c = i % 3, X = (i / 3) % S2, Y = i / 3 / S2;
+      const float* p = e + ((2 * Y) * S + 2 * X) * 3 + c;
+      e2[i] = 0.25f * ((p[0] + p[3]) + (p[3 * S] + p[3 * S + 3]));
+    }
+    __syncthreads();
+  }
+  float sq = 0.f, d1 = 0.f, d2 = 0.f;
+  for (int i = threadIdx.x; i < S * S * 3; i += blockDim.x) {
+    const int c = i % 3, x = (i / 3) % S, y = i / 3 / S;
+    const float v = e[i];
+    sq += v * v;
+    float g = lam_mse * 2.f * v * inv_mse;
+    if (lam_perc != 0.f) {
+      float gp = 0.f;
+      if (x + 1 < S) { const float d = e[i + 3] - v; d1 += fabsf(d); gp -= sgnf(d); }
+      if (x > 0) gp += sgnf(v - e[i - 3]);
+      if (y + 1 < S) { const float d = e[i + 3 * S] - v; d1 += fabsf(d); gp -= sgnf(d); }
+      if (y > 0) gp += sgnf(v - e[i - 3 * S]);
+      const int X = x >> 1, Y = y >> 1, j = (Y * S2 + X) * 3 + c;
+      const float v2 = e2[j];
+      float gq = 0.f;
+      if (X + 1 < S2) gq -= sgnf(e2[j + 3] - v2);
+      if (X > 0) gq += sgnf(v2 - e2[j - 3]);
+      if (Y + 1 < S2) gq -= sgnf(e2[j + 3 * S2] - v2);
+      if (Y > 0) gq += sgnf(v2 - e2[j - 3 * S2]);
+      if ((x & 1) == 0 && (y & 1) == 0) {     // each pooled pixel's own differences once
+        if (X + 1 < S2) d2 += fabsf(e2[j + 3] - v2);
+        if (Y + 1 < S2) d2 += fabsf(e2[j + 3 * S2] - v2);
+      }
+      g += lam_perc * (gp * inv_d1 + 0.25f * gq * inv_d2);
+    }
+    drgb[3 * (base + i / 3) + c] = g;
+  }
+  for (int o = 16; o; o >>= 1) {
+    sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+    d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = sq; red[1][threadIdx.x >> 5] = d1; red[2][threadIdx.x >> 5] = d2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = 0.f, b = 0.f, c = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += red[0][w]; b += red[1][w]; c += red[2][w]; }
+    const float mse = a * inv_mse, perc = b * inv_d1 + c * inv_d2;
+    atomicAdd(loss + 1, mse);
+    atomicAdd(loss + 2, perc);
+    atomicAdd(loss, lam_mse * mse + lam_perc * perc);
+  }
+}
+
+extern "C" int32_t fv_patch_loss(const float* d_rgb, const float* d_target, const int32_t* d_pix, int32_t n_patches,
+                                 int32_t size, float lam_mse, float lam_perc, float* d_loss, float* d_drgb,
+                                 void* stream) {
+  if (n_patches < 0 || size < 2 || size > 64 || (lam_perc != 0.f && size % 2))
+    return set_error(FV_EDIM, "fv_patch_loss: patches must be 2..64 pixels (even for the perceptual term)");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(d_loss, 0, 3 * sizeof(float), st);
+  if (n_patches == 0) return FV_OK;
+  const double n_el = 3.0 * n_patches * size * size;
+  // mean |d| over both axes at one scale: 2 * G * S * (S - 1) * 3 differences, halved per axis mean
+  const float inv_mse = (float)(1.0 / n_el);
+  const float inv_d1 = (float)(1.0 / (3.0 * n_patches * size * (size - 1)));
+  const int s2 = size / 2;
+  const float inv_d2 = s2 > 1 ? (float)(1.0 / (3.0 * n_patches * s2 * (s2 - 1))) : 0.f;
+  const size_t smem = (size_t)(size * size * 3 + s2 * s2 * 3) * sizeof(float);
+  k_patch_loss<<<n_patches, 256, smem, st>>>(d_rgb, d_target, d_pix, size, lam_mse, lam_perc, inv_mse, inv_d1,
+                                             inv_d2, d_loss, d_drgb);
+  return check_launch("fv_patch_loss");
+}
+
 extern "C" int32_t fv_mse_loss(const float* d_rgb, const float* d_target, const int32_t* d_pix, int64_t n_rays,
                                float* d_loss, float* d_drgb, void* stream) {
   if (n_rays < 0) return set_error(FV_EDIM, "fv_mse_loss: n < 0");

@@ -17,8 +17,13 @@ buffer is all-reduced (mean) between backward and Adam -- the only exchange of t
 
 from __future__ import annotations
 
+import csv
 import ctypes as C
-from typing import Optional
+import json
+import os
+import time
+from dataclasses import dataclass
+from typing import List, Optional
 
 import numpy as np
 import torch
@@ -61,7 +66,7 @@ class Trainer:
 
     def __init__(self, nets: FreeviewModel, camera: CameraModel, target: np.ndarray, mask: np.ndarray,
                  settings: RenderSettings, n_patches: int = 6, patch: int = 32, seed: int = 0,
-                 process_group=None, precision: str = "tf32"):
+                 process_group=None, precision: str = "tf32", lam_mse: float = 1.0, lam_perc: float = 0.0):
         if precision not in ("tf32", "fp32"):
             raise ValueError("precision must be 'tf32' (tcgen05 kind::tf32 layers) or 'fp32' (SIMT, strict parity)")
         self.tc = precision == "tf32"
@@ -100,7 +105,10 @@ class Trainer:
         self.rgb = torch.empty((self.R, 3), **f32)
         self.alpha = torch.empty(self.R, **f32)
         self.trans = torch.empty((self.R, self.N + 1), **f32)
-        self.loss = torch.zeros(1, **f32)
+        self.loss = torch.zeros(3, **f32)      # (total, mse term, perceptual-proxy term)
+        self.lam_mse, self.lam_perc = float(lam_mse), float(lam_perc)
+        if self.lam_perc != 0.0 and patch % 2:
+            raise ValueError("the perceptual proxy needs an even patch size (2x2 pooling, ad:862-866)")
         self.drgb = torch.empty((self.R, 3), **f32)
         self.d_rgbs = torch.empty((S, 4), **f32)
         self.dh = torch.empty((S, 4), **f32)
@@ -123,8 +131,17 @@ class Trainer:
         self.seg_end = (C.c_int64 * 2)(*[int(e) for e, _ in nets.segments])
         self.seg_lr = (C.c_float * 2)(*[float(lr) for _, lr in nets.segments])
         self.pe_w = (C.c_float * 8)(*hann_band_weights(PE_BANDS, nets.pe_alpha).tolist())
+        self.residual = bool(nets.offset_enabled)
         self.bg = (C.c_float * 3)(*settings.background)
         self.table_elems = nets.views["table"].numel()
+
+    def set_schedule(self, alpha: float, residual: bool) -> None:
+        """Coarse-to-fine state of one iteration: Hann window alpha of the
+        positional encoding and whether the residual stage runs (off => x_res exactly 0 and
+        no residual-MLP gradient)."""
+        self.nets.set_schedule(alpha=alpha, residual=residual)
+        self.pe_w = (C.c_float * 8)(*hann_band_weights(PE_BANDS, self.nets.pe_alpha).tolist())
+        self.residual = bool(residual)
 
     # ------------------------------------------------------------------------------------
     def _lin(self, x, w, b, y, k, n, act, sp, bits=None):
@@ -165,13 +182,15 @@ class Trainer:
         _lib.check(lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), self.R, self.xs.data_ptr(),
                                      self.delta.data_ptr(), self.x.data_ptr(), None, sp), "fv_march_warp")
         V = nets.views
-        _lib.check(lib.fv_posenc_fwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.pe.data_ptr(), self.pe_ld,
-                                     sp))
-        self._lin(self.pe, V["off_w0"], nets.b0_eff, self.h[0], self.d_pe, 128, 1, sp, self.hbits[0])
-        for i in range(1, 4):
-            self._lin(self.h[i - 1], V[f"off_w{i}"], V[f"off_b{i}"], self.h[i], 128, 128, 1, sp, self.hbits[i])
-        self._lin(self.h[3], V["off_w4"], V["off_b4"], self.xres, 128, 3, 0, sp)
-        _lib.check(lib.fv_xfinal(self.xs.data_ptr(), self.xres.data_ptr(), S, eps, self.xf.data_ptr(), sp))
+        if self.residual:
+            _lib.check(lib.fv_posenc_fwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.pe.data_ptr(),
+                                         self.pe_ld, sp))
+            self._lin(self.pe, V["off_w0"], nets.b0_eff, self.h[0], self.d_pe, 128, 1, sp, self.hbits[0])
+            for i in range(1, 4):
+                self._lin(self.h[i - 1], V[f"off_w{i}"], V[f"off_b{i}"], self.h[i], 128, 128, 1, sp, self.hbits[i])
+            self._lin(self.h[3], V["off_w4"], V["off_b4"], self.xres, 128, 3, 0, sp)
+        _lib.check(lib.fv_xfinal(self.xs.data_ptr(), self.xres.data_ptr() if self.residual else None, S, eps,
+                                 self.xf.data_ptr(), sp))
         _lib.check(lib.fv_hash_fwd(C.byref(h), self.xf.data_ptr(), S, self.feat.data_ptr(), None, sp), "fv_hash_fwd")
         self._lin(self.feat, V["rad_w0"], V["rad_b0"], self.r[0], 32, 64, 1, sp, self.rbits[0])
         self._lin(self.r[0], V["rad_w1"], V["rad_b1"], self.r[1], 64, 64, 1, sp, self.rbits[1])
@@ -180,9 +199,14 @@ class Trainer:
         _lib.check(lib.fv_composite_fwd(self.rgbs.data_ptr(), self.delta.data_ptr(), self.xs[:, 3:].data_ptr(), 4, 1,
                                         self.R, self.N, self.bg, eps, 0.0, self.rgb.data_ptr(), self.alpha.data_ptr(),
                                         self.trans.data_ptr(), sp), "fv_composite_fwd")
-        _lib.check(lib.fv_mse_loss(self.rgb.data_ptr(), self.target.data_ptr(), self.pix.data_ptr(), self.R,
-                                   self.loss.data_ptr(), self.drgb.data_ptr(), sp), "fv_mse_loss")
-        return self.loss
+        if self.lam_perc == 0.0 and self.lam_mse == 1.0:   # config 3: plain L2
+            _lib.check(lib.fv_mse_loss(self.rgb.data_ptr(), self.target.data_ptr(), self.pix.data_ptr(), self.R,
+                                       self.loss.data_ptr(), self.drgb.data_ptr(), sp), "fv_mse_loss")
+        else:                                                # SPEC compute_loss
+            _lib.check(lib.fv_patch_loss(self.rgb.data_ptr(), self.target.data_ptr(), self.pix.data_ptr(),
+                                         self.n_patches, self.patch, self.lam_mse, self.lam_perc,
+                                         self.loss.data_ptr(), self.drgb.data_ptr(), sp), "fv_patch_loss")
+        return self.loss[0]
 
     def backward(self):
         nets, lib, S, V, G = self.nets, self.lib, self.S, self.nets.views, self.gviews
@@ -196,33 +220,38 @@ class Trainer:
         _lib.check(lib.fv_heads_bwd(self.xs.data_ptr(), self.hd.data_ptr(), self.d_rgbs.data_ptr(), S, eps,
                                     self.dh.data_ptr(), sp))
         h = nets.hash_struct()
-        if self.tc:  # dz-form: each dx epilogue applies the previous layer's ReLU mask
+        # radiance MLP (tcgen05 dz-form: each dx epilogue applies the previous layer's ReLU bits)
+        if self.tc:
             self._lin_bwd_tc(self.r[1], V["rad_w2"], self.dh, self.g64[0], self.rbits[1], G["rad_w2"], G["rad_b2"], 64, 4, sp)
             self._lin_bwd_tc(self.r[0], V["rad_w1"], self.g64[0], self.g64[1], self.rbits[0], G["rad_w1"], G["rad_b1"], 64, 64, sp)
             self._lin_bwd_tc(self.feat, V["rad_w0"], self.g64[1], self.dfeat, None, G["rad_w0"], G["rad_b0"], 32, 64, sp)
-            _lib.check(lib.fv_hash_bwd(C.byref(h), self.xf.data_ptr(), S, self.dfeat.data_ptr(),
-                                       G["table"].data_ptr(), self.dxf.data_ptr(), sp), "fv_hash_bwd")
+        else:
+            self._lin_bwd(self.r[1], V["rad_w2"], self.hd, self.dh, self.g64[0], G["rad_w2"], G["rad_b2"], 64, 4, 0, sp)
+            self._lin_bwd(self.r[0], V["rad_w1"], self.r[1], self.g64[0], self.g64[1], G["rad_w1"], G["rad_b1"], 64, 64, 1, sp)
+            self._lin_bwd(self.feat, V["rad_w0"], self.r[0], self.g64[1], self.dfeat, G["rad_w0"], G["rad_b0"], 32, 64, 1, sp)
+        _lib.check(lib.fv_hash_bwd(C.byref(h), self.xf.data_ptr(), S, self.dfeat.data_ptr(),
+                                   G["table"].data_ptr(), self.dxf.data_ptr(), sp), "fv_hash_bwd")
+        # residual MLP; when the stage is off x_final = x_skel and the gradient goes straight to the warp
+        if not self.residual:
+            self.dxs.copy_(self.dxf)
+        elif self.tc:
             self._lin_bwd_tc(self.h[3], V["off_w4"], self.dxf, self.g128[0], self.hbits[3], G["off_w4"], G["off_b4"], 128, 3, sp)
             self._lin_bwd_tc(self.h[2], V["off_w3"], self.g128[0], self.g128[1], self.hbits[2], G["off_w3"], G["off_b3"], 128, 128, sp)
             self._lin_bwd_tc(self.h[1], V["off_w2"], self.g128[1], self.g128[0], self.hbits[1], G["off_w2"], G["off_b2"], 128, 128, sp)
             self._lin_bwd_tc(self.h[0], V["off_w1"], self.g128[0], self.g128[1], self.hbits[0], G["off_w1"], G["off_b1"], 128, 128, sp)
             self._lin_bwd_tc(self.pe, V["off_w0"], self.g128[1], self.dpe, None, G["off_w0"], G["off_b0"], self.d_pe, 128, sp)
         else:
-            self._lin_bwd(self.r[1], V["rad_w2"], self.hd, self.dh, self.g64[0], G["rad_w2"], G["rad_b2"], 64, 4, 0, sp)
-            self._lin_bwd(self.r[0], V["rad_w1"], self.r[1], self.g64[0], self.g64[1], G["rad_w1"], G["rad_b1"], 64, 64, 1, sp)
-            self._lin_bwd(self.feat, V["rad_w0"], self.r[0], self.g64[1], self.dfeat, G["rad_w0"], G["rad_b0"], 32, 64, 1, sp)
-            _lib.check(lib.fv_hash_bwd(C.byref(h), self.xf.data_ptr(), S, self.dfeat.data_ptr(),
-                                       G["table"].data_ptr(), self.dxf.data_ptr(), sp), "fv_hash_bwd")
             self._lin_bwd(self.h[3], V["off_w4"], self.xres, self.dxf, self.g128[0], G["off_w4"], G["off_b4"], 128, 3, 0, sp)
             self._lin_bwd(self.h[2], V["off_w3"], self.h[3], self.g128[0], self.g128[1], G["off_w3"], G["off_b3"], 128, 128, 1, sp)
             self._lin_bwd(self.h[1], V["off_w2"], self.h[2], self.g128[1], self.g128[0], G["off_w2"], G["off_b2"], 128, 128, 1, sp)
             self._lin_bwd(self.h[0], V["off_w1"], self.h[1], self.g128[0], self.g128[1], G["off_w1"], G["off_b1"], 128, 128, 1, sp)
             self._lin_bwd(self.pe, V["off_w0"], self.h[0], self.g128[1], self.dpe, G["off_w0"], G["off_b0"], self.d_pe, 128, 1, sp)
-        # the folded pose rows of W0: dW0[D:, :] = pose (outer) d b0_eff  (b0_eff = b0 + pose @ W0[D:])
-        G["off_w0"][self.d_pe:].addr_(nets.pose_dev, G["off_b0"])
-        self.dxs.copy_(self.dxf)
-        _lib.check(lib.fv_posenc_bwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.dpe.data_ptr(), self.pe_ld,
-                                     self.dxs.data_ptr(), sp))
+        if self.residual:
+            # the folded pose rows of W0: dW0[D:, :] = pose (outer) d b0_eff  (b0_eff = b0 + pose @ W0[D:])
+            G["off_w0"][self.d_pe:].addr_(nets.pose_dev, G["off_b0"])
+            self.dxs.copy_(self.dxf)
+            _lib.check(lib.fv_posenc_bwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.dpe.data_ptr(),
+                                         self.pe_ld, self.dxs.data_ptr(), sp))
         w = nets.warp_struct()
         _lib.check(lib.fv_warp_bwd(C.byref(w), eps, self.x.data_ptr(), S, self.dxs.data_ptr(), self.dvol.data_ptr(), sp),
                    "fv_warp_bwd")
@@ -257,3 +286,118 @@ class Trainer:
         self.allreduce()
         self.optimizer_step()
         return loss
+
+
+# ------------------------------------------------------------------------------- driver
+
+@dataclass
+class TrainConfig:
+    """SPEC TrainConfig: iterations, loss weights (Eq 14, perceptual proxy), patches,
+    coarse-to-fine milestones as fractions of the run (paper 10K / 50K of 150K),
+    checkpoint cadence.  The learning rates live with the parameter blocks (model.LR_*)."""
+    iterations: int = 1500
+    lam_mse: float = 0.2
+    lam_perc: float = 1.0
+    n_patches: int = 6
+    patch: int = 20
+    residual_on: float = 10.0 / 150.0
+    full_band: float = 50.0 / 150.0
+    seed: int = 0
+    precision: str = "tf32"
+    checkpoint_every: int = 100
+    log_path: Optional[str] = None
+
+    def __post_init__(self):
+        if not (0.0 < self.residual_on < self.full_band < 1.0):
+            raise ValueError("milestones must satisfy 0 < residual_on < full_band < 1 (S:475)")
+        if self.iterations < 1 or self.lam_mse < 0 or self.lam_perc < 0:
+            raise ValueError("iterations >= 1 and non-negative loss weights")
+
+
+def schedule(it: int, cfg: TrainConfig, bands: int = PE_BANDS):
+    """(alpha, residual stage on) at iteration ``it``: alpha = L * clamp((it - it_on) /
+    (it_full - it_on), 0, 1); the residual net is held at exactly zero before
+    it_on (S:352, S:511)."""
+    it_on = int(round(cfg.residual_on * cfg.iterations))
+    it_full = max(int(round(cfg.full_band * cfg.iterations)), it_on + 1)
+    alpha = bands * min(max((it - it_on) / (it_full - it_on), 0.0), 1.0)
+    return float(alpha), it >= it_on
+
+
+def save_checkpoint(path: str, trainer: "Trainer", iteration: int) -> None:
+    """Manifest + raw little-endian float32 arrays: params.bin (the flat master
+    buffer), adam_m.bin, adam_v.bin, manifest.json (block table, Adam step, schedule)."""
+    os.makedirs(path, exist_ok=True)
+    nets = trainer.nets
+    for name, t in (("params", nets.flat), ("adam_m", trainer.m), ("adam_v", trainer.v)):
+        t.detach().cpu().numpy().astype("<f4").tofile(os.path.join(path, f"{name}.bin"))
+    man = {"format": "freeview-b200-checkpoint", "version": 1, "iteration": iteration, "adam_t": trainer.t,
+           "n_params": nets.n_params, "pe_alpha": nets.pe_alpha, "residual": bool(trainer.residual),
+           "blocks": {k: {"offset": a, "size": b - a, "shape": list(nets.views[k].shape)}
+                      for k, (a, b) in nets.block_ranges.items()}}
+    with open(os.path.join(path, "manifest.json"), "w") as f:
+        json.dump(man, f, indent=1)
+
+
+def load_checkpoint(path: str, trainer: "Trainer") -> int:
+    """Restore a save_checkpoint directory into the trainer's model and Adam state; returns
+    the iteration.  Raises DimensionError-style ValueError on a block-table mismatch."""
+    with open(os.path.join(path, "manifest.json")) as f:
+        man = json.load(f)
+    nets = trainer.nets
+    want = {k: [a, b - a] for k, (a, b) in nets.block_ranges.items()}
+    got = {k: [v["offset"], v["size"]] for k, v in man["blocks"].items()}
+    if want != got:
+        raise ValueError("checkpoint block table does not match the model")
+    for name, t in (("params", nets.flat), ("adam_m", trainer.m), ("adam_v", trainer.v)):
+        a = np.fromfile(os.path.join(path, f"{name}.bin"), dtype="<f4")
+        t.copy_(torch.from_numpy(a.astype(np.float32)).to(t.device))
+    trainer.t = int(man["adam_t"])
+    trainer.set_schedule(man["pe_alpha"], man["residual"])
+    nets.refresh()
+    return int(man["iteration"])
+
+
+def train(nets: FreeviewModel, camera: CameraModel, target: np.ndarray, mask: np.ndarray,
+          settings: RenderSettings, cfg: TrainConfig, process_group=None) -> List[dict]:
+    """SPEC train: per iteration apply the coarse-to-fine schedule, sample
+    patches, render them through the full pipeline, loss (Eq 14 with the perceptual proxy),
+    backward, (all-reduce), Adam at the per-group rates; log (iteration, loss, mse_term,
+    perc_term, alpha, stage, wall_ms) to a CSV.  A non-finite loss or gradient restores the
+    last good state (kept every ``checkpoint_every`` iterations) and raises TrainingError."""
+    tr = Trainer(nets, camera, target, mask, settings, n_patches=cfg.n_patches, patch=cfg.patch, seed=cfg.seed,
+                 process_group=process_group, precision=cfg.precision, lam_mse=cfg.lam_mse, lam_perc=cfg.lam_perc)
+    good = (nets.flat.clone(), tr.m.clone(), tr.v.clone(), tr.t)
+    rows = []
+    writer, fh = None, None
+    if cfg.log_path:
+        fh = open(cfg.log_path, "w", newline="")
+        writer = csv.writer(fh)
+        writer.writerow(["iteration", "loss", "mse_term", "perc_term", "alpha", "stage", "wall_ms"])
+    try:
+        t0 = time.perf_counter()
+        for it in range(cfg.iterations):
+            alpha, residual = schedule(it, cfg)
+            tr.set_schedule(alpha, residual)
+            tr.step(it)
+            vals = tr.loss.tolist()
+            mse = vals[1] if tr.lam_perc != 0.0 or tr.lam_mse != 1.0 else vals[0]
+            flag = int(tr.flag.item())
+            if not np.isfinite(vals[0]) or flag:
+                nets.flat.copy_(good[0]); tr.m.copy_(good[1]); tr.v.copy_(good[2]); tr.t = good[3]
+                nets.refresh()
+                raise TrainingError(f"non-finite loss/gradient at iteration {it}; last good state restored")
+            row = {"iteration": it, "loss": vals[0], "mse_term": mse, "perc_term": vals[2] if tr.lam_perc else 0.0,
+                   "alpha": alpha, "stage": "residual" if residual else "skeleton",
+                   "wall_ms": (time.perf_counter() - t0) * 1e3}
+            rows.append(row)
+            if writer:
+                writer.writerow([row[k] for k in ("iteration", "loss", "mse_term", "perc_term", "alpha", "stage",
+                                                  "wall_ms")])
+            if cfg.checkpoint_every and (it + 1) % cfg.checkpoint_every == 0:
+                good = (nets.flat.clone(), tr.m.clone(), tr.v.clone(), tr.t)
+    finally:
+        if fh:
+            fh.close()
+    train.last_trainer = tr
+    return rows

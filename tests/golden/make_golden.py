@@ -197,6 +197,29 @@ def main():
     g["wp_fg"], g["wp_xskel"], g["wp_L"], g["wp_up"] = fgm, xs.data, L.data, upx
     g["wp_dlogits"] = grads(lambda lg: ad.tsum(ad.mul(warp(lg)[0], ad.Tensor(upx))), ad.Tensor(logits.copy()))[0]
 
+    # --- SPEC compute_loss composed from reference ops: lam_mse * MSE + lam_perc *
+    # multi-scale gradient difference (diff_axis ad:844, avgpool2 ad:862, absval, tmean)
+    pr = rng.uniform(0, 1, (3, 8, 8, 3))
+    pt = rng.uniform(0, 1, (3, 8, 8, 3))
+
+    def patch_loss(r, t, lam_mse=0.2, lam_perc=1.0):
+        e = ad.sub(r, t)
+        mse = ad.tmean(ad.mul(e, e))
+        terms = []
+        for lvl in range(2):
+            if lvl:
+                r, t = ad.avgpool2(r), ad.avgpool2(t)
+            for ax in (2, 1):
+                terms.append(ad.tmean(ad.absval(ad.sub(ad.diff_axis(r, ax), ad.diff_axis(t, ax)))))
+        perc = ad.add(ad.add(terms[0], terms[1]), ad.add(terms[2], terms[3]))
+        return ad.add(ad.mul_scalar(mse, lam_mse), ad.mul_scalar(perc, lam_perc)), mse, perc
+
+    tot, mse, perc = patch_loss(ad.Tensor(pr), ad.Tensor(pt))
+    g["pl_r"], g["pl_t"] = pr, pt
+    g["pl_loss"], g["pl_mse"], g["pl_perc"] = tot.data, mse.data, perc.data
+    g["pl_dr"] = grads(lambda r: patch_loss(r, ad.Tensor(pt))[0], ad.Tensor(pr.copy()))[0]
+    g["pl_offset_loss"] = patch_loss(ad.Tensor(pt + 0.1), ad.Tensor(pt))[0].data   # S:502 known answer
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT) / 1024:.1f} KiB, {len(g)} arrays)")
 

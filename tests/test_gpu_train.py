@@ -281,3 +281,107 @@ def test_training_reduces_loss_and_trainer_raises_on_nan():
     tr.step(200)
     with pytest.raises(TrainingError):
         tr.check_finite()
+
+
+def test_patch_loss_kernel_matches_oracle():
+    """fv_patch_loss (SPEC compute_loss with the perceptual proxy) vs oracle/loss.py."""
+    from oracle import loss as oloss
+    rng = np.random.default_rng(11)
+    g, s = 6, 20
+    rgb = rng.uniform(0, 1, (g * s * s, 3)).astype(np.float32)
+    img = rng.uniform(0, 1, (64 * 64, 3)).astype(np.float32)
+    pix = rng.permutation(64 * 64)[: g * s * s].astype(np.int32)
+    lib = _lib.load()
+    loss = torch.zeros(3, device=DEV)
+    drgb = torch.empty((g * s * s, 3), device=DEV)
+    for lam_mse, lam_perc in ((0.2, 1.0), (1.0, 0.0), (0.0, 1.0)):
+        _lib.check(lib.fv_patch_loss(_t(rgb).data_ptr(), _t(img).data_ptr(), _t(pix, torch.int32).data_ptr(), g, s,
+                                     lam_mse, lam_perc, loss.data_ptr(), drgb.data_ptr(), _lib.stream_ptr()))
+        tot, mse, perc, grad = oloss.patch_loss(rgb.reshape(g, s, s, 3), img[pix].reshape(g, s, s, 3), lam_mse,
+                                                lam_perc)
+        got = loss.cpu().numpy()
+        assert abs(got[0] - tot) < 1e-5 * max(1.0, tot) and abs(got[1] - mse) < 1e-6
+        if lam_perc:
+            assert abs(got[2] - perc) < 1e-5 * max(1.0, perc)
+        _close(drgb.cpu().numpy(), grad.reshape(-1, 3), 1e-4, f"dloss/drgb ({lam_mse}, {lam_perc})")
+    # S:501-503 known answers: identical -> 0; constant offset 0.1 -> 0.2 * 0.01, zero gradient term
+    _lib.check(lib.fv_patch_loss(_t(img[pix] + 0.1).data_ptr(), _t(img).data_ptr(), _t(pix, torch.int32).data_ptr(),
+                                 g, s, 0.2, 1.0, loss.data_ptr(), drgb.data_ptr(), _lib.stream_ptr()))
+    got = loss.cpu().numpy()
+    assert abs(got[0] - 0.002) < 1e-6 and got[2] < 1e-6
+
+
+@pytest.mark.parametrize("residual,lam_perc", [(False, 1.0), (True, 1.0)])
+def test_step_gradients_with_schedule_and_patch_loss(residual, lam_perc):
+    """Training step with the SPEC loss (0.2 MSE + 1.0 gradient-difference proxy) and the
+    coarse-to-fine state (alpha window, residual stage on/off) vs the oracle's float64
+    backward; residual off => x_final == x_skel exactly and zero residual-MLP gradients."""
+    sc = make("c1", width=48, height=48, n_samples=24, table_scale=0.5, bias_scale=0.05, background=(0.1, 0.3, 0.8))
+    nets = FreeviewModel(sc)
+    target, mask = target_image(sc)
+    st = RenderSettings.from_config(sc.cfg, seed=5)
+    tr = Trainer(nets, sc.camera, target, mask, st, n_patches=2, patch=16, seed=3, precision="fp32", lam_mse=0.2,
+                 lam_perc=lam_perc)
+    alpha = 2.5
+    tr.set_schedule(alpha, residual)
+    pix = patch_pixels(sample_patches(mask, 2, 16, 3, 0), 16, 48)
+    loss = tr.forward(pix)
+    tr.backward()
+    torch.cuda.synchronize()
+    osc = oracle_scene(sc, nets=nets)
+    cc = ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera)
+    ost = osettings(sc.cfg, seed=5, pe_alpha=alpha, offset_enabled=residual)
+    oloss_, og, _ = opipe.loss_and_grads(osc, cc, pix, 48, ost, target.reshape(-1, 3)[pix], patch=(16, 0.2, lam_perc))
+    assert abs(loss.item() - oloss_) < 1e-5 * max(1.0, oloss_)
+    G = tr.gviews
+    if not residual:
+        fg = tr.xs[:, 3] > st.eps_w
+        assert torch.equal(tr.xf[fg], tr.xs[fg, :3])                        # x_res exactly 0
+        for i in range(5):
+            assert float(G[f"off_w{i}"].abs().max()) == 0.0 and float(G[f"off_b{i}"].abs().max()) == 0.0
+    for name, ref in [("table", og["table"]), ("rad_w0", og["rad_w"][0]), ("rad_b2", og["rad_b"][2])] + \
+            ([("off_w1", og["off_w"][1]), ("off_b0", og["off_b"][0])] if residual else []):
+        got = G[name].cpu().numpy().astype(np.float64)
+        assert np.abs(got - ref).max() <= 1e-3, name
+        fro = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+        print(f"{name}: frobenius {fro:.2e}")
+        assert fro < 2e-2, name
+    vol = osc["vol"].astype(np.float64)
+    ref = owarp.softmax0_bwd(vol, og["vol"])
+    got = G["vol_logits"].cpu().numpy().astype(np.float64)
+    assert np.abs(got - ref).max() <= 1e-3
+
+
+def test_train_driver_schedule_log_and_checkpoint_roundtrip(tmp_path):
+    """SPEC train: CSV log rows, x_res exactly 0 before the residual milestone,
+    alpha law, loss decreases; checkpoint save -> load into a fresh model renders bitwise
+    identically (S:513)."""
+    from paper_2306_16541_b200.render import Renderer
+    from paper_2306_16541_b200.train import TrainConfig, load_checkpoint, save_checkpoint, schedule, train
+    sc = make("c3", width=64, height=64, n_samples=32)
+    nets = FreeviewModel(sc)
+    target, mask = target_image(sc)
+    st = RenderSettings.from_config(sc.cfg, seed=1)
+    cfg = TrainConfig(iterations=120, n_patches=4, patch=16, log_path=str(tmp_path / "log.csv"), checkpoint_every=40)
+    rows = train(nets, sc.camera, target, mask, st, cfg)
+    assert len(rows) == 120 and open(cfg.log_path).read().count("\n") == 121
+    it_on = int(round(cfg.residual_on * cfg.iterations))
+    assert all(r["stage"] == "skeleton" and r["alpha"] == 0.0 for r in rows[:it_on])
+    assert rows[-1]["alpha"] == 6.0 and rows[-1]["stage"] == "residual"
+    alphas = [r["alpha"] for r in rows]
+    assert all(b >= a for a, b in zip(alphas, alphas[1:]))
+    assert np.mean([r["loss"] for r in rows[-20:]]) < np.mean([r["loss"] for r in rows[:20]])
+    assert schedule(0, cfg) == (0.0, False)
+    tr = train.last_trainer
+    save_checkpoint(str(tmp_path / "ck"), tr, 120)
+    rnd = Renderer()
+    st_r = RenderSettings.from_config(sc.cfg, seed=2, occupancy=False)
+    img0, _ = rnd.render_image(nets, sc.camera, sc.poses[0], st_r)
+    img0 = img0.clone()
+    nets2 = FreeviewModel(sc)
+    tr2 = Trainer(nets2, sc.camera, target, mask, st, n_patches=4, patch=16)
+    assert load_checkpoint(str(tmp_path / "ck"), tr2) == 120
+    img1, _ = rnd.render_image(nets2, sc.camera, sc.poses[0], st_r)
+    torch.cuda.synchronize()
+    assert torch.equal(img0, img1)
+    assert torch.equal(tr2.m, tr.m) and tr2.t == tr.t

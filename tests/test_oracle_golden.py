@@ -136,3 +136,17 @@ def test_skeleton_warp_forward_and_volume_gradient():
     dvol = owarp.skeleton_warp_bwd(out, d, vol.shape, BMIN, BMAX)
     dlog = owarp.softmax0_bwd(vol, dvol)
     assert np.max(np.abs(dlog - G["wp_dlogits"])) < 1e-12
+
+
+def test_patch_loss_matches_reference_composition():
+    from oracle import loss as oloss
+    tot, mse, perc, dr = oloss.patch_loss(G["pl_r"], G["pl_t"])
+    assert abs(tot - float(G["pl_loss"])) < 1e-12
+    assert abs(mse - float(G["pl_mse"])) < 1e-12 and abs(perc - float(G["pl_perc"])) < 1e-12
+    assert np.max(np.abs(dr - G["pl_dr"])) < 1e-12
+    # S:500-503 known answers: identical patches -> 0; constant offset -> 0.2 * 0.01; symmetry
+    t = G["pl_t"]
+    assert oloss.patch_loss(t, t)[0] == 0.0
+    off = oloss.patch_loss(t + 0.1, t)
+    assert abs(off[0] - float(G["pl_offset_loss"])) < 1e-15 and abs(off[0] - 0.002) < 1e-12 and off[2] < 1e-12
+    assert abs(oloss.patch_loss(G["pl_r"], t)[0] - oloss.patch_loss(t, G["pl_r"])[0]) < 1e-12

@@ -17,4 +17,4 @@ tr = Trainer(nets, sc.camera, target, mask, RenderSettings.from_config(sc.cfg, s
 for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
     tr.step(i)
 torch.cuda.synchronize()
-print("loss", tr.loss.item())
+print("loss", tr.loss[0].item())
