@@ -83,7 +83,11 @@ class Trainer:
         f32 = dict(device=dev, dtype=torch.float32)
         self.target = torch.from_numpy(np.ascontiguousarray(target.reshape(-1, 3), np.float32)).to(dev)
         self.pix = torch.empty(self.R, device=dev, dtype=torch.int32)
-        self.pix_host = torch.empty(self.R, dtype=torch.int32, pin_memory=True)
+        # pinned ring for the per-step patch pixel ids: the host may run ahead of the GPU, so a
+        # slot is rewritten only after the H2D copy that last read it has completed
+        self.pix_ring = [torch.empty(self.R, dtype=torch.int32, pin_memory=True) for _ in range(4)]
+        self.pix_events = [None] * 4
+        self.pix_slot = 0
         d_pe = 3 + 6 * PE_BANDS
         self.d_pe = d_pe
         self.pe_ld = (d_pe + 3) // 4 * 4 if self.tc else d_pe   # 16-byte rows for the TF32 GEMMs
@@ -175,8 +179,15 @@ class Trainer:
         if pix_np is None:
             pix_np = patch_pixels(sample_patches(self.mask, self.n_patches, self.patch, self.seed, step),
                                   self.patch, self.cam.width)
-        self.pix_host.numpy()[:] = pix_np
-        self.pix.copy_(self.pix_host, non_blocking=True)
+        k = self.pix_slot
+        self.pix_slot = (k + 1) % len(self.pix_ring)
+        if self.pix_events[k] is not None:
+            self.pix_events[k].synchronize()
+        self.pix_ring[k].numpy()[:] = pix_np
+        self.pix.copy_(self.pix_ring[k], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.pix_events[k] = ev
         m, cs, w = march_struct(self.st, self.pix, None), camera_struct(self.cam), nets.warp_struct()
         h, eps = nets.hash_struct(), self.st.eps_w
         _lib.check(lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), self.R, self.xs.data_ptr(),
