@@ -597,7 +597,8 @@ __global__ void __launch_bounds__(384, 1) k_dw(DwArgs3 a, const __grid_constant_
 }
 
 // ============================================================================ host side
-// FV_G3_NOTMA=1: converter warps load every operand themselves (tests the unaligned path)
+// FV_G3_NOTMA=1: converter / producer warps load every operand themselves (exercises the
+// path unaligned operands take; the tests also reach it with odd row strides)
 static bool no_tma() {
   static const int v = [] { const char* e = std::getenv("FV_G3_NOTMA"); return e && e[0] == '1' ? 1 : 0; }();
   return v != 0;
@@ -652,10 +653,7 @@ int32_t rows_gemm(RowsArgs a, cudaStream_t st) {
   if (a.M == 0) return FV_OK;
   CUtensorMap tm{}, to{};
   a.tma = make_tmap(&tm, a.A, a.K, a.M, a.lda, 128) ? 1 : 0;
-  static const int dbg = [] { const char* e = std::getenv("FV_G3_DBG"); return e ? atoi(e) : 0; }();
-  a.dbg = dbg;
-  static const bool no_out = [] { const char* e = std::getenv("FV_G3_NOTMAOUT"); return e && e[0] == '1'; }();
-  a.tma_out = !no_out && make_tmap(&to, a.out, a.N, a.M, a.ldo, 32) ? 1 : 0;
+  a.tma_out = make_tmap(&to, a.out, a.N, a.M, a.ldo, 32) ? 1 : 0;
   const int bbytes = 2 * a.nkc * a.Np * 128;
   const int obytes = a.tma_out ? 2 * kStageA : 0;
   a.stages = std::min(6, (kSmemMax - 2048 - bbytes - obytes) / kStageA);

@@ -15,7 +15,7 @@ struct RowsArgs {
   uint32_t* bits_out = nullptr;                // epilogue: bit (y > 0) per output, [M][ceil(N/32)] words
   const uint32_t* bits_in = nullptr;           // epilogue: * bit, [M][ceil(N/32)] words (ReLU mask as bits)
   // filled by rows_gemm
-  int Np = 0, nkc = 0, nsteps = 0, tma = 0, tma_out = 0, stages = 0, dbg = 0;
+  int Np = 0, nkc = 0, nsteps = 0, tma = 0, tma_out = 0, stages = 0;
 };
 
 struct DwArgs3 {

@@ -75,10 +75,13 @@ def test_linear_bwd_matches_numpy():
 
 
 @pytest.mark.parametrize("m,k,ld,n,act", [(3000, 39, 40, 128, 1), (2999, 128, 128, 128, 1), (4096, 128, 128, 3, 0),
-                                          (1000, 64, 64, 4, 0), (5000, 32, 32, 64, 1)])
+                                          (1000, 64, 64, 4, 0), (5000, 32, 32, 64, 1),
+                                          # odd row strides: operands TMA cannot address take the
+                                          # converter-loaded / direct-store paths
+                                          (1501, 39, 39, 128, 1), (777, 20, 21, 24, 1), (300, 5, 7, 9, 0)])
 def test_linear_tf32_tensor_core_layers(m, k, ld, n, act):
-    """fv_linear_fwd_tc / fv_linear_bwd_tc (tcgen05 kind::tf32) vs float64 numpy; TF32 has a
-    10-bit mantissa, so the bar is 1e-2 relative to the output scale."""
+    """fv_linear_fwd_tc / fv_linear_bwd_tc (tcgen05 kind::tf32, split-precision 3xTF32 with
+    fp32 accumulation) vs float64 numpy: ~fp32 accuracy, bar 2e-5 relative to the output scale."""
     rng = np.random.default_rng(m + k + n)
     x = np.zeros((m, ld), np.float32)
     x[:, :k] = rng.normal(size=(m, k))
@@ -101,8 +104,8 @@ def test_linear_tf32_tensor_core_layers(m, k, ld, n, act):
     _lib.check(lib.fv_linear_bwd_tc(xt.data_ptr(), ld, wt.data_ptr(), dzt.data_ptr(), n, dx.data_ptr(), ld,
                                     xm.data_ptr(), dw.data_ptr(), db.data_ptr(), m, k, n, _lib.stream_ptr()))
     dxr = (dz.astype(np.float64) @ w.T.astype(np.float64)) * (xmask[:, :k] > 0)
-    _close(dx.cpu().numpy()[:, :k], dxr, 1e-2, "dx")
-    _close(dw.cpu().numpy(), x[:, :k].T.astype(np.float64) @ dz, 1e-2, "dw")
+    _close(dx.cpu().numpy()[:, :k], dxr, 2e-5, "dx")
+    _close(dw.cpu().numpy(), x[:, :k].T.astype(np.float64) @ dz, 2e-5, "dw")
     _close(db.cpu().numpy(), dz.sum(0, dtype=np.float64), 1e-5, "db")
 
 
