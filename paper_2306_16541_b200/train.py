@@ -34,7 +34,7 @@ from .errors import TrainingError
 from .model import FreeviewModel, hann_band_weights
 from .render import RenderSettings, camera_struct, march_struct
 from .scene import PE_BANDS
-from .shard import allreduce_mean
+from .shard import GradBuckets
 
 
 def sample_patches(mask: np.ndarray, n_patches: int, size: int, seed: int, step: int) -> np.ndarray:
@@ -128,6 +128,7 @@ class Trainer:
         self.m = torch.zeros_like(nets.flat)
         self.v = torch.zeros_like(nets.flat)
         self.flag = torch.zeros(1, device=dev, dtype=torch.int32)
+        self.buckets = GradBuckets(self.grad, process_group)
         self.t = 0
         self.gviews = {}
         for name, (a, b) in nets.block_ranges.items():
@@ -242,6 +243,8 @@ class Trainer:
             self._lin_bwd(self.feat, V["rad_w0"], self.r[0], self.g64[1], self.dfeat, G["rad_w0"], G["rad_b0"], 32, 64, 1, sp)
         _lib.check(lib.fv_hash_bwd(C.byref(h), self.xf.data_ptr(), S, self.dfeat.data_ptr(),
                                    G["table"].data_ptr(), self.dxf.data_ptr(), sp), "fv_hash_bwd")
+        # table + radiance-MLP gradients are final: their all-reduce overlaps the rest
+        self.buckets.launch(0, self.nets.segments[0][0])
         # residual MLP; when the stage is off x_final = x_skel and the gradient goes straight to the warp
         if not self.residual:
             self.dxs.copy_(self.dxf)
@@ -271,7 +274,8 @@ class Trainer:
                                        G["vol_logits"].data_ptr(), sp))
 
     def allreduce(self):
-        allreduce_mean(self.grad, self.pg)
+        """Sum over ranks / world of the flat gradient (the path's only exchange)."""
+        self.buckets.finish()
 
     def optimizer_step(self):
         nets = self.nets

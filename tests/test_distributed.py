@@ -62,11 +62,15 @@ def _maxtime(rank, world):
 
 
 def _trainer_allreduce(rank, world):
-    # the Trainer's exchange on its flat gradient buffer (CPU tensor stands in for CUDA)
+    # the Trainer's exchange on its flat gradient buffer (CPU tensor stands in for CUDA):
+    # bucket [0, 11) launched asynchronously mid-backward, the rest at allreduce()
     from paper_2306_16541_b200.train import Trainer
     class T:  # minimal stand-in with the attributes Trainer.allreduce uses
-        pg = None
         grad = torch.full((17,), float(rank * 2 + 1))
+        grad[3] = 10.0 * rank
+        buckets = shard.GradBuckets(grad)
+    T.buckets.launch(0, 11)
+    T.grad[11:] += 1.0                     # later backward kernels touch only later blocks
     Trainer.allreduce(T)
     return T.grad.numpy()
 
@@ -92,7 +96,10 @@ def test_max_over_ranks_world2():
 
 def test_trainer_gradient_exchange_world2():
     out = _run(_trainer_allreduce)
-    assert np.allclose(out[0], 2.0) and np.allclose(out[1], 2.0)
+    want = np.full(17, 2.0)
+    want[3] = 5.0
+    want[11:] = 3.0
+    assert np.allclose(out[0], want) and np.allclose(out[1], want)
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
