@@ -15,6 +15,12 @@ __device__ __forceinline__ int64_t sidx(const CompIn& in, int64_t r, int i, int 
   return in.blocked ? sample_index(r, i, n) : r * n + i;
 }
 
+// Samples are read in chunks of CH (all loads of a chunk issued before the sequential
+// arithmetic consumes them: with few rays per SM -- 6,144 in a training step -- the
+// per-sample load latency, not bandwidth, bounds a one-sample-at-a-time loop).  The
+// arithmetic and its order are unchanged.
+constexpr int CH = 8;
+
 __global__ void k_composite_fwd(CompIn in, int64_t n_rays, int n, float3 bg, float eps_w, float eps_t,
                                 const int32_t* __restrict__ out_pix, float* __restrict__ rgb_out,
                                 float* __restrict__ alpha_out, float* __restrict__ trans) {
@@ -22,23 +28,38 @@ __global__ void k_composite_fwd(CompIn in, int64_t n_rays, int n, float3 bg, flo
   if (r >= n_rays) return;
   float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
   int i = 0;
-  for (; i < n; ++i) {
-    if (eps_t > 0.f && T < eps_t) break;
-    const int64_t s = sidx(in, r, i, n);
-    if (trans) trans[r * (n + 1) + i] = T;
-    const float L = in.lik[s * in.lik_stride];
-    // background samples carry sigma = 0 (abar = 0, T unchanged): with a compacted field
-    // their [c, sigma] slot was never written, so they are skipped without reading it
-    if (in.skip_bg && !(L > eps_w)) continue;
-    const float4 v = in.rgbs[s];
-    const float a = __fsub_rn(1.f, expf(-__fmul_rn(v.w, in.delta[s])));
-    const float gate = fminf(fmaxf(__fdiv_rn(L, eps_w), 0.f), 1.f);
-    const float ab = __fmul_rn(a, gate);
-    const float w = __fmul_rn(T, ab);
-    cr = __fadd_rn(cr, __fmul_rn(w, v.x));
-    cg = __fadd_rn(cg, __fmul_rn(w, v.y));
-    cb = __fadd_rn(cb, __fmul_rn(w, v.z));
-    T = __fmul_rn(T, __fsub_rn(1.f, ab));
+  bool stop = false;
+  for (int i0 = 0; i0 < n && !stop; i0 += CH) {
+    float Lc[CH], dc[CH];
+    float4 vc[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      if (i0 + k < n) {
+        const int64_t s = sidx(in, r, i0 + k, n);
+        Lc[k] = in.lik[s * in.lik_stride];
+        // background samples carry sigma = 0 (abar = 0, T unchanged): with a compacted
+        // field their [c, sigma] slot was never written, so it is not read
+        vc[k] = (in.skip_bg && !(Lc[k] > eps_w)) ? make_float4(0.f, 0.f, 0.f, 0.f) : in.rgbs[s];
+        dc[k] = in.delta[s];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      if (i0 + k >= n) break;
+      if (eps_t > 0.f && T < eps_t) { stop = true; break; }
+      i = i0 + k + 1;
+      if (trans) trans[r * (n + 1) + i0 + k] = T;
+      if (in.skip_bg && !(Lc[k] > eps_w)) continue;
+      const float4 v = vc[k];
+      const float a = __fsub_rn(1.f, expf(-__fmul_rn(v.w, dc[k])));
+      const float gate = fminf(fmaxf(__fdiv_rn(Lc[k], eps_w), 0.f), 1.f);
+      const float ab = __fmul_rn(a, gate);
+      const float w = __fmul_rn(T, ab);
+      cr = __fadd_rn(cr, __fmul_rn(w, v.x));
+      cg = __fadd_rn(cg, __fmul_rn(w, v.y));
+      cb = __fadd_rn(cb, __fmul_rn(w, v.z));
+      T = __fmul_rn(T, __fsub_rn(1.f, ab));
+    }
   }
   if (trans) for (int j = i; j <= n; ++j) trans[r * (n + 1) + j] = T;
   cr = __fadd_rn(cr, __fmul_rn(T, bg.x));
@@ -59,23 +80,40 @@ __global__ void k_composite_bwd(CompIn in, const float* __restrict__ trans, int6
   const float gr = drgb[3 * r], gg = drgb[3 * r + 1], gb = drgb[3 * r + 2];
   const float ga = dalpha ? dalpha[r] : 0.f;
   float qr = bg.x, qg = bg.y, qb = bg.z, P = 1.f;
-  for (int i = n - 1; i >= 0; --i) {
-    const int64_t s = sidx(in, r, i, n);
-    const float4 v = in.rgbs[s];
-    const float d = in.delta[s];
-    const float L = in.lik[s * in.lik_stride];
-    const float e = expf(-v.w * d);
-    const float a = 1.f - e;
-    const float gate = fminf(fmaxf(L / eps_w, 0.f), 1.f);
-    const float ab = a * gate;
-    const float Ti = trans[r * (n + 1) + i];
-    const float dab = Ti * (gr * (v.x - qr) + gg * (v.y - qg) + gb * (v.z - qb) + ga * P);
-    const float wt = Ti * ab;
-    dout[s] = make_float4(wt * gr, wt * gg, wt * gb, dab * gate * d * e);
-    qr = ab * v.x + (1.f - ab) * qr;
-    qg = ab * v.y + (1.f - ab) * qg;
-    qb = ab * v.z + (1.f - ab) * qb;
-    P *= 1.f - ab;
+  for (int i1 = n - 1; i1 >= 0; i1 -= CH) {           // chunks of CH samples, back to front
+    float4 vc[CH];
+    float dc[CH], Lc[CH], Tc[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int i = i1 - k;
+      if (i >= 0) {
+        const int64_t s = sidx(in, r, i, n);
+        vc[k] = in.rgbs[s];
+        dc[k] = in.delta[s];
+        Lc[k] = in.lik[s * in.lik_stride];
+        Tc[k] = trans[r * (n + 1) + i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int i = i1 - k;
+      if (i < 0) break;
+      const int64_t s = sidx(in, r, i, n);
+      const float4 v = vc[k];
+      const float d = dc[k];
+      const float e = expf(-v.w * d);
+      const float a = 1.f - e;
+      const float gate = fminf(fmaxf(Lc[k] / eps_w, 0.f), 1.f);
+      const float ab = a * gate;
+      const float Ti = Tc[k];
+      const float dab = Ti * (gr * (v.x - qr) + gg * (v.y - qg) + gb * (v.z - qb) + ga * P);
+      const float wt = Ti * ab;
+      dout[s] = make_float4(wt * gr, wt * gg, wt * gb, dab * gate * d * e);
+      qr = ab * v.x + (1.f - ab) * qr;
+      qg = ab * v.y + (1.f - ab) * qg;
+      qb = ab * v.z + (1.f - ab) * qb;
+      P *= 1.f - ab;
+    }
   }
 }
 

@@ -6,24 +6,36 @@
 
 namespace fv {
 
+// One thread per sample, levels in turn; the 2L features of the block's 128 rows are
+// staged in shared memory and stored as contiguous runs (coalesced) instead of 2L strided
+// 4-byte stores per thread.
 __global__ void __launch_bounds__(128) k_hash_fwd(fv_hash h, const float* __restrict__ x, int64_t n,
                                                   float* __restrict__ feat, uint32_t* __restrict__ index) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  float xn[3]; bool mask[3];
-  hash_norm(h, x[3 * p], x[3 * p + 1], x[3 * p + 2], xn, mask);
-  for (int l = 0; l < h.n_levels; ++l) {
-    HashCell c;
-    hash_level_cell(xn, h.res[l], c);
-    uint32_t idx[8];
-    const float2 f = hash_level_feat(h, l, c, index ? idx : nullptr);
-    feat[p * (2 * h.n_levels) + 2 * l] = f.x;
-    feat[p * (2 * h.n_levels) + 2 * l + 1] = f.y;
-    if (index) {
+  __shared__ float sf[128 * (2 * FV_MAX_LEVELS + 1)];
+  const int t = threadIdx.x;
+  const int64_t p0 = (int64_t)blockIdx.x * 128;
+  const int64_t p = p0 + t;
+  const int F = 2 * h.n_levels, L1 = F + 1;
+  if (p < n) {
+    float xn[3]; bool mask[3];
+    hash_norm(h, x[3 * p], x[3 * p + 1], x[3 * p + 2], xn, mask);
+    for (int l = 0; l < h.n_levels; ++l) {
+      HashCell c;
+      hash_level_cell(xn, h.res[l], c);
+      uint32_t idx[8];
+      const float2 f = hash_level_feat(h, l, c, index ? idx : nullptr);
+      sf[t * L1 + 2 * l] = f.x;
+      sf[t * L1 + 2 * l + 1] = f.y;
+      if (index) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) index[(p * h.n_levels + l) * 8 + q] = idx[q];
+        for (int q = 0; q < 8; ++q) index[(p * h.n_levels + l) * 8 + q] = idx[q];
+      }
     }
   }
+  __syncthreads();
+  const int64_t rows = n - p0 < 128 ? n - p0 : 128;
+  float* dst = feat + p0 * F;
+  for (int64_t i = t; i < rows * F; i += 128) dst[i] = sf[(i / F) * L1 + i % F];
 }
 
 // dtable += w_corner * dfeat (float2 vector atomics); dx = sum_l d feat_l / d x.

@@ -8,27 +8,42 @@
 namespace fv {
 
 // xs (n,4) = [x_skel, L]; rows with L <= eps_w produce zeros.
-__global__ void k_posenc_fwd(const float4* __restrict__ xs, int64_t n, float eps_w, int bands, PeW w,
-                             float* __restrict__ pe, int64_t ld) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const int D = 3 + 6 * bands;
-  const float4 v = xs[p];
-  float* o = pe + p * ld;
-  for (int j = D; j < ld; ++j) o[j] = 0.f;  // row padding (16-byte aligned rows for the GEMMs)
-  if (!(v.w > eps_w)) { for (int j = 0; j < D; ++j) o[j] = 0.f; return; }
-  const float x[3] = {v.x, v.y, v.z};
-  o[0] = x[0]; o[1] = x[1]; o[2] = x[2];
-  for (int k = 0; k < bands; ++k) {
-    const float freq = __fmul_rn((float)(1 << k), 3.14159265358979323846f);
+// Rows of ld floats (ld = 40 at 6 bands) are assembled in shared memory and written by
+// the block as contiguous 16-byte chunks: a thread-per-row store pattern scatters 4-byte
+// writes over 32 rows per warp instruction (a partial sector each), which made this
+// write-only kernel ~6x slower than its 126 MB of output.
+__global__ void __launch_bounds__(128) k_posenc_fwd(const float4* __restrict__ xs, int64_t n, float eps_w, int bands,
+                                                    PeW w, float* __restrict__ pe, int64_t ld) {
+  extern __shared__ float srow[];                       // [128][ld + 1]
+  const int64_t p0 = (int64_t)blockIdx.x * 128;
+  const int t = threadIdx.x;
+  const int64_t p = p0 + t;
+  const int D = 3 + 6 * bands, L1 = (int)ld + 1;
+  float* o = srow + t * L1;
+  for (int j = 0; j < ld; ++j) o[j] = 0.f;              // row padding + background rows
+  if (p < n) {
+    const float4 v = xs[p];
+    if (v.w > eps_w) {
+      const float x[3] = {v.x, v.y, v.z};
+      o[0] = x[0]; o[1] = x[1]; o[2] = x[2];
+      for (int k = 0; k < bands; ++k) {
+        const float freq = __fmul_rn((float)(1 << k), 3.14159265358979323846f);
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      float s, c;
-      sincosf(__fmul_rn(x[j], freq), &s, &c);
-      o[3 + 6 * k + j] = __fmul_rn(w.w[k], s);
-      o[3 + 6 * k + 3 + j] = __fmul_rn(w.w[k], c);
+        for (int j = 0; j < 3; ++j) {
+          float sn, cs;
+          sincosf(__fmul_rn(x[j], freq), &sn, &cs);
+          o[3 + 6 * k + j] = __fmul_rn(w.w[k], sn);
+          o[3 + 6 * k + 3 + j] = __fmul_rn(w.w[k], cs);
+        }
+      }
     }
   }
+  (void)D;
+  __syncthreads();
+  const int64_t rows = n - p0 < 128 ? n - p0 : 128;
+  const int64_t total = rows * ld;                        // the block's rows are contiguous in pe
+  float* dst = pe + p0 * ld;
+  for (int64_t i = t; i < total; i += 128) dst[i] = srow[(i / ld) * L1 + i % ld];
 }
 
 // dx[p] += d posenc / d x  (ad:602-609): raw columns + sum_k w_k f_k (gs cos - gc sin)
@@ -150,7 +165,10 @@ extern "C" int32_t fv_posenc_fwd(const float* d_xs, int64_t n, float eps_w, int3
   if (n == 0) return FV_OK;
   PeW pw{};
   for (int i = 0; i < bands; ++i) pw.w[i] = w[i];
-  k_posenc_fwd<<<g1(n), 128, 0, (cudaStream_t)stream>>>((const float4*)d_xs, n, eps_w, bands, pw, d_pe, ld);
+  const size_t smem = (size_t)128 * (ld + 1) * sizeof(float);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_posenc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_posenc_fwd<<<(unsigned)((n + 127) / 128), 128, smem, (cudaStream_t)stream>>>((const float4*)d_xs, n, eps_w, bands,
+                                                                                  pw, d_pe, ld);
   return check_launch("fv_posenc_fwd");
 }
 
