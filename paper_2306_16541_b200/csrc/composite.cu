@@ -17,10 +17,12 @@ __device__ __forceinline__ int64_t sidx(const CompIn& in, int64_t r, int i, int 
 
 // Samples are read in chunks of CH (all loads of a chunk issued before the sequential
 // arithmetic consumes them: with few rays per SM -- 6,144 in a training step -- the
-// per-sample load latency, not bandwidth, bounds a one-sample-at-a-time loop).  The
-// arithmetic and its order are unchanged.
-constexpr int CH = 8;
+// per-sample load latency, not bandwidth, bounds a one-sample-at-a-time loop; with a full
+// frame of rays CH = 1 keeps registers low and occupancy high).  The arithmetic and its
+// order are the same for every CH.
+constexpr int kFewRays = 65536;
 
+template <int CH>
 __global__ void k_composite_fwd(CompIn in, int64_t n_rays, int n, float3 bg, float eps_w, float eps_t,
                                 const int32_t* __restrict__ out_pix, float* __restrict__ rgb_out,
                                 float* __restrict__ alpha_out, float* __restrict__ trans) {
@@ -39,8 +41,9 @@ __global__ void k_composite_fwd(CompIn in, int64_t n_rays, int n, float3 bg, flo
         Lc[k] = in.lik[s * in.lik_stride];
         // background samples carry sigma = 0 (abar = 0, T unchanged): with a compacted
         // field their [c, sigma] slot was never written, so it is not read
-        vc[k] = (in.skip_bg && !(Lc[k] > eps_w)) ? make_float4(0.f, 0.f, 0.f, 0.f) : in.rgbs[s];
-        dc[k] = in.delta[s];
+        const bool skip = in.skip_bg && !(Lc[k] > eps_w);
+        vc[k] = skip ? make_float4(0.f, 0.f, 0.f, 0.f) : in.rgbs[s];
+        dc[k] = skip ? 0.f : in.delta[s];
       }
     }
 #pragma unroll
@@ -72,6 +75,7 @@ __global__ void k_composite_fwd(CompIn in, int64_t n_rays, int n, float3 bg, flo
 
 // Q_N = bg, Q_i = ab_i c_i + (1-ab_i) Q_{i+1};  P_N = 1, P_i = (1-ab_i) P_{i+1}
 // d rgb/d ab_i = T_i (c_i - Q_{i+1});  d alpha/d ab_i = T_i P_{i+1}   (eps_t must be 0)
+template <int CH>
 __global__ void k_composite_bwd(CompIn in, const float* __restrict__ trans, int64_t n_rays, int n, float3 bg,
                                 float eps_w, const float* __restrict__ drgb, const float* __restrict__ dalpha,
                                 float4* __restrict__ dout) {
@@ -120,16 +124,24 @@ __global__ void k_composite_bwd(CompIn in, const float* __restrict__ trans, int6
 int32_t composite_fwd(const CompIn& in, int64_t n_rays, int n, const float* bg, float eps_w, float eps_t,
                       const int32_t* out_pix, float* rgb, float* alpha, float* trans, cudaStream_t st) {
   if (n_rays == 0) return FV_OK;
-  k_composite_fwd<<<(unsigned)((n_rays + 127) / 128), 128, 0, st>>>(in, n_rays, n, make_float3(bg[0], bg[1], bg[2]),
-                                                                     eps_w, eps_t, out_pix, rgb, alpha, trans);
+  const unsigned grid = (unsigned)((n_rays + 127) / 128);
+  const float3 b = make_float3(bg[0], bg[1], bg[2]);
+  if (n_rays < kFewRays)
+    k_composite_fwd<8><<<grid, 128, 0, st>>>(in, n_rays, n, b, eps_w, eps_t, out_pix, rgb, alpha, trans);
+  else
+    k_composite_fwd<1><<<grid, 128, 0, st>>>(in, n_rays, n, b, eps_w, eps_t, out_pix, rgb, alpha, trans);
   return check_launch("composite_fwd");
 }
 
 int32_t composite_bwd(const CompIn& in, const float* trans, int64_t n_rays, int n, const float* bg, float eps_w,
                       const float* drgb, const float* dalpha, float4* dout, cudaStream_t st) {
   if (n_rays == 0) return FV_OK;
-  k_composite_bwd<<<(unsigned)((n_rays + 127) / 128), 128, 0, st>>>(in, trans, n_rays, n, make_float3(bg[0], bg[1], bg[2]),
-                                                                     eps_w, drgb, dalpha, dout);
+  const unsigned grid = (unsigned)((n_rays + 127) / 128);
+  const float3 b = make_float3(bg[0], bg[1], bg[2]);
+  if (n_rays < kFewRays)
+    k_composite_bwd<8><<<grid, 128, 0, st>>>(in, trans, n_rays, n, b, eps_w, drgb, dalpha, dout);
+  else
+    k_composite_bwd<1><<<grid, 128, 0, st>>>(in, trans, n_rays, n, b, eps_w, drgb, dalpha, dout);
   return check_launch("composite_bwd");
 }
 
