@@ -308,6 +308,12 @@ int main() {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   long long* d;
   cudaMalloc(&d, 512 * sizeof(long long));
+  if (getenv("CONTEND")) {
+    run_contend<2>("ld only", d, nsm, 2000, 2000);
+    run_contend<1>("mma only", d, nsm, 2000, 2000);
+    run_contend<3>("mma+ld", d, nsm, 2000, 2000);
+    return 0;
+  }
   if (getenv("TF32")) {
     run<2, 128>("f16_ts", d, nsm);
     run<3, 128>("tf32_ts", d, nsm);
