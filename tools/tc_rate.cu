@@ -308,6 +308,14 @@ int main() {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   long long* d;
   cudaMalloc(&d, 512 * sizeof(long long));
+  if (getenv("LAYER")) {
+    run_lat<16 + 11, 2, 8>("ts +ld/cvt+tmem.st", d, nsm);
+    run_lat<16 + 11, 2, 16>("ts +ld/cvt+tmem.st", d, nsm);
+    run_lat<16 + 2, 2, 8>("ts mma+wait+bar", d, nsm);
+    run_lat<16 + 2, 2, 16>("ts mma+wait+bar", d, nsm);
+    run_lat<16 + 3, 2, 8>("ts +ld/cvt (no st)", d, nsm);
+    return 0;
+  }
   if (getenv("CONTEND")) {
     run_contend<2>("ld only", d, nsm, 2000, 2000);
     run_contend<1>("mma only", d, nsm, 2000, 2000);
