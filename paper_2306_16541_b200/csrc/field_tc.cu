@@ -382,11 +382,19 @@ __global__ void __launch_bounds__(NWG * 128, 1)
   const int64_t tstep = (int64_t)gridDim.x * NWG;
   int64_t tile = (int64_t)blockIdx.x * NWG + wg;
   float4 vnext = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (tile * 128 + t < n) vnext = xf[tile * 128 + t];
+  int32_t onext = 0;                      // output slot (scatter index of the compacted stream)
+  if (tile * 128 + t < n) {
+    vnext = xf[tile * 128 + t];
+    onext = idx ? idx[tile * 128 + t] : (int32_t)(tile * 128 + t);
+  }
   for (; tile < ntiles; tile += tstep) {
     const int64_t s = tile * 128 + t;
     const float4 v = vnext;
-    if (s + tstep * 128 < n) vnext = xf[s + tstep * 128];   // prefetch the warpgroup's next tile
+    const int64_t o_s = idx ? (int64_t)onext : s;
+    if (s + tstep * 128 < n) {            // prefetch the warpgroup's next tile (input + scatter slot)
+      vnext = xf[s + tstep * 128];
+      if (idx) onext = idx[s + tstep * 128];
+    }
     const bool fg = s < n && v.w > eps_w;
     {  // hash-grid features -> A words 0..15 (4 levels = 4 words per batch)
       float xn[3]; bool msk[3];
@@ -412,7 +420,7 @@ __global__ void __launch_bounds__(NWG * 128, 1)
     if (s < n) {
       float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
       if (fg) r = make_float4(sigmoid_fast(o[0]), sigmoid_fast(o[1]), sigmoid_fast(o[2]), softplus_fast(o[3] - 1.f));
-      rgbs[idx ? (int64_t)idx[s] : s] = r;   // scatter back to the full sample layout
+      rgbs[o_s] = r;                         // scatter back to the full sample layout
     }
   }
   tc::fence_before();

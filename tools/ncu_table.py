@@ -22,7 +22,9 @@ def main(path, title=""):
     print(f"# {title}")
     print(f"# {'kernel':22s} {'us':>8s} {'rd MB':>9s} {'wr MB':>9s} {'GB/s':>7s} {'tensor%':>7s} {'L1%':>6s} {'L2%':>6s} {'DRAMcyc%':>8s}")
     for r in rows[2:]:
-        t = val(r, "gpu__time_duration.sum") / (1e3 if units[hdr.index("gpu__time_duration.sum")] == "ns" else 1.0)
+        tu = units[hdr.index("gpu__time_duration.sum")]
+        t = val(r, "gpu__time_duration.sum") * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0,
+                                                 "ms": 1e3, "msecond": 1e3}.get(tu, 1.0)
         rd, wr = mb(r, "dram__bytes_read.sum"), mb(r, "dram__bytes_write.sum")
         print(f"{r[hdr.index('Kernel Name')].split('(')[0][:22]:24s} {t:8.1f} {rd:9.1f} {wr:9.1f} {(rd + wr) / t * 1e3:7.0f} "
               f"{val(r, 'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active'):7.1f} "
