@@ -39,11 +39,16 @@ __global__ void k_composite_fwd(CompIn in, int64_t n_rays, int n, float3 bg, flo
       if (i0 + k < n) {
         const int64_t s = sidx(in, r, i0 + k, n);
         Lc[k] = in.lik[s * in.lik_stride];
-        // background samples carry sigma = 0 (abar = 0, T unchanged): with a compacted
-        // field their [c, sigma] slot was never written, so it is not read
-        const bool skip = in.skip_bg && !(Lc[k] > eps_w);
-        vc[k] = skip ? make_float4(0.f, 0.f, 0.f, 0.f) : in.rgbs[s];
-        dc[k] = skip ? 0.f : in.delta[s];
+        if (!in.skip_bg) {                 // independent loads (no wait on the likelihood)
+          vc[k] = in.rgbs[s];
+          dc[k] = in.delta[s];
+        } else {
+          // background samples carry sigma = 0 (abar = 0, T unchanged): with a compacted
+          // field their [c, sigma] slot was never written, so it is not read
+          const bool skip = !(Lc[k] > eps_w);
+          vc[k] = skip ? make_float4(0.f, 0.f, 0.f, 0.f) : in.rgbs[s];
+          dc[k] = skip ? 0.f : in.delta[s];
+        }
       }
     }
 #pragma unroll

@@ -65,7 +65,20 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
     hash_level_cell(xn, h.res[l], c);
     const float wx[2] = {1.f - c.f[0], c.f[0]}, wy[2] = {1.f - c.f[1], c.f[1]}, wz[2] = {1.f - c.f[2], c.f[2]};
     uint32_t gi[8];
-    float2 v[8];
+    float2 v[8], tv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      gi[q] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + (q >> 2), c.i0[1] + ((q >> 1) & 1),
+                                       c.i0[2] + (q & 1));
+    if (dx) {   // all 8 table loads in flight before any is consumed
+      if (h.table_half) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tv[q] = __half22float2(__ldg(reinterpret_cast<const __half2*>(h.d_table) + gi[q]));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tv[q] = __ldg(reinterpret_cast<const float2*>(h.d_table) + gi[q]);
+      }
+    }
     float px = 0.f, py = 0.f, pz = 0.f;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -74,14 +87,10 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int q = a * 4 + b * 2 + cc;
-          gi[q] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + a, c.i0[1] + b, c.i0[2] + cc);
           const float wgt = wx[a] * wy[b] * wz[cc];
           v[q] = make_float2(wgt * g0, wgt * g1);
           if (dx) {
-            float2 t;
-            if (h.table_half) t = __half22float2(__ldg(reinterpret_cast<const __half2*>(h.d_table) + gi[q]));
-            else t = __ldg(reinterpret_cast<const float2*>(h.d_table) + gi[q]);
-            const float gv = g0 * t.x + g1 * t.y;
+            const float gv = g0 * tv[q].x + g1 * tv[q].y;
             px += (a ? 1.f : -1.f) * wy[b] * wz[cc] * gv;
             py += wx[a] * (b ? 1.f : -1.f) * wz[cc] * gv;
             pz += wx[a] * wy[b] * (cc ? 1.f : -1.f) * gv;
