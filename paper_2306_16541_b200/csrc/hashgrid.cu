@@ -57,20 +57,14 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
   hash_norm(h, x[3 * p], x[3 * p + 1], x[3 * p + 2], xn, mask);
   const uint32_t maskT = (1u << h.log2_T) - 1u;
   float2* dt2 = reinterpret_cast<float2*>(dtable);
-  float gx = 0.f, gy = 0.f, gz = 0.f;
-  for (int l = 0; l < h.n_levels; ++l) {
-    const float g0 = valid ? dfeat[p * (2 * h.n_levels) + 2 * l] : 0.f;
-    const float g1 = valid ? dfeat[p * (2 * h.n_levels) + 2 * l + 1] : 0.f;
-    HashCell c;
+  // corner indices + table values of level l+1 are fetched while level l is processed
+  auto corners = [&](int l, HashCell& c, uint32_t (&gi)[8], float2 (&tv)[8]) {
     hash_level_cell(xn, h.res[l], c);
-    const float wx[2] = {1.f - c.f[0], c.f[0]}, wy[2] = {1.f - c.f[1], c.f[1]}, wz[2] = {1.f - c.f[2], c.f[2]};
-    uint32_t gi[8];
-    float2 v[8], tv[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       gi[q] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + (q >> 2), c.i0[1] + ((q >> 1) & 1),
                                        c.i0[2] + (q & 1));
-    if (dx) {   // all 8 table loads in flight before any is consumed
+    if (dx) {
       if (h.table_half) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) tv[q] = __half22float2(__ldg(reinterpret_cast<const __half2*>(h.d_table) + gi[q]));
@@ -79,6 +73,23 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
         for (int q = 0; q < 8; ++q) tv[q] = __ldg(reinterpret_cast<const float2*>(h.d_table) + gi[q]);
       }
     }
+  };
+  float gx = 0.f, gy = 0.f, gz = 0.f;
+  HashCell cn;
+  uint32_t gin[8];
+  float2 tvn[8];
+  corners(0, cn, gin, tvn);
+  for (int l = 0; l < h.n_levels; ++l) {
+    const float g0 = valid ? dfeat[p * (2 * h.n_levels) + 2 * l] : 0.f;
+    const float g1 = valid ? dfeat[p * (2 * h.n_levels) + 2 * l + 1] : 0.f;
+    const HashCell c = cn;
+    uint32_t gi[8];
+    float2 tv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { gi[q] = gin[q]; tv[q] = tvn[q]; }
+    if (l + 1 < h.n_levels) corners(l + 1, cn, gin, tvn);
+    const float wx[2] = {1.f - c.f[0], c.f[0]}, wy[2] = {1.f - c.f[1], c.f[1]}, wz[2] = {1.f - c.f[2], c.f[2]};
+    float2 v[8];
     float px = 0.f, py = 0.f, pz = 0.f;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
