@@ -21,10 +21,29 @@ __device__ __forceinline__ int seg_of(const AdamSegs& s, int64_t e) {
   return k;
 }
 
+// Both passes stream float4s (the flat buffer is 16-byte aligned; a scalar tail covers
+// n % 4); each element still picks its own segment's learning rate.
 __global__ void k_adam_check(const float* __restrict__ grad, int64_t n, AdamSegs segs, int32_t* __restrict__ flag) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    if (!isfinite(grad[e])) atomicCAS(flag, 0, 1 + seg_of(segs, e));
+  const int64_t n4 = n / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(grad);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 g = g4[i];
+    if (!(isfinite(g.x) && isfinite(g.y) && isfinite(g.z) && isfinite(g.w))) {
+      const float gv[4] = {g.x, g.y, g.z, g.w};
+      for (int k = 0; k < 4; ++k)
+        if (!isfinite(gv[k])) atomicCAS(flag, 0, 1 + seg_of(segs, 4 * i + k));
+    }
   }
+  for (int64_t e = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(grad[e])) atomicCAS(flag, 0, 1 + seg_of(segs, e));
+}
+
+__device__ __forceinline__ float adam_one(float& p, float g, float& m, float& v, float lr, float b1, float b2,
+                                          float eps, float rb1, float rb2) {
+  m = b1 * m + (1.f - b1) * g;
+  v = b2 * v + (1.f - b2) * g * g;
+  p = p - lr * (m * rb1) / (sqrtf(v * rb2) + eps);
+  return p;
 }
 
 __global__ void k_adam_update(float* __restrict__ p, const float* __restrict__ grad, float* __restrict__ m,
@@ -33,16 +52,45 @@ __global__ void k_adam_update(float* __restrict__ p, const float* __restrict__ g
                               const int32_t* __restrict__ flag) {
   if (*flag != 0) return;
   const float rb1 = 1.f / bc1, rb2 = 1.f / bc2;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const float g = grad[e];
-    const float mm = b1 * m[e] + (1.f - b1) * g;
-    const float vv = b2 * v[e] + (1.f - b2) * g * g;
-    m[e] = mm;
-    v[e] = vv;
-    const float lr = segs.lr[seg_of(segs, e)];
-    const float pn = p[e] - lr * (mm * rb1) / (sqrtf(vv * rb2) + eps);
-    p[e] = pn;
-    if (half && e >= hb && e < he) half[e - hb] = __float2half_rn(pn);
+  const int64_t n4 = n / 4;
+  const bool hvec = half && (hb % 4 == 0);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 pp = reinterpret_cast<float4*>(p)[i];
+    const float4 gg = reinterpret_cast<const float4*>(grad)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    const int64_t e = 4 * i;
+    const int s0 = seg_of(segs, e), s3 = seg_of(segs, e + 3);
+    const float l0 = segs.lr[s0];
+    const float l3 = segs.lr[s3];
+    const float l1 = s0 == s3 ? l0 : segs.lr[seg_of(segs, e + 1)];
+    const float l2 = s0 == s3 ? l0 : segs.lr[seg_of(segs, e + 2)];
+    adam_one(pp.x, gg.x, mm.x, vv.x, l0, b1, b2, eps, rb1, rb2);
+    adam_one(pp.y, gg.y, mm.y, vv.y, l1, b1, b2, eps, rb1, rb2);
+    adam_one(pp.z, gg.z, mm.z, vv.z, l2, b1, b2, eps, rb1, rb2);
+    adam_one(pp.w, gg.w, mm.w, vv.w, l3, b1, b2, eps, rb1, rb2);
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    if (half && e + 3 >= hb && e < he) {
+      if (hvec && e >= hb && e + 3 < he) {
+        const __half2 a = __floats2half2_rn(pp.x, pp.y), b = __floats2half2_rn(pp.z, pp.w);
+        uint2 u;
+        u.x = *reinterpret_cast<const uint32_t*>(&a);
+        u.y = *reinterpret_cast<const uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(half + (e - hb)) = u;
+      } else {
+        const float pv[4] = {pp.x, pp.y, pp.z, pp.w};
+        for (int k = 0; k < 4; ++k)
+          if (e + k >= hb && e + k < he) half[e + k - hb] = __float2half_rn(pv[k]);
+      }
+    }
+  }
+  for (int64_t e = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    float pe = p[e], me = m[e], ve = v[e];
+    adam_one(pe, grad[e], me, ve, segs.lr[seg_of(segs, e)], b1, b2, eps, rb1, rb2);
+    p[e] = pe; m[e] = me; v[e] = ve;
+    if (half && e >= hb && e < he) half[e - hb] = __float2half_rn(pe);
   }
 }
 
@@ -63,8 +111,12 @@ extern "C" int32_t fv_adam_step(float* d_param, const float* d_grad, float* d_m,
   const float bc1 = (float)(1.0 - pow((double)beta1, step));
   const float bc2 = (float)(1.0 - pow((double)beta2, step));
   cudaStream_t st = (cudaStream_t)stream;
-  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
   if (n == 0) return FV_OK;
+  if ((reinterpret_cast<uintptr_t>(d_param) | reinterpret_cast<uintptr_t>(d_grad) | reinterpret_cast<uintptr_t>(d_m) |
+       reinterpret_cast<uintptr_t>(d_v)) & 15)
+    return set_error(FV_EDIM, "fv_adam_step: buffers must be 16-byte aligned");
+  if (d_half && (reinterpret_cast<uintptr_t>(d_half) & 7)) return set_error(FV_EDIM, "fv_adam_step: fp16 copy must be 8-byte aligned");
+  const int grid = (int)std::min<int64_t>((n / 4 + 255) / 256 + 1, 148 * 8);
   k_adam_check<<<grid, 256, 0, st>>>(d_grad, n, s, d_flag);
   k_adam_update<<<grid, 256, 0, st>>>(d_param, d_grad, d_m, d_v, n, s, beta1, beta2, eps, bc1, bc2, (__half*)d_half,
                                       half_begin, half_end, d_flag);

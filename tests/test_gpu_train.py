@@ -239,9 +239,10 @@ def test_full_step_gradients_match_oracle(precision):
         _close(got, ref, bound, name, norm=True)
 
 
-def test_adam_matches_oracle_and_flags_nonfinite():
+@pytest.mark.parametrize("n0,n1", [(1000, 700), (1001, 702), (3, 6)])
+def test_adam_matches_oracle_and_flags_nonfinite(n0, n1):
+    """Segment boundaries and the fp16 range end off the 4-element vector grid, scalar tail."""
     rng = np.random.default_rng(4)
-    n0, n1 = 1000, 700
     p = rng.normal(size=n0 + n1).astype(np.float32)
     grads = [rng.normal(size=n0 + n1).astype(np.float32) for _ in range(3)]
     lib = _lib.load()
@@ -262,7 +263,7 @@ def test_adam_matches_oracle_and_flags_nonfinite():
     assert np.array_equal(half.cpu().numpy(), out[:n0].astype(np.float16))
     assert flag.item() == 0
     bad = grads[0].copy()
-    bad[n0 + 5] = np.nan
+    bad[n0 + min(5, n1 - 1)] = np.nan
     before = pt.clone()
     _lib.check(lib.fv_adam_step(pt.data_ptr(), _t(bad).data_ptr(), m.data_ptr(), v.data_ptr(), n0 + n1, ends, lrs,
                                 2, 4, 0.9, 0.99, 1e-8, None, 0, 0, flag.data_ptr(), _lib.stream_ptr()))
