@@ -3,6 +3,9 @@
 // The kernels are the split-precision 3xTF32 warp-specialised GEMMs of gemm_tf32x3.cu:
 // forward and dX on k_rows, dW (+ db) on k_dw.
 //
+// Layers with n_out <= 4 (the 128 -> 3 residual output and the 64 -> 4 radiance head) go to
+// the fp32 SIMT kernels of narrow_layers.cu instead: a 128-wide MMA tile would be ~97% padding.
+//
 // Why TF32x3 rather than fp16 here: the training forward must reproduce the oracle's
 // float32 x_final (it picks the hash cells the gradient is scattered into), and dW reduces
 // over ~786K samples of gradients that are 1e-9..1e-5 in magnitude -- below fp16's normal
@@ -11,6 +14,7 @@
 #include <cuda_runtime.h>
 #include "fv_internal.h"
 #include "gemm_tf32x3.h"
+#include "narrow_layers.h"
 
 using namespace fv;
 
@@ -21,6 +25,7 @@ extern "C" int32_t fv_linear_fwd_tc(const float* d_x, int64_t ldx, const float* 
   if (m < 0 || k_in < 1 || k_in > 256 || n_out < 1 || n_out > 128 || ldx < k_in || ldy < n_out)
     return set_error(FV_EDIM, "fv_linear_fwd_tc: bad shape");
   if (m == 0) return FV_OK;
+  if (n_out <= 4 && k_in <= 128) return nl::narrow_fwd(d_x, ldx, k_in, d_w, d_b, act, d_y, ldy, m, n_out, (cudaStream_t)stream);
   g3::RowsArgs r{d_x, ldx, k_in, d_w, 1, n_out, n_out, d_b, act, nullptr, 0, d_y, ldy, m};
   return g3::rows_gemm(r, (cudaStream_t)stream);
 }
@@ -38,12 +43,20 @@ extern "C" int32_t fv_linear_bwd_tc(const float* d_x, int64_t ldx, const float* 
   cudaStream_t st = (cudaStream_t)stream;
   if (d_dx) {
     // dx[m, k] = sum_n dz[m, n] W[k, n]  : K' = n_out, N' = k_in, B(n'=k, k'=n) = W[k*n_out + n]
-    g3::RowsArgs r{d_dz, ldz, n_out, d_w, n_out, 1, k_in, nullptr, 0, d_xmask, ldx, d_dx, lddx, m};
-    if (int32_t e = g3::rows_gemm(r, st)) return e;
+    if (n_out <= 4) {
+      if (int32_t e = nl::narrow_dx(d_dz, ldz, n_out, d_w, k_in, nullptr, d_xmask, ldx, d_dx, lddx, m, st)) return e;
+    } else {
+      g3::RowsArgs r{d_dz, ldz, n_out, d_w, n_out, 1, k_in, nullptr, 0, d_xmask, ldx, d_dx, lddx, m};
+      if (int32_t e = g3::rows_gemm(r, st)) return e;
+    }
   }
   if (d_dw) {
-    g3::DwArgs3 w{d_x, ldx, k_in, d_dz, ldz, n_out, d_dw, d_db, m};
-    if (int32_t e = g3::dw_gemm(w, st)) return e;
+    if (n_out <= 4) {
+      if (int32_t e = nl::narrow_dw(d_x, ldx, k_in, d_dz, ldz, n_out, d_dw, d_db, m, st)) return e;
+    } else {
+      g3::DwArgs3 w{d_x, ldx, k_in, d_dz, ldz, n_out, d_dw, d_db, m};
+      if (int32_t e = g3::dw_gemm(w, st)) return e;
+    }
   }
   return FV_OK;
 }
@@ -57,6 +70,8 @@ extern "C" int32_t fv_linear_fwd_tc_bits(const float* d_x, int64_t ldx, const fl
   if (m < 0 || k_in < 1 || k_in > 256 || n_out < 1 || n_out > 128 || ldx < k_in || ldy < n_out)
     return set_error(FV_EDIM, "fv_linear_fwd_tc_bits: bad shape");
   if (m == 0) return FV_OK;
+  if (n_out <= 4 && k_in <= 128 && !d_relu_bits)
+    return nl::narrow_fwd(d_x, ldx, k_in, d_w, d_b, act, d_y, ldy, m, n_out, (cudaStream_t)stream);
   g3::RowsArgs r{d_x, ldx, k_in, d_w, 1, n_out, n_out, d_b, act, nullptr, 0, d_y, ldy, m};
   r.bits_out = d_relu_bits;
   return g3::rows_gemm(r, (cudaStream_t)stream);
@@ -71,13 +86,21 @@ extern "C" int32_t fv_linear_bwd_tc_bits(const float* d_x, int64_t ldx, const fl
   if (m == 0) return FV_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (d_dx) {
-    g3::RowsArgs r{d_dz, ldz, n_out, d_w, n_out, 1, k_in, nullptr, 0, nullptr, 0, d_dx, lddx, m};
-    r.bits_in = d_xmask_bits;
-    if (int32_t e = g3::rows_gemm(r, st)) return e;
+    if (n_out <= 4) {
+      if (int32_t e = nl::narrow_dx(d_dz, ldz, n_out, d_w, k_in, d_xmask_bits, nullptr, 0, d_dx, lddx, m, st)) return e;
+    } else {
+      g3::RowsArgs r{d_dz, ldz, n_out, d_w, n_out, 1, k_in, nullptr, 0, nullptr, 0, d_dx, lddx, m};
+      r.bits_in = d_xmask_bits;
+      if (int32_t e = g3::rows_gemm(r, st)) return e;
+    }
   }
   if (d_dw) {
-    g3::DwArgs3 w{d_x, ldx, k_in, d_dz, ldz, n_out, d_dw, d_db, m};
-    if (int32_t e = g3::dw_gemm(w, st)) return e;
+    if (n_out <= 4) {
+      if (int32_t e = nl::narrow_dw(d_x, ldx, k_in, d_dz, ldz, n_out, d_dw, d_db, m, st)) return e;
+    } else {
+      g3::DwArgs3 w{d_x, ldx, k_in, d_dz, ldz, n_out, d_dw, d_db, m};
+      if (int32_t e = g3::dw_gemm(w, st)) return e;
+    }
   }
   return FV_OK;
 }
