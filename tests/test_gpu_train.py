@@ -78,7 +78,9 @@ def test_linear_bwd_matches_numpy():
                                           (1000, 64, 64, 4, 0), (5000, 32, 32, 64, 1),
                                           # odd row strides: operands TMA cannot address take the
                                           # converter-loaded / direct-store paths
-                                          (1501, 39, 39, 128, 1), (777, 20, 21, 24, 1), (300, 5, 7, 9, 0)])
+                                          (1501, 39, 39, 128, 1), (777, 20, 21, 24, 1), (300, 5, 7, 9, 0),
+                                          # n_out <= 4: fp32 SIMT narrow-layer kernels (8/16/32 lanes per row)
+                                          (2000, 20, 21, 2, 1), (999, 100, 100, 1, 0)])
 def test_linear_tf32_tensor_core_layers(m, k, ld, n, act):
     """fv_linear_fwd_tc / fv_linear_bwd_tc (tcgen05 kind::tf32, split-precision 3xTF32 with
     fp32 accumulation) vs float64 numpy: ~fp32 accuracy, bar 2e-5 relative to the output scale."""
