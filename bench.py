@@ -522,11 +522,16 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if os.environ.get("FV_BENCH_SINGLE_GPU") == "1":
+        # functional check of the multi-rank code paths on a one-GPU box: every rank on
+        # device 0, gloo collectives (host-mediated; no rank's kernel waits on another's).
+        # The numbers of such a run are not measurements.
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if os.environ.get("FV_BENCH_SINGLE_GPU") == "1" else "nccl")
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

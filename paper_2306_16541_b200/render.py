@@ -284,7 +284,10 @@ class SceneRenderer:
         return self._bufs
 
     def subject_pix(self, s: int, cam: CameraModel, settings: RenderSettings, rows=None) -> torch.Tensor:
-        key = (s, cam.world_to_camera.tobytes(), cam.width, cam.height, settings.box_min, settings.box_max, rows)
+        if rows is not None:
+            rows = tuple((int(a), int(b)) for a, b in rows)
+        key = (s, cam.world_to_camera.tobytes(), cam.width, cam.height, tuple(settings.box_min),
+               tuple(settings.box_max), rows)
         if key not in self._pix:
             self._pix[key] = torch.from_numpy(subject_pixels(cam, settings.box_min, settings.box_max, rows)).to(self.device)
         return self._pix[key]

@@ -68,6 +68,7 @@ def test_scene_row_sharding_reproduces_full_frame():
     for rank in range(3):                         # three "ranks", interleaved 4-row tile bands
         bands = [(y, y + 4) for y in range(4 * rank, 64, 12)]
         out, oa = r.render_scene(nets, ms, st, bg, rows=bands)
+        assert r.subject_pix(0, ms.subject_camera(0), st[0], bands).numel() >= 0   # list bands (bench path)
         for a, b in bands:
             parts[a:b] = out[a:b]
             pa[a:b] = oa[a:b]
