@@ -66,7 +66,8 @@ class Trainer:
 
     def __init__(self, nets: FreeviewModel, camera: CameraModel, target: np.ndarray, mask: np.ndarray,
                  settings: RenderSettings, n_patches: int = 6, patch: int = 32, seed: int = 0,
-                 process_group=None, precision: str = "tf32", lam_mse: float = 1.0, lam_perc: float = 0.0):
+                 process_group=None, precision: str = "tf32", lam_mse: float = 1.0, lam_perc: float = 0.0,
+                 weight_net=None):
         if precision not in ("tf32", "fp32"):
             raise ValueError("precision must be 'tf32' (tcgen05 kind::tf32 layers) or 'fp32' (SIMT, strict parity)")
         self.tc = precision == "tf32"
@@ -139,6 +140,15 @@ class Trainer:
         self.residual = bool(nets.offset_enabled)
         self.bg = (C.c_float * 3)(*settings.background)
         self.table_elems = nets.views["table"].numel()
+        # optional canonical weight-volume generator (weightnet.py): W^c logits come from it
+        self.weight_net = weight_net
+        self._wlogits = None
+        if weight_net is not None:
+            weight_net.to(dev)
+            if tuple(weight_net().shape) != tuple(nets.views["vol_logits"].shape):
+                raise ValueError("weight-volume generator output does not match the model's W^c logits")
+            from .model import LR_OTHER
+            self.wopt = torch.optim.Adam(weight_net.parameters(), lr=LR_OTHER, betas=(0.9, 0.99), eps=1e-8)
 
     def set_schedule(self, alpha: float, residual: bool) -> None:
         """Coarse-to-fine state of one iteration: Hann window alpha of the
@@ -189,6 +199,10 @@ class Trainer:
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream())
         self.pix_events[k] = ev
+        if self.weight_net is not None:        # W^c logits of this step from the generator
+            self._wlogits = self.weight_net()
+            nets.views["vol_logits"].copy_(self._wlogits.detach())
+            nets._softmax_pack(sp)
         m, cs, w = march_struct(self.st, self.pix, None), camera_struct(self.cam), nets.warp_struct()
         h, eps = nets.hash_struct(), self.st.eps_w
         _lib.check(lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), self.R, self.xs.data_ptr(),
@@ -272,10 +286,19 @@ class Trainer:
         k1, g = self.dvol.shape[0], self.dvol.shape[1]
         _lib.check(lib.fv_softmax0_bwd(nets.vol.data_ptr(), self.dvol.data_ptr(), k1, g ** 3,
                                        G["vol_logits"].data_ptr(), sp))
+        if self._wlogits is not None:          # logits gradient -> generator parameters
+            self.wopt.zero_grad(set_to_none=False)
+            self._wlogits.backward(G["vol_logits"])
+            G["vol_logits"].zero_()            # the logits are derived: Adam must not move them
 
     def allreduce(self):
         """Sum over ranks / world of the flat gradient (the path's only exchange)."""
         self.buckets.finish()
+        if self.weight_net is not None and self.buckets.world > 1:
+            import torch.distributed as dist
+            for p in self.weight_net.parameters():
+                dist.all_reduce(p.grad, group=self.pg)
+                p.grad.mul_(1.0 / self.buckets.world)
 
     def optimizer_step(self):
         nets = self.nets
@@ -287,6 +310,8 @@ class Trainer:
                                          self.table_elems if half is not None else 0, self.flag.data_ptr(),
                                          _lib.stream_ptr()), "fv_adam_step")
         nets.refresh_after_step()
+        if self.weight_net is not None:
+            self.wopt.step()
 
     def check_finite(self):
         """Raise TrainingError naming the block if the last Adam pass saw a non-finite gradient."""

@@ -220,6 +220,15 @@ def main():
     g["pl_dr"] = grads(lambda r: patch_loss(r, ad.Tensor(pt))[0], ad.Tensor(pr.copy()))[0]
     g["pl_offset_loss"] = patch_loss(ad.Tensor(pt + 0.1), ad.Tensor(pt))[0].data   # S:502 known answer
 
+    # --- conv_transpose3d (ad:633-699), the weight-volume generator's layer
+    cx = rng.normal(size=(3, 4, 4, 4))
+    cw = rng.normal(size=(3, 2, 4, 4, 4))
+    cup = rng.normal(size=(2, 8, 8, 8))
+    g["ct_x"], g["ct_w"], g["ct_up"] = cx, cw, cup
+    g["ct_out"] = ad.conv_transpose3d(ad.Tensor(cx), ad.Tensor(cw), 2, 1).data
+    g["ct_dx"], g["ct_dw"] = grads(lambda a, b: ad.tsum(ad.mul(ad.conv_transpose3d(a, b, 2, 1), ad.Tensor(cup))),
+                                   ad.Tensor(cx.copy()), ad.Tensor(cw.copy()))
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT) / 1024:.1f} KiB, {len(g)} arrays)")
 

@@ -150,3 +150,27 @@ def test_patch_loss_matches_reference_composition():
     off = oloss.patch_loss(t + 0.1, t)
     assert abs(off[0] - float(G["pl_offset_loss"])) < 1e-15 and abs(off[0] - 0.002) < 1e-12 and off[2] < 1e-12
     assert abs(oloss.patch_loss(G["pl_r"], t)[0] - oloss.patch_loss(t, G["pl_r"])[0]) < 1e-12
+
+
+def test_weight_volume_generator_layer_matches_reference():
+    """The generator's transposed convolution (torch/cuDNN) is the reference's
+    conv_transpose3d (ad:633-699): values and both gradients."""
+    import torch
+    x = torch.tensor(G["ct_x"][None], requires_grad=True)
+    w = torch.tensor(G["ct_w"], requires_grad=True)
+    out = torch.nn.functional.conv_transpose3d(x, w, stride=2, padding=1)
+    assert np.max(np.abs(out[0].detach().numpy() - G["ct_out"])) < 1e-12
+    (out[0] * torch.tensor(G["ct_up"])).sum().backward()
+    assert np.max(np.abs(x.grad[0].numpy() - G["ct_dx"])) < 1e-12
+    assert np.max(np.abs(w.grad.numpy() - G["ct_dw"])) < 1e-12
+
+
+def test_weight_volume_generator_shape_and_softmax():
+    import torch
+    from paper_2306_16541_b200.weightnet import WeightVolumeNet
+    net = WeightVolumeNet(25, seed=3)
+    logits = net()
+    assert tuple(logits.shape) == (25, 32, 32, 32)                      # S:295-296 known answer
+    wc = torch.softmax(logits, 0)
+    assert float((wc.sum(0) - 1).abs().max()) < 1e-6
+    assert torch.equal(WeightVolumeNet(25, seed=3)(), logits)             # constant latent: deterministic
