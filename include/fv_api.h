@@ -129,6 +129,10 @@ int32_t fv_warp_fwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t 
 /* d x_skel (n,3) -> d W^c (C,G,G,G) fp32 (accumulated, atomics).  ad:775-789 + Eq 9. */
 int32_t fv_warp_bwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
                     const float* d_dxskel, float* d_dvol, void* stream);
+/* fv_warp_bwd that also accumulates dL/dG_i (the gradient into the motion bases, for pose
+ * refinement) into d_dg [K][12] = (R row-major, t); d_dvol may be NULL. */
+int32_t fv_warp_bwd_g(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
+                      const float* d_dxskel, float* d_dvol, float* d_dg, void* stream);
 
 /* ---- hash grid (builder-defined; PARITY UNPINNED) ------------------------------------- */
 

@@ -216,3 +216,26 @@ def skeleton_warp_bwd(warp, d_xskel, vol_shape, box_min, box_max, dtype=np.float
     dvol = np.zeros(vol_shape, dtype=dtype)
     dvol[:k] = dvol_k
     return dvol
+
+
+def skeleton_warp_bwd_g(warp, x, d_xskel, vol, box_min, box_max):
+    """d x_skel (N,3) -> (d G_r (K,3,3), d G_t (K,3)): the gradient into the motion bases
+    (SURVEY §8a A4).  With p_i = G_i(x) = R_i x + t_i, x_skel = sum_i (w_i / L) p_i and
+    w_i = trilinear(W^c_i, p_i) (``ad:728-808``):
+    ``dL/dp_i = (w_i / L) g + dw_i * dw_i/dp_i`` with ``dw_i = <g, p_i - x_skel> / L``, then
+    ``dR_i = sum_n dp_i x^T`` and ``dt_i = sum_n dp_i`` (float64; pinned to the reference's
+    Tape through ``bmm`` / ``sample_bone_channels`` / ``weighted_sum0``, golden ``wg_*``)."""
+    fg = warp["fg"]
+    lik = np.where(fg, warp["L"], 1.0).astype(np.float64)
+    p = warp["p"].astype(np.float64)
+    xs = warp["x_skel"].astype(np.float64)
+    w = warp["w"].astype(np.float64)
+    g = np.asarray(d_xskel, np.float64) * fg[:, None]
+    dw = np.einsum("nd,knd->kn", g, p - xs[None]) / lik[None]
+    k = p.shape[0]
+    vol = np.asarray(vol, np.float64)
+    _, dpts = sample_bone_channels_bwd((k,) + vol.shape[1:], p, box_min, box_max, dw, dtype=np.float64,
+                                       vol=vol[:k])
+    dp = (w / lik[None])[:, :, None] * g[None] + dpts
+    xx = np.asarray(x, np.float64)
+    return np.einsum("kna,nb->kab", dp, xx), dp.sum(axis=1)

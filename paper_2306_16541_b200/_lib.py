@@ -74,6 +74,7 @@ SIGNATURES = {
     "fv_warp_pack": (i32, [vp, i32, P(FvWarp), vp, vp]),
     "fv_warp_fwd": (i32, [P(FvWarp), f32, vp, i64, vp, vp, vp, vp, vp]),
     "fv_warp_bwd": (i32, [P(FvWarp), f32, vp, i64, vp, vp, vp]),
+    "fv_warp_bwd_g": (i32, [P(FvWarp), f32, vp, i64, vp, vp, vp, vp]),
     "fv_hash_fwd": (i32, [P(FvHash), vp, i64, vp, vp, vp]),
     "fv_hash_bwd": (i32, [P(FvHash), vp, i64, vp, vp, vp, vp]),
     "fv_linear_fwd": (i32, [vp, vp, vp, vp, i64, i32, i32, i32, vp]),

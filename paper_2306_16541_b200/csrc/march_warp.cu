@@ -154,11 +154,21 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
 // dL/dx_skel . (G_i(x) - x_skel) / L.  Warp-aggregated like k_hash_bwd: lanes sharing a
 // bone cell (a warp = 32 neighbouring rays at one depth, ~8 rays per 1/32-box cell) sum
 // their 8 corner terms in shared memory and the group's lowest lane issues the atomics.
+// With WANT_G the kernel also returns dL/dG_i (oracle.warp.skeleton_warp_bwd_g):
+// dL/dp_i = (w_i / L) g + dw_i * dw_i/dp_i (trilinear gradient of the bone's W^c channel),
+// dR_i += dp_i x^T, dt_i += dp_i, reduced over the warp by shuffles, over the block in shared
+// memory and over the grid with one atomicAdd per (bone, entry) per block.
+template <bool WANT_G>
 __global__ void __launch_bounds__(128) k_warp_bwd(fv_warp w, float eps_w, const float* __restrict__ x, int64_t n,
-                                                  const float* __restrict__ dxs, float* __restrict__ dvol) {
+                                                  const float* __restrict__ dxs, float* __restrict__ dvol,
+                                                  float* __restrict__ dg) {
   __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
   __shared__ float scratch[4][8][33];
-  for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
+  __shared__ float sdg[WANT_G ? FV_MAX_BONES * 12 : 1];
+  for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) {
+    sg[i] = w.d_g[i];
+    if (WANT_G) sdg[i] = 0.f;
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -166,7 +176,11 @@ __global__ void __launch_bounds__(128) k_warp_bwd(fv_warp w, float eps_w, const 
   const int64_t q = live ? q0 : n - 1;
   const float g0 = dxs[3 * q], g1 = dxs[3 * q + 1], g2 = dxs[3 * q + 2];
   live = live && !(g0 == 0.f && g1 == 0.f && g2 == 0.f);
-  if (!__any_sync(0xffffffffu, live)) return;
+  if (!__any_sync(0xffffffffu, live)) {
+    if (WANT_G) goto flush;            // every block still publishes its (partial) dG
+    return;
+  }
+  {
   const float x0 = x[3 * q], x1 = x[3 * q + 1], x2 = x[3 * q + 2];
   float xsk[3];
   const float L = warp_point<false>(w, sg, eps_w, x0, x1, x2, xsk);
@@ -179,7 +193,38 @@ __global__ void __launch_bounds__(128) k_warp_bwd(fv_warp w, float eps_w, const 
     int i0[3]; float f[3];
     const bool in = warp_cell(w, p, i0, f);
     const float dw = (g0 * (p[0] - xsk[0]) + g1 * (p[1] - xsk[1]) + g2 * (p[2] - xsk[2])) * invL;
-    const bool any = live && in && dw != 0.f;
+    if (WANT_G) {
+      float dp[3] = {0.f, 0.f, 0.f};
+      if (live && in) {
+        float cv[8];
+        load_corners(w.d_vol_packed, w.vol_half, vol_cell_index(i, G, i0), cv);
+        const float wi = trilerp8(f, cv);
+        const float gy0 = 1.f - f[1], gz0 = 1.f - f[2];
+        // trilinear gradient in grid units (corner order a*4 + b*2 + c = x, y, z)
+        const float dfx = gy0 * gz0 * (cv[4] - cv[0]) + gy0 * f[2] * (cv[5] - cv[1]) +
+                          f[1] * gz0 * (cv[6] - cv[2]) + f[1] * f[2] * (cv[7] - cv[3]);
+        const float gx0 = 1.f - f[0];
+        const float dfy = gx0 * gz0 * (cv[2] - cv[0]) + gx0 * f[2] * (cv[3] - cv[1]) +
+                          f[0] * gz0 * (cv[6] - cv[4]) + f[0] * f[2] * (cv[7] - cv[5]);
+        const float dfz = gx0 * gy0 * (cv[1] - cv[0]) + gx0 * f[1] * (cv[3] - cv[2]) +
+                          f[0] * gy0 * (cv[5] - cv[4]) + f[0] * f[1] * (cv[7] - cv[6]);
+        const float a = wi * invL;
+        dp[0] = a * g0 + dw * dfx * w.wscale[0];
+        dp[1] = a * g1 + dw * dfy * w.wscale[1];
+        dp[2] = a * g2 + dw * dfz * w.wscale[2];
+      }
+      float v[12] = {dp[0] * x0, dp[0] * x1, dp[0] * x2, dp[1] * x0, dp[1] * x1, dp[1] * x2,
+                     dp[2] * x0, dp[2] * x1, dp[2] * x2, dp[0], dp[1], dp[2]};
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < 12; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+      if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < 12; ++j) atomicAdd(&sdg[12 * i + j], v[j]);
+      }
+    }
+    const bool any = live && in && dw != 0.f && dvol != nullptr;
     const float wx[2] = {1.f - f[0], f[0]}, wy[2] = {1.f - f[1], f[1]}, wz[2] = {1.f - f[2], f[2]};
     float v[8];
 #pragma unroll
@@ -212,6 +257,13 @@ __global__ void __launch_bounds__(128) k_warp_bwd(fv_warp w, float eps_w, const 
         atomicAdd(dvol + (((int64_t)i * G + vx) * G + vy) * G + vz, v[c]);
       }
     }
+  }
+  }
+flush:
+  if (WANT_G) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < w.n_bones * 12; j += blockDim.x)
+      if (sdg[j] != 0.f) atomicAdd(dg + j, sdg[j]);
   }
 }
 
@@ -258,8 +310,21 @@ extern "C" int32_t fv_warp_bwd(const fv_warp* warp, float eps_w, const float* d_
   if (!warp || n < 0) return set_error(FV_EDIM, "fv_warp_bwd: bad arguments");
   if (int32_t e = check_warp(warp)) return e;
   if (n == 0) return FV_OK;
-  k_warp_bwd<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*warp, eps_w, d_x, n, d_dxskel, d_dvol);
+  k_warp_bwd<false><<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*warp, eps_w, d_x, n, d_dxskel,
+                                                                                    d_dvol, nullptr);
   return check_launch("fv_warp_bwd");
+}
+
+// fv_warp_bwd that also accumulates dL/dG_i into d_dg [K][12] (R row-major, t); d_dvol may
+// be NULL (no volume gradient).
+extern "C" int32_t fv_warp_bwd_g(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
+                                 const float* d_dxskel, float* d_dvol, float* d_dg, void* stream) {
+  if (!warp || n < 0 || !d_dg) return set_error(FV_EDIM, "fv_warp_bwd_g: bad arguments");
+  if (int32_t e = check_warp(warp)) return e;
+  if (n == 0) return FV_OK;
+  k_warp_bwd<true><<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*warp, eps_w, d_x, n, d_dxskel,
+                                                                                   d_dvol, d_dg);
+  return check_launch("fv_warp_bwd_g");
 }
 
 extern "C" int32_t fv_march_warp(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays,

@@ -229,6 +229,31 @@ def main():
     g["ct_dx"], g["ct_dw"] = grads(lambda a, b: ad.tsum(ad.mul(ad.conv_transpose3d(a, b, 2, 1), ad.Tensor(cup))),
                                    ad.Tensor(cx.copy()), ad.Tensor(cw.copy()))
 
+    # --- gradients into the motion bases and the pose (A4: dL/dG_i of the skinning warp,
+    # chained through motion_basis to the joint angles) -- the reference's own Tape
+    xf = xw[fgm]
+    mf = xf.shape[0]
+
+    def warp_g(rr, tt):
+        xk = ad.Tensor(np.broadcast_to(xf, (K, mf, 3)).copy())
+        pts = ad.add(ad.bmm(xk, ad.transpose_last2(rr)), ad.bmm(ad.Tensor(np.ones((K, mf, 1))), tt))
+        v = ad.Tensor(ad.softmax0(ad.Tensor(logits)).data)
+        w = ad.sample_bone_channels(v, pts, bmin, bmax)
+        L = ad.sum0(w)
+        wn = ad.div(w, ad.stack0([L] * K))
+        return ad.weighted_sum0(wn, pts)
+
+    g["wg_dgr"], g["wg_dgt"] = grads(lambda rr, tt: ad.tsum(ad.mul(warp_g(rr, tt), ad.Tensor(upx))),
+                                     ad.Tensor(grw.copy()), ad.Tensor(gtw.reshape(K, 1, 3).copy()))
+    ugr, ugt = rng.normal(size=(24, 3, 3)), rng.normal(size=(24, 3))
+
+    def mb_loss(a, r0):
+        gr__, gt__ = sk.motion_basis(skel, a, r0)
+        return ad.add(ad.tsum(ad.mul(gr__, ad.Tensor(ugr))), ad.tsum(ad.mul(gt__, ad.Tensor(ugt))))
+
+    g["mb_ugr"], g["mb_ugt"] = ugr, ugt
+    g["mb_dang"], g["mb_droot"] = grads(mb_loss, ad.Tensor(ang.copy()), ad.Tensor(root.copy()))
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT) / 1024:.1f} KiB, {len(g)} arrays)")
 

@@ -190,6 +190,32 @@ def test_warp_bwd_matches_oracle():
     _close(dvol.cpu().numpy(), ref, 1e-4, "dvol")
 
 
+@pytest.mark.parametrize("half", [False, True])
+def test_warp_bwd_motion_basis_gradient_matches_oracle(half):
+    """fv_warp_bwd_g: dL/dG_i (A4) vs the oracle's float64 restatement (itself pinned to the
+    reference Tape, golden wg_*), plus the unchanged volume gradient."""
+    sc = make("c2" if half else "c1", width=16, height=16)
+    nets = FreeviewModel(sc)
+    osc = oracle_scene(sc, nets=nets)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1.0, 1.0, (4000, 3)).astype(np.float32)
+    g = rng.normal(size=(4000, 3)).astype(np.float32)
+    wr = owarp.skeleton_warp(x, osc["g_r"], osc["g_t"], osc["vol"], osc["wbox_min"], osc["wbox_max"], 1e-4,
+                             np.float32)
+    ref_r, ref_t = owarp.skeleton_warp_bwd_g(wr, x, g * wr["fg"][:, None], osc["vol"], osc["wbox_min"],
+                                             osc["wbox_max"])
+    ref_v = owarp.skeleton_warp_bwd(wr, g * wr["fg"][:, None], osc["vol"].shape, osc["wbox_min"], osc["wbox_max"])
+    dvol = torch.zeros_like(nets.vol)
+    dg = torch.zeros((sc.cfg.n_bones, 12), device=DEV)
+    w = nets.warp_struct()
+    _lib.check(nets.lib.fv_warp_bwd_g(C.byref(w), 1e-4, _t(x).data_ptr(), 4000, _t(g).data_ptr(), dvol.data_ptr(),
+                                      dg.data_ptr(), _lib.stream_ptr()))
+    got = dg.cpu().numpy().astype(np.float64)
+    _close(got[:, :9].reshape(-1, 3, 3), ref_r, 1e-4, "dG_r")
+    _close(got[:, 9:], ref_t, 1e-4, "dG_t")
+    _close(dvol.cpu().numpy(), ref_v, 1e-4, "dvol")
+
+
 @pytest.mark.parametrize("precision", ["fp32", "tf32"])
 def test_full_step_gradients_match_oracle(precision):
     """Whole-step gradients vs the oracle's float64 backward on the same inputs.

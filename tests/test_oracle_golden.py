@@ -174,3 +174,15 @@ def test_weight_volume_generator_shape_and_softmax():
     wc = torch.softmax(logits, 0)
     assert float((wc.sum(0) - 1).abs().max()) < 1e-6
     assert torch.equal(WeightVolumeNet(25, seed=3)(), logits)             # constant latent: deterministic
+
+
+def test_warp_gradient_into_motion_bases():
+    """dL/dG_i of the skinning warp (A4) vs the reference Tape (golden wg_*)."""
+    K = G["wp_gr"].shape[0]
+    vol = owarp.softmax0(G["wp_logits"])
+    xf = G["wp_x"][G["wp_fg"]]
+    wr = owarp.skeleton_warp(xf, G["wp_gr"], G["wp_gt"], vol, BMIN, BMAX, 1e-4, np.float64)
+    assert wr["fg"].all()
+    dgr, dgt = owarp.skeleton_warp_bwd_g(wr, xf, G["wp_up"], vol, BMIN, BMAX)
+    assert np.max(np.abs(dgr - G["wg_dgr"])) < 1e-10
+    assert np.max(np.abs(dgt - G["wg_dgt"].reshape(K, 3))) < 1e-10
