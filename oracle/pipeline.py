@@ -128,6 +128,13 @@ def loss_and_grads(scene, cc, pix, width, settings, target, dtype=np.float32, pa
     d_xskel_valid[wr["fg"]] = dxs
     grads["vol"] = warp.skeleton_warp_bwd(wr, d_xskel_valid, np.asarray(scene["vol"]).shape,
                                           scene["wbox_min"], scene["wbox_max"])
+    # motion bases (A4) and the pose vector through the residual MLP's first layer
+    x_valid = r["x"].reshape(-1, 3)[r["flat"]]
+    grads["g_r"], grads["g_t"] = warp.skeleton_warp_bwd_g(wr, x_valid, d_xskel_valid, scene["vol"],
+                                                          scene["wbox_min"], scene["wbox_max"])
+    if settings.get("offset_enabled", True):
+        npe = f["pe"].shape[1]
+        grads["pose_vec"] = np.asarray(scene["off_w"][0], np.float64)[npe:] @ grads["off_b"][0]
     return loss, grads, r
 
 

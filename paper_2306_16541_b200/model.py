@@ -172,6 +172,14 @@ class FreeviewModel:
         self._pose = pose
         self._fold_pose(_lib.stream_ptr(stream))
 
+    def set_pose_bases(self, g_r: np.ndarray, g_t: np.ndarray, pose_vec: np.ndarray, stream=None) -> None:
+        """Upload given motion bases and pose vector (e.g. of a refined pose) and fold the
+        pose into the residual bias; the refined pose is remembered for refresh()."""
+        self.g.copy_(torch.from_numpy(pack_g(np.asarray(g_r), np.asarray(g_t))), non_blocking=False)
+        self.pose_dev.copy_(torch.from_numpy(np.asarray(pose_vec, np.float32).reshape(-1)))
+        self._pose = Pose(np.asarray(pose_vec, np.float64).reshape(-1, 3), np.zeros(3))
+        self._fold_pose(_lib.stream_ptr(stream))
+
     def _fold_pose(self, st) -> None:
         f = self.field_struct()
         _lib.check(self.lib.fv_offset_bias(C.byref(f), self.pose_dev.data_ptr(), 3 * self.n_bones,

@@ -67,7 +67,7 @@ class Trainer:
     def __init__(self, nets: FreeviewModel, camera: CameraModel, target: np.ndarray, mask: np.ndarray,
                  settings: RenderSettings, n_patches: int = 6, patch: int = 32, seed: int = 0,
                  process_group=None, precision: str = "tf32", lam_mse: float = 1.0, lam_perc: float = 0.0,
-                 weight_net=None):
+                 weight_net=None, pose_refiner=None, pose=None):
         if precision not in ("tf32", "fp32"):
             raise ValueError("precision must be 'tf32' (tcgen05 kind::tf32 layers) or 'fp32' (SIMT, strict parity)")
         self.tc = precision == "tf32"
@@ -140,6 +140,18 @@ class Trainer:
         self.residual = bool(nets.offset_enabled)
         self.bg = (C.c_float * 3)(*settings.background)
         self.table_elems = nets.views["table"].numel()
+        # optional pose refiner (pose.py): per step the frame's pose is refined, its motion bases
+        # uploaded, and dL/dG_i (fv_warp_bwd_g) plus the residual MLP's pose-input gradient are
+        # chained to the refiner on the host
+        self.pose_refiner = pose_refiner
+        if pose_refiner is not None:
+            if pose is None:
+                raise ValueError("a pose refiner needs the frame's pose")
+            from .model import LR_OTHER
+            self.base_pose = pose
+            self.dg = torch.zeros((nets.n_bones, 12), device=dev, dtype=torch.float32)
+            self.popt = torch.optim.Adam(pose_refiner.parameters(), lr=LR_OTHER, betas=(0.9, 0.99), eps=1e-8)
+            self._refined = None
         # optional canonical weight-volume generator (weightnet.py): W^c logits come from it
         self.weight_net = weight_net
         self._wlogits = None
@@ -199,6 +211,14 @@ class Trainer:
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream())
         self.pix_events[k] = ev
+        if self.pose_refiner is not None:     # refined pose -> motion bases of this step
+            from .pose import motion_basis as mb_t
+            om = torch.as_tensor(self.base_pose.angles, dtype=torch.float64)
+            refined = self.pose_refiner.refine(om)
+            g_r, g_t = mb_t(nets.scene.skeleton, refined,
+                            torch.as_tensor(self.base_pose.root_translation, dtype=torch.float64))
+            self._refined = (refined, g_r, g_t)
+            nets.set_pose_bases(g_r.detach().numpy(), g_t.detach().numpy(), refined.detach().numpy().reshape(-1))
         if self.weight_net is not None:        # W^c logits of this step from the generator
             self._wlogits = self.weight_net()
             nets.views["vol_logits"].copy_(self._wlogits.detach())
@@ -281,11 +301,25 @@ class Trainer:
             _lib.check(lib.fv_posenc_bwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.dpe.data_ptr(),
                                          self.pe_ld, self.dxs.data_ptr(), sp))
         w = nets.warp_struct()
-        _lib.check(lib.fv_warp_bwd(C.byref(w), eps, self.x.data_ptr(), S, self.dxs.data_ptr(), self.dvol.data_ptr(), sp),
-                   "fv_warp_bwd")
+        if self.pose_refiner is not None:
+            self.dg.zero_()
+            _lib.check(lib.fv_warp_bwd_g(C.byref(w), eps, self.x.data_ptr(), S, self.dxs.data_ptr(),
+                                         self.dvol.data_ptr(), self.dg.data_ptr(), sp), "fv_warp_bwd_g")
+        else:
+            _lib.check(lib.fv_warp_bwd(C.byref(w), eps, self.x.data_ptr(), S, self.dxs.data_ptr(),
+                                       self.dvol.data_ptr(), sp), "fv_warp_bwd")
         k1, g = self.dvol.shape[0], self.dvol.shape[1]
         _lib.check(lib.fv_softmax0_bwd(nets.vol.data_ptr(), self.dvol.data_ptr(), k1, g ** 3,
                                        G["vol_logits"].data_ptr(), sp))
+        if self.pose_refiner is not None:     # dL/dG_i and the pose input -> refiner parameters
+            refined, g_r, g_t = self._refined
+            dg = self.dg.double().cpu()
+            d_pose = torch.zeros(refined.numel(), dtype=torch.float64)
+            if self.residual:                   # b0_eff = b0 + pose @ W0[D:]: d pose = W0[D:] @ d b0_eff
+                d_pose = (V["off_w0"][self.d_pe:].double() @ G["off_b0"].double()).cpu()
+            self.popt.zero_grad(set_to_none=False)
+            ((g_r * dg[:, :9].view(-1, 3, 3)).sum() + (g_t * dg[:, 9:]).sum()
+             + (refined.reshape(-1) * d_pose).sum()).backward()
         if self._wlogits is not None:          # logits gradient -> generator parameters
             self.wopt.zero_grad(set_to_none=False)
             self._wlogits.backward(G["vol_logits"])
@@ -294,11 +328,13 @@ class Trainer:
     def allreduce(self):
         """Sum over ranks / world of the flat gradient (the path's only exchange)."""
         self.buckets.finish()
-        if self.weight_net is not None and self.buckets.world > 1:
+        if self.buckets.world > 1:
             import torch.distributed as dist
-            for p in self.weight_net.parameters():
-                dist.all_reduce(p.grad, group=self.pg)
-                p.grad.mul_(1.0 / self.buckets.world)
+            nets_ = [m for m in (self.weight_net, self.pose_refiner) if m is not None]
+            for m in nets_:
+                for p in m.parameters():
+                    dist.all_reduce(p.grad, group=self.pg)
+                    p.grad.mul_(1.0 / self.buckets.world)
 
     def optimizer_step(self):
         nets = self.nets
@@ -312,6 +348,8 @@ class Trainer:
         nets.refresh_after_step()
         if self.weight_net is not None:
             self.wopt.step()
+        if self.pose_refiner is not None:
+            self.popt.step()
 
     def check_finite(self):
         """Raise TrainingError naming the block if the last Adam pass saw a non-finite gradient."""

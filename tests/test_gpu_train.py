@@ -449,3 +449,40 @@ def test_weight_volume_generator_training_chain():
     losses = [tr.step(i).item() for i in range(60)]
     assert not torch.equal(net.z.detach(), z0)
     assert np.mean(losses[-10:]) < np.mean(losses[:10])
+
+
+def test_pose_refiner_chain_matches_oracle():
+    """Training step with the pose refiner (fp32 layers): the motion-basis gradient
+    (fv_warp_bwd_g over the whole step) and the residual MLP's pose-input gradient match the
+    oracle's float64 backward on the same inputs; the refiner starts at the identity and
+    its parameters train."""
+    from paper_2306_16541_b200.pose import PoseRefinerNet
+    sc = make("c1", width=48, height=48, n_samples=24, table_scale=0.5, bias_scale=0.05, background=(0.1, 0.3, 0.8))
+    nets = FreeviewModel(sc)
+    target, mask = target_image(sc)
+    st = RenderSettings.from_config(sc.cfg, seed=5)
+    ref_net = PoseRefinerNet(sc.cfg.n_bones, seed=4)
+    tr = Trainer(nets, sc.camera, target, mask, st, n_patches=2, patch=16, seed=3, precision="fp32",
+                 pose_refiner=ref_net, pose=sc.poses[0])
+    pix = patch_pixels(sample_patches(mask, 2, 16, 3, 0), 16, 48)
+    tr.forward(pix)
+    refined = tr._refined[0].detach().numpy()
+    assert np.array_equal(refined, sc.poses[0].angles)            # zero last layer: identity
+    tr.backward()
+    torch.cuda.synchronize()
+    osc = oracle_scene(sc, nets=nets)
+    cc = ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera)
+    _, og, _ = opipe.loss_and_grads(osc, cc, pix, 48, osettings(sc.cfg, seed=5), target.reshape(-1, 3)[pix])
+    dg = tr.dg.cpu().numpy().astype(np.float64)
+    for name, got, ref in [("dG_r", dg[:, :9].reshape(-1, 3, 3), og["g_r"]), ("dG_t", dg[:, 9:], og["g_t"])]:
+        fro = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+        print(f"{name}: |ref| {np.abs(ref).max():.3e} frobenius {fro:.2e}")
+        assert np.abs(got - ref).max() <= 1e-3 and fro < 2e-2
+    d_pose = (nets.views["off_w0"][tr.d_pe:].double() @ tr.gviews["off_b0"].double()).cpu().numpy()
+    fro = np.linalg.norm(d_pose - og["pose_vec"]) / np.linalg.norm(og["pose_vec"])
+    print(f"d pose: frobenius {fro:.2e}")
+    assert fro < 2e-2
+    p0 = [p.detach().clone() for p in ref_net.parameters()]
+    for i in range(5):
+        tr.step(i)
+    assert any(not torch.equal(a, b.detach()) for a, b in zip(p0, ref_net.parameters()))

@@ -186,3 +186,37 @@ def test_warp_gradient_into_motion_bases():
     dgr, dgt = owarp.skeleton_warp_bwd_g(wr, xf, G["wp_up"], vol, BMIN, BMAX)
     assert np.max(np.abs(dgr - G["wg_dgr"])) < 1e-10
     assert np.max(np.abs(dgt - G["wg_dgt"].reshape(K, 3))) < 1e-10
+
+
+def test_torch_motion_basis_and_pose_gradient_match_reference():
+    """pose.motion_basis (float64 torch, used to train the pose refiner) reproduces the
+    reference's motion bases and its Tape gradient into the joint angles (golden mb_*)."""
+    import torch
+    from paper_2306_16541_b200.pose import motion_basis as mb_t
+    from paper_2306_16541_b200.skeleton import Skeleton
+    skel = Skeleton(parent=G["mb_parent"], rest_offset=G["mb_offs"], canonical_angles=np.zeros((24, 3)),
+                    canonical_root=np.zeros(3))
+    ang = torch.tensor(G["mb_ang"], requires_grad=True)
+    root = torch.tensor(G["mb_root"], requires_grad=True)
+    gr, gt = mb_t(skel, ang, root)
+    assert np.max(np.abs(gr.detach().numpy() - G["mb_gr"])) < 1e-12
+    assert np.max(np.abs(gt.detach().numpy() - G["mb_gt"])) < 1e-12
+    ((gr * torch.tensor(G["mb_ugr"])).sum() + (gt * torch.tensor(G["mb_ugt"])).sum()).backward()
+    assert np.max(np.abs(ang.grad.numpy() - G["mb_dang"])) < 1e-10
+    assert np.max(np.abs(root.grad.numpy() - G["mb_droot"])) < 1e-10
+
+
+def test_pose_refiner_known_answers():
+    """SPEC refine_pose examples: fresh net -> identity exactly; rotation
+    composition about a shared axis; joints untouched."""
+    import torch
+    from paper_2306_16541_b200.pose import PoseRefinerNet, rodrigues, rotation_log
+    net = PoseRefinerNet(24, seed=1)
+    om = torch.tensor(np.random.default_rng(0).normal(0, 0.3, (24, 3)))
+    assert torch.equal(net.refine(om), om)
+    w = torch.tensor([[0.0, 0.0, np.pi / 4]], dtype=torch.float64)
+    dw = torch.tensor([[0.0, 0.0, np.pi / 2]], dtype=torch.float64)
+    comp = rotation_log(rodrigues(dw) @ rodrigues(w))
+    assert np.max(np.abs(comp.numpy() - [[0.0, 0.0, 3 * np.pi / 4]])) < 1e-9
+    r = rodrigues(om)
+    assert float((rotation_log(r) - om).abs().max()) < 1e-12
