@@ -330,7 +330,8 @@ class Trainer:
         self.buckets.finish()
         if self.buckets.world > 1:
             import torch.distributed as dist
-            nets_ = [m for m in (self.weight_net, self.pose_refiner) if m is not None]
+            nets_ = [m for m in (getattr(self, "weight_net", None), getattr(self, "pose_refiner", None))
+                     if m is not None]
             for m in nets_:
                 for p in m.parameters():
                     dist.all_reduce(p.grad, group=self.pg)
