@@ -169,11 +169,13 @@ def test_weight_volume_generator_shape_and_softmax():
     import torch
     from paper_2306_16541_b200.weightnet import WeightVolumeNet
     net = WeightVolumeNet(25, seed=3)
-    logits = net()
+    with torch.no_grad():
+        logits = net()
     assert tuple(logits.shape) == (25, 32, 32, 32)                      # S:295-296 known answer
     wc = torch.softmax(logits, 0)
     assert float((wc.sum(0) - 1).abs().max()) < 1e-6
-    assert torch.equal(WeightVolumeNet(25, seed=3)(), logits)             # constant latent: deterministic
+    with torch.no_grad():
+        assert torch.equal(WeightVolumeNet(25, seed=3)(), logits)         # constant latent: deterministic
 
 
 def test_warp_gradient_into_motion_bases():
