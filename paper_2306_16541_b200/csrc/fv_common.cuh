@@ -188,6 +188,38 @@ __device__ __forceinline__ float warp_point(const fv_warp& w, const float* sg, f
   return lik;
 }
 
+// ---------------------------------------------------------------- warp aggregation
+// Sum v over each run of consecutive lanes holding the same key (segmented inclusive scan,
+// 5 shuffle steps); returns true on the run's last lane, which then holds the run total.
+// Lanes of one key that are not contiguous form several runs (each still correct).  The
+// backward kernels' warps are 32 neighbouring rays of a patch row at one depth, so a
+// cell's lanes are contiguous and this replaces one serial leader loop per group.
+template <int N, typename K>
+__device__ __forceinline__ bool seg_sum(float (&v)[N], K key, int lane) {
+  const K prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || prev != key);
+  if (heads == 0xffffffffu) return true;            // all runs of one (fine levels): nothing to sum
+  const int start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+  // the longest run bounds the scan depth: skip the shuffle steps no run needs
+  const unsigned tails = (heads >> 1) | 0x80000000u;
+  int longest = 1;
+  for (unsigned h = heads; h; h &= h - 1) {
+    const int s0 = __ffs(h) - 1;
+    const int e0 = __ffs(tails & (0xffffffffu << s0)) - 1;
+    longest = max(longest, e0 - s0 + 1);
+  }
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    if (d >= longest) break;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const float y = __shfl_up_sync(0xffffffffu, v[j], d);
+      if (lane - d >= start) v[j] += y;
+    }
+  }
+  return lane == 31 || ((heads >> (lane + 1)) & 1u);
+}
+
 // ---------------------------------------------------------------- hash grid
 struct HashCell { int i0[3]; float f[3]; };
 

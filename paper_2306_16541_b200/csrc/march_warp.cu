@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
 // dvol[i, corner] += trilinear weight * dL/dw_i (ad:778-789 bincount scatter); dL/dw_i =
 // dL/dx_skel . (G_i(x) - x_skel) / L.  Warp-aggregated like k_hash_bwd: lanes sharing a
 // bone cell (a warp = 32 neighbouring rays at one depth, ~8 rays per 1/32-box cell) sum
-// their 8 corner terms in shared memory and the group's lowest lane issues the atomics.
+// their 8 corner terms with a segmented shuffle scan and the run's last lane issues the
+// atomics.
 // With WANT_G the kernel also returns dL/dG_i (oracle.warp.skeleton_warp_bwd_g):
 // dL/dp_i = (w_i / L) g + dw_i * dw_i/dp_i (trilinear gradient of the bone's W^c channel),
 // dR_i += dp_i x^T, dt_i += dp_i, reduced over the warp by shuffles, over the block in shared
@@ -163,14 +164,13 @@ __global__ void __launch_bounds__(128) k_warp_bwd(fv_warp w, float eps_w, const 
                                                   const float* __restrict__ dxs, float* __restrict__ dvol,
                                                   float* __restrict__ dg) {
   __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
-  __shared__ float scratch[4][8][33];
   __shared__ float sdg[WANT_G ? FV_MAX_BONES * 12 : 1];
   for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) {
     sg[i] = w.d_g[i];
     if (WANT_G) sdg[i] = 0.f;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   bool live = q0 < n;
   const int64_t q = live ? q0 : n - 1;
@@ -230,25 +230,7 @@ __global__ void __launch_bounds__(128) k_warp_bwd(fv_warp w, float eps_w, const 
 #pragma unroll
     for (int c = 0; c < 8; ++c) v[c] = wx[c >> 2] * wy[(c >> 1) & 1] * wz[c & 1] * dw;
     const uint32_t key = any ? (uint32_t)vol_cell_index(i, G, i0) : (0xFFFFFFFFu - (uint32_t)lane);
-    const unsigned grp = __match_any_sync(0xffffffffu, key);
-    const unsigned multi = __ballot_sync(0xffffffffu, grp != (1u << lane));
-    bool lead = any;
-    if (grp != (1u << lane)) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) scratch[wib][c][lane] = v[c];
-      __syncwarp(multi);
-      lead = any && lane == __ffs(grp) - 1;
-      if (lead) {
-        unsigned rest = grp & (grp - 1);
-        while (rest) {
-          const int o = __ffs(rest) - 1;
-          rest &= rest - 1;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) v[c] += scratch[wib][c][o];
-        }
-      }
-      __syncwarp(multi);
-    }
+    const bool lead = seg_sum<8>(v, key, lane) && any;
     if (lead) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
