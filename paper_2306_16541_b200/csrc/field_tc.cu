@@ -26,6 +26,9 @@
 #include "fv_internal.h"
 #include "tc_sm100.cuh"
 
+#ifndef FV_OFF_LEAD
+#define FV_OFF_LEAD 2
+#endif
 namespace fv {
 
 // ---- weight pack layout (bytes) ------------------------------------------------------
@@ -170,17 +173,39 @@ __device__ __forceinline__ void tc_prologue_sync() {
 // epilogue's stores stall them: tools/tc_rate.cu measures 2175 vs 1743 cycles per layer.)
 // A team of 8 warps (two warpgroups) owns a 128-sample tile: warp w reads TMEM lane quadrant
 // w%4 and accumulator columns [64*(w/4%2), +64).  Biases ride in the GEMM (pack layout).
-// TMEM per team: D = columns [0, 128), A = [128, 200) (K = 144 fp16 pairs); 2 teams.
+// TMEM per team: D = columns [0, 128), A = [128, 200) (K = 144 fp16 pairs), the next
+// tile's posenc [200, 224), the last layer's accumulator [224, 240); 2 teams.
 constexpr uint32_t OF_W = PK_RAD0 - PK_OFF0;               // 126976
 constexpr uint32_t OF_B4 = OF_W;                           // off b4: 16 floats
 constexpr uint32_t OF_SMEM = OF_B4 + 64;
 constexpr uint32_t OF_TA = 128;                            // A-operand column offset in a team
+constexpr uint32_t OF_TPE = 200;                           // next tile's posenc (layer-0 A, 24 columns)
+constexpr uint32_t OF_TD4 = 224;                           // layer-4 accumulator (16 columns)
 
 // One layer of a team with A in TMEM: A stores done -> barrier -> one thread issues K/16
-// MMAs (8 A columns each) + commit -> everyone waits.
-template <int K, int N, int NTHR>
+// MMAs (8 A columns each) + commit -> `overlap()` (independent work of the waiting
+// threads) -> everyone waits.
+struct NoOverlap { __device__ __forceinline__ void operator()() const {} };
+// A batch of MMAs issued by `issue()` (one thread) with the same barrier/commit/wait protocol.
+template <typename I>
+__device__ __forceinline__ void layer_issue_ts(uint64_t* bar, uint32_t& phase, int t, int grp, I&& issue) {
+  tc::tmem_st_wait();
+  tc::fence_before();
+  named_bar(1 + grp, 256);
+  if (t == 0) {
+    tc::fence_after();
+    issue();
+    tc::mma_commit(bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(bar, phase);
+  phase ^= 1u;
+  tc::fence_after();
+}
+
+template <int K, int N, int NTHR, typename F = NoOverlap>
 __device__ __forceinline__ void layer_mma_ts(uint32_t tcol, const uint8_t* Wt, uint64_t* bar, uint32_t& phase,
-                                             int t, int grp) {
+                                             int t, int grp, F&& overlap = F()) {
   tc::tmem_st_wait();
   tc::fence_before();
   named_bar(1 + grp, NTHR);
@@ -195,6 +220,7 @@ __device__ __forceinline__ void layer_mma_ts(uint32_t tcol, const uint8_t* Wt, u
     tc::mma_commit(bar);
   }
   __syncwarp();
+  overlap();
   tc::mbar_wait(bar, phase);
   phase ^= 1u;
   tc::fence_after();
@@ -220,6 +246,8 @@ __global__ void __launch_bounds__(TEAMS * 256, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[TEAMS];
   __shared__ uint32_t tmem_base;
+  __shared__ int lead_done;   // team 0's completed batches (counted up to FV_OFF_LEAD)
+  if (threadIdx.x == 0) lead_done = 0;
   constexpr uint32_t TCOLS = TEAMS == 1 ? 256 : 512;
   float* sB4 = reinterpret_cast<float*>(smem + OF_B4);
   tc_prologue<TEAMS, TCOLS>(reinterpret_cast<const uint8_t*>(f.d_tc_pack), PK_OFF0, PK_RAD0, BI_OFF4, 16, smem,
@@ -251,66 +279,124 @@ __global__ void __launch_bounds__(TEAMS * 256, 1)
   const int64_t ntiles = (n + 127) / 128;
   const int64_t tstep = (int64_t)gridDim.x * TEAMS;
   int64_t tile = (int64_t)blockIdx.x * TEAMS + team;
-  float4 vnext = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (tile * 128 + row < n) vnext = xs[tile * 128 + row];
+  // posenc of one sample -> this thread's 12 A-operand words (columns [12*half, +12) of the
+  // 24 holding 39 values, zero pad, ones at k = 46/47): sin/cos(pi x) once per coordinate,
+  // higher bands by double-angle recurrences (error 2^k ulp << fp16 resolution)
+  auto posenc12 = [&](const float4 v, int64_t s, uint32_t (&w)[12]) {
+    const bool fg = s < n && v.w > eps_w;
+    const float xx[3] = {fg ? v.x : 0.f, fg ? v.y : 0.f, fg ? v.z : 0.f};
+    __half pe[48];
+    pe[0] = __float2half_rn(xx[0]); pe[1] = __float2half_rn(xx[1]); pe[2] = __float2half_rn(xx[2]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      float sv, cv;
+      sincospif(xx[j], &sv, &cv);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const float wk = k < f.pe_bands ? f.pe_w[k] : 0.f;
+        pe[3 + 6 * k + j] = __float2half_rn(wk * sv);
+        pe[3 + 6 * k + 3 + j] = __float2half_rn(wk * cv);
+        const float s2 = 2.f * sv * cv, c2 = (cv - sv) * (cv + sv);
+        sv = s2; cv = c2;
+      }
+    }
+#pragma unroll
+    for (int j = 39; j < 46; ++j) pe[j] = __float2half_rn(0.f);
+    pe[46] = pe[47] = __float2half_rn(1.f);
+    const uint32_t* pw = reinterpret_cast<const uint32_t*>(pe);
+#pragma unroll
+    for (int i = 0; i < 12; ++i) w[i] = half ? pw[12 + i] : pw[i];
+  };
+  // Software pipeline per team:
+  //  * the input is loaded two tiles ahead and the next tile's posenc is computed (and
+  //    stored to its own TMEM block, OF_TPE) while this tile's layer-1 MMAs run;
+  //  * the last layer (N = 16, accumulator block OF_TD4) of tile t-1 and layer 0 of tile t
+  //    are independent, so they go out as ONE batch with one commit: 4 MMA round trips per
+  //    tile instead of 5.
+  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 vcur = tile * 128 + row < n ? xs[tile * 128 + row] : zero4;
+  float4 vnext = (tile + tstep) * 128 + row < n ? xs[(tile + tstep) * 128 + row] : zero4;
+  const uint32_t pe_dst = tcol + lane + OF_TPE + half * 12;
+  {
+    uint32_t pw[12];
+    posenc12(vcur, tile * 128 + row, pw);
+    tc::tmem_st8(pe_dst, pw);
+    tc::tmem_st4(pe_dst + 8, pw + 8);
+  }
+  const auto emit = [&](const float4 v, int64_t s) {   // x_final = x_skel + x_res of one sample
+    float o[16];
+    tc::tmem_ld16(tcol + lane + OF_TD4, o);
+    tc::tmem_ld_wait();
+    if (s < n) {
+      const bool fg = v.w > eps_w;
+      const float y0 = v.x + (o[0] + sB4[0]), y1 = v.y + (o[1] + sB4[1]), y2 = v.z + (o[2] + sB4[2]);
+      out[s] = fg ? make_float4(y0, y1, y2, v.w) : make_float4(0.f, 0.f, 0.f, v.w);
+      if (xfinal) {
+        xfinal[3 * s] = fg ? y0 : 0.f; xfinal[3 * s + 1] = fg ? y1 : 0.f; xfinal[3 * s + 2] = fg ? y2 : 0.f;
+      }
+    }
+  };
+  const uint32_t b4 = tc::smem_u32(smem + PK_OFF4), b0 = tc::smem_u32(smem + PK_OFF0);
+  float4 vprev = zero4;
+  int64_t sprev = -1;
+  const auto lead = [&] {
+    if (TEAMS == 2 && team == 0 && tt == 0) {
+      volatile int* p = &lead_done;
+      if (*p < FV_OFF_LEAD) *p = *p + 1;
+    }
+  };
   for (; tile < ntiles; tile += tstep) {
     const int64_t s = tile * 128 + row;
-    const float4 v = vnext;
-    if (s + tstep * 128 < n) vnext = xs[s + tstep * 128];   // prefetch the team's next tile
-    const bool fg = s < n && v.w > eps_w;
-    const float x0 = fg ? v.x : 0.f, x1 = fg ? v.y : 0.f, x2 = fg ? v.z : 0.f;
-    {  // posenc -> A columns [12*half, +12) of 0..23 (39 values, zero pad, ones at k = 46/47):
-       // sin/cos(pi x) once per coordinate, higher bands by double-angle recurrences
-       // (error 2^k ulp << fp16 resolution)
-      __half pe[48];
-      pe[0] = __float2half_rn(x0); pe[1] = __float2half_rn(x1); pe[2] = __float2half_rn(x2);
-      const float xx[3] = {x0, x1, x2};
+    const float4 v = vcur;
+    // [layer 4 of the previous tile] + layer 0 of this tile, one commit
+    layer_issue_ts(bar, phase, tt, team, [&] {
+      // De-phase the two teams: team 1 starts once team 0 has FV_OFF_LEAD batches done, so
+      // one team's epilogues run under the other's MMAs instead of both teams' at once.
+      if (TEAMS == 2 && team == 1 && sprev < 0)
+        while (*reinterpret_cast<volatile int*>(&lead_done) < FV_OFF_LEAD) {}
+      if (sprev >= 0) {
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        float sv, cv;
-        sincospif(xx[j], &sv, &cv);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          const float wk = k < f.pe_bands ? f.pe_w[k] : 0.f;
-          pe[3 + 6 * k + j] = __float2half_rn(wk * sv);
-          pe[3 + 6 * k + 3 + j] = __float2half_rn(wk * cv);
-          const float s2 = 2.f * sv * cv, c2 = (cv - sv) * (cv + sv);
-          sv = s2; cv = c2;
-        }
+        for (int k = 0; k < 8; ++k)
+          tc::mma_f16_ts(tcol + OF_TD4, tcol + OF_TA + k * 8, tc::make_desc(b4 + k * 2 * 16 * 16, 16 * 16, 128),
+                         tc::idesc_f16(128, 16), k > 0 ? 1u : 0u);
       }
 #pragma unroll
-      for (int j = 39; j < 46; ++j) pe[j] = __float2half_rn(0.f);
-      pe[46] = pe[47] = __float2half_rn(1.f);
-      const uint32_t* pw = reinterpret_cast<const uint32_t*>(pe);
-      if (half == 0) {
-        tc::tmem_st8(tcol + lane + OF_TA, pw);
-        tc::tmem_st4(tcol + lane + OF_TA + 8, pw + 8);
-      } else {
-        tc::tmem_st8(tcol + lane + OF_TA + 12, pw + 12);
-        tc::tmem_st4(tcol + lane + OF_TA + 20, pw + 20);
-      }
-    }
-    layer_mma_ts<48, 128, 256>(tcol, smem + PK_OFF0, bar, phase, tt, team);
+      for (int k = 0; k < 3; ++k)
+        tc::mma_f16_ts(tcol, tcol + OF_TPE + k * 8, tc::make_desc(b0 + k * 2 * 128 * 16, 128 * 16, 128),
+                       tc::idesc_f16(128, 128), k > 0 ? 1u : 0u);
+    });
+    lead();
+    if (sprev >= 0 && half == 0) emit(vprev, sprev);
     epi_relu64_ts(dsrc, adst);
-    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF1, bar, phase, tt, team);
+    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF1, bar, phase, tt, team, [&] {
+      const int64_t s1 = s + tstep * 128, s2 = s1 + tstep * 128;
+      uint32_t pw[12];
+      posenc12(vnext, s1, pw);
+      tc::tmem_st8(pe_dst, pw);
+      tc::tmem_st4(pe_dst + 8, pw + 8);
+      vcur = vnext;
+      vnext = s2 < n ? xs[s2] : zero4;
+    });
+    lead();
     epi_relu64_ts(dsrc, adst);
     layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF2, bar, phase, tt, team);
+    lead();
     epi_relu64_ts(dsrc, adst);
     layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF3, bar, phase, tt, team);
+    lead();
     epi_relu64_ts(dsrc, adst);
-    layer_mma_ts<128, 16, 256>(tcol, smem + PK_OFF4, bar, phase, tt, team);
-    if (half == 0) {
-      float o[16];
-      tc::tmem_ld16(dsrc, o);
-      tc::tmem_ld_wait();
-      if (s < n) {
-        const float y0 = x0 + (o[0] + sB4[0]), y1 = x1 + (o[1] + sB4[1]), y2 = x2 + (o[2] + sB4[2]);
-        out[s] = fg ? make_float4(y0, y1, y2, v.w) : make_float4(0.f, 0.f, 0.f, v.w);
-        if (xfinal) {
-          xfinal[3 * s] = fg ? y0 : 0.f; xfinal[3 * s + 1] = fg ? y1 : 0.f; xfinal[3 * s + 2] = fg ? y2 : 0.f;
-        }
-      }
-    }
+    const bool fg = s < n && v.w > eps_w;
+    vprev = fg ? v : make_float4(0.f, 0.f, 0.f, v.w);
+    sprev = s;
+  }
+  if (sprev >= 0) {   // layer 4 of the team's last tile
+    layer_issue_ts(bar, phase, tt, team, [&] {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        tc::mma_f16_ts(tcol + OF_TD4, tcol + OF_TA + k * 8, tc::make_desc(b4 + k * 2 * 16 * 16, 16 * 16, 128),
+                       tc::idesc_f16(128, 16), k > 0 ? 1u : 0u);
+    });
+    if (half == 0) emit(vprev, sprev);
   }
   tc::fence_before();
   __syncthreads();
