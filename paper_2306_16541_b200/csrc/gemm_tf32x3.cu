@@ -30,6 +30,9 @@
 #include "gemm_tf32x3.h"
 
 namespace fv {
+#ifndef FV_G3_OBUF
+#define FV_G3_OBUF 1   // per-warp output staging buffers (1 frees a ring stage)
+#endif
 namespace g3 {
 
 // ------------------------------------------------------------------------- device helpers
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(384, 1) k_rows(RowsArgs a, const __grid_consta
     const bool vout = (a.ldo % 4 == 0) && (a.N % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0) &&
                       (!a.mask || ((a.ldm % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.mask) & 15) == 0)));
     const int ngroups = (a.Np + 31) / 32, nw = (a.N + 31) / 32;
-    uint8_t* wbuf = sRaw + ST * kStageA + quarter * 2 * 4096;
+    uint8_t* wbuf = sRaw + ST * kStageA + quarter * FV_G3_OBUF * 4096;
     uint32_t it = 0, wcount = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t acc = it & 1;
@@ -357,8 +360,8 @@ __global__ void __launch_bounds__(384, 1) k_rows(RowsArgs a, const __grid_consta
         }
         if (a.bits_out && rowok) a.bits_out[m * nw + cg] = bits;
         if (a.tma_out) {
-          uint8_t* ob = wbuf + (wcount & 1) * 4096;
-          if (lane == 0) bulk_wait_read<1>();      // the store that used this buffer has read it
+          uint8_t* ob = wbuf + (FV_G3_OBUF == 2 ? (wcount & 1) * 4096 : 0);
+          if (lane == 0) bulk_wait_read<FV_G3_OBUF - 1>();      // the store that used this buffer has read it
           __syncwarp();
 #pragma unroll
           for (int u = 0; u < 4; ++u)
@@ -655,7 +658,7 @@ int32_t rows_gemm(RowsArgs a, cudaStream_t st) {
   a.tma = make_tmap(&tm, a.A, a.K, a.M, a.lda, 128) ? 1 : 0;
   a.tma_out = make_tmap(&to, a.out, a.N, a.M, a.ldo, 32) ? 1 : 0;
   const int bbytes = 2 * a.nkc * a.Np * 128;
-  const int obytes = a.tma_out ? 2 * kStageA : 0;
+  const int obytes = a.tma_out ? FV_G3_OBUF * kStageA : 0;
   a.stages = std::min(6, (kSmemMax - 2048 - bbytes - obytes) / kStageA);
   if (a.stages < 2) return set_error(FV_EDIM, "rows_gemm: B operand too large for shared memory");
   const size_t smem = 1024 + bbytes + (size_t)a.stages * kStageA + obytes;
