@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--no-train", action="store_true", help="skip the config-3 training-step measurement")
     p.add_argument("--train-steps", type=int, default=20)
     p.add_argument("--no-scene", action="store_true", help="skip the config-5 multi-subject measurement")
+    p.add_argument("--no-occ-variants", action="store_true", help="skip the dense / ellipsoid-occupancy runs")
     return p.parse_args()
 
 
@@ -268,6 +269,7 @@ def run_ours(args, rank, world, local_rank):
     dominant = max(roofs, key=lambda k: stages.get(k, 0.0))
     roof = dict(roofs[dominant])
 
+    occ_var = occupancy_variants(nets, rnd, cam, st, dev) if rank == 0 and not args.no_occ_variants else None
     train = None if args.no_train else train_throughput(args, rank, world, dev)
     multi = None if args.no_scene else scene_throughput(args, rank, world, dev)
 
@@ -292,6 +294,7 @@ def run_ours(args, rank, world, local_rank):
             "train": train,
             "multi_subject": multi,
             "stages_ms": stages,
+            "occupancy_variants": occ_var,
             "roofline": roof,
             "stage_rooflines": roofs,
             "cpu_baseline": cpu,
@@ -469,7 +472,7 @@ def scene_throughput(args, rank, world, dev):
             "l2": "flushed (256 MB write) before every timed frame"}
 
 
-def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5):
+def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5, occ_grid=None):
     """Device time of each stage of the actual render path (fv_render_fwd_timed: CUDA
     events between march+warp+compaction, k_offset_tc, k_radiance_tc and the compositor),
     median over `reps` frames; plus the occupancy rebuild."""
@@ -481,7 +484,7 @@ def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5):
     sp = torch.cuda.current_stream().cuda_stream
     pix = rnd.pixel_order(cam)
     n = pix.numel()
-    occ = rnd.build_occupancy(nets, st) if occ_on else None
+    occ = occ_grid if occ_grid is not None else (rnd.build_occupancy(nets, st) if occ_on else None)
     m, cs, w = march_struct(st, pix, occ, True), camera_struct(cam), nets.warp_struct()
     h, f = nets.hash_struct(), nets.field_struct()
     rgb = torch.empty((n, 3), device=dev)
@@ -501,7 +504,7 @@ def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5):
            "composite": float(med[3]), "render_total": float(med[4]),
            "field": float(med[1] + med[2]), "samples": S, "fg_samples": int(nfg.value),
            "fg_fraction": nfg.value / S}
-    if occ_on:
+    if occ_on and occ_grid is None:
         ts = []
         for _ in range(reps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -511,6 +514,24 @@ def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5):
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
         out["occupancy_build"] = float(np.median(ts))
+    return out
+
+
+def occupancy_variants(nets, rnd, cam, st, dev, reps=5):
+    """the flat random-init density turns every occupancy cell on, so next to the
+    headline (grid rebuilt from density) report a dense run (no skip grid) and a run with a
+    seeded body-ellipsoid skip grid, each with its evaluated-sample fraction (device time of
+    fv_render_fwd_timed, median of `reps` frames)."""
+    import torch
+    from paper_2306_16541_b200.scene import ellipsoid_occupancy
+    n_rays = cam.width * cam.height
+    out = {}
+    ell = torch.from_numpy(ellipsoid_occupancy(st.box_min, st.box_max)).to(dev)
+    for name, occ_on, grid in (("dense", False, None), ("ellipsoid", True, ell)):
+        s = stage_times(nets, rnd, cam, st, dev, occ_on, reps=reps, occ_grid=grid)
+        out[name] = {"render_ms": s["render_total"], "frames_per_s": 1000.0 / s["render_total"],
+                     "rays_per_s": n_rays / (s["render_total"] / 1000.0), "evaluated_fraction": s["fg_fraction"]}
+    out["ellipsoid"]["occupied_cells"] = int(sum(bin(int(v) & 0xFFFFFFFF).count("1") for v in ell.cpu().numpy()))
     return out
 
 

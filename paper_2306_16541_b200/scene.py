@@ -205,6 +205,27 @@ def target_image(scene: Scene, seed: int = 7):
     return out.astype(np.float32), mask
 
 
+OCC_RES = 32
+
+
+def ellipsoid_occupancy(box_min, box_max, seed: int = 11, axes=(0.8, 1.0, 0.6), jitter: float = 0.1) -> np.ndarray:
+    """Seeded-ellipsoid 32^3 occupancy bitfield over the observation box (the C2
+    run with a body-shaped skip grid next to the flat-density one).  Cell (i,j,k) -- bit
+    ((i*32 + j)*32 + k) of an int32[1024], the layout of ``occ_test`` -- is set iff its
+    centre lies inside the ellipsoid with semi-axes ``axes`` (x the box half-extent), each
+    scaled by a seeded factor in [1 - jitter, 1 + jitter]."""
+    rng = np.random.default_rng(np.random.SeedSequence(seed))
+    bmin, bmax = np.asarray(box_min, np.float64), np.asarray(box_max, np.float64)
+    half, ctr = 0.5 * (bmax - bmin), 0.5 * (bmax + bmin)
+    semi = np.asarray(axes) * half * rng.uniform(1.0 - jitter, 1.0 + jitter, 3)
+    c = (np.arange(OCC_RES) + 0.5) / OCC_RES
+    gx, gy, gz = np.meshgrid(*[bmin[j] + c * (bmax[j] - bmin[j]) for j in range(3)], indexing="ij")
+    inside = ((gx - ctr[0]) / semi[0]) ** 2 + ((gy - ctr[1]) / semi[1]) ** 2 + ((gz - ctr[2]) / semi[2]) ** 2 <= 1.0
+    bits = inside.reshape(-1).astype(np.uint64)
+    words = (bits.reshape(-1, 32) << np.arange(32, dtype=np.uint64)).sum(1)
+    return words.astype(np.uint32).view(np.int32)
+
+
 @dataclass
 class MultiScene:
     """Config 5: subjects (each a full single-subject Scene in its own frame) placed at

@@ -76,3 +76,21 @@ def test_single_subject_merge_is_the_plain_render():
     plain = opipe.render_rays(dict(scenes[0], bg=bg), ccs[0], pix, ms.camera.width, sts[0])
     assert np.max(np.abs(res["rgb"] - plain["rgb"])) < 1e-6
     assert np.max(np.abs(res["alpha"] - plain["alpha"])) < 1e-7
+
+
+def test_ellipsoid_occupancy_bit_layout():
+    """The seeded-ellipsoid skip grid (bench occupancy_variants) uses the occ_test layout:
+    a point's cell bit is set iff the cell centre is inside the ellipsoid."""
+    bmin, bmax = (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0)
+    bits = psc.ellipsoid_occupancy(bmin, bmax, seed=11)
+    assert bits.dtype == np.int32 and bits.shape == (1024,)
+    assert np.array_equal(bits, psc.ellipsoid_occupancy(bmin, bmax, seed=11))
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, (4000, 3)).astype(np.float32)
+    cell = ocam.occ_cell(x, bmin, ocam.occ_scale(bmin, bmax))
+    got = ocam.occ_test(bits.view(np.uint32), cell)
+    c = np.stack([cell // 1024, (cell // 32) % 32, cell % 32], -1)
+    centre = -1.0 + (c + 0.5) * (2.0 / 32)
+    r = np.linalg.norm(centre / np.array([0.8, 1.0, 0.6]), axis=-1)
+    assert np.all(got[r < 0.85]) and not np.any(got[r > 1.15])   # seeded axis factors within +-10 %
+    assert 0.15 < got.mean() < 0.35
