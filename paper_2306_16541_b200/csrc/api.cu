@@ -67,7 +67,7 @@ int32_t field_fwd(const fv_field* f, const fv_hash* h, const float4* xs, int64_t
 // occupancy probe points: cell c (x-major), sub-point j in 2x2x2
 __global__ void k_occ_points(fv_march m, fv_warp w, float4* __restrict__ xs) {
   __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
-  for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
+  fill_bones_x2(sg, w.d_g, w.n_bones);
   __syncthreads();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= OCC_RES * OCC_RES * OCC_RES * 8) return;

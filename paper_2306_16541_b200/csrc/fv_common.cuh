@@ -93,19 +93,27 @@ __device__ __forceinline__ bool occ_test(const uint32_t* occ, const float* bmin,
 
 // ---------------------------------------------------------------- skeleton warp
 // Corner-packed weight volume: for channel i and padded-grid cell (ix,iy,iz) in [0,G]^3 the
-// 8 corner values vp[i, ix+a, iy+b, iz+c] (a*4+b*2+c order) are stored contiguously
-// (one 16-byte word in fp16, two in fp32), so one gather replaces the 8 of ad:767-773.
-__device__ __forceinline__ void load_corners(const void* vol, int half, size_t cell, float (&cv)[8]) {
+// 8 corner values vp[i, ix+a, iy+b, iz+c] are stored contiguously (one 16-byte word in fp16,
+// two in fp32) as x-pairs Z_q = (v[0,b,c], v[1,b,c]), q = 2b + c (k_warp_pack), so one
+// gather replaces the 8 of ad:767-773.  load_corners returns them in a*4+b*2+c order.
+__device__ __forceinline__ void load_corners_x2(const void* vol, int half, size_t cell, float2 (&z)[4]) {
   if (half) {
     const uint4 w = __ldg(reinterpret_cast<const uint4*>(vol) + cell);
     const __half2* h = reinterpret_cast<const __half2*>(&w);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) { float2 f = __half22float2(h[q]); cv[2 * q] = f.x; cv[2 * q + 1] = f.y; }
+    for (int q = 0; q < 4; ++q) z[q] = __half22float2(h[q]);
   } else {
     const float4 a = __ldg(reinterpret_cast<const float4*>(vol) + 2 * cell);
     const float4 b = __ldg(reinterpret_cast<const float4*>(vol) + 2 * cell + 1);
-    cv[0] = a.x; cv[1] = a.y; cv[2] = a.z; cv[3] = a.w; cv[4] = b.x; cv[5] = b.y; cv[6] = b.z; cv[7] = b.w;
+    z[0] = make_float2(a.x, a.y); z[1] = make_float2(a.z, a.w); z[2] = make_float2(b.x, b.y); z[3] = make_float2(b.z, b.w);
   }
+}
+
+__device__ __forceinline__ void load_corners(const void* vol, int half, size_t cell, float (&cv)[8]) {
+  float2 z[4];
+  load_corners_x2(vol, half, cell, z);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) { cv[q] = z[q].x; cv[4 + q] = z[q].y; }
 }
 
 // Grid coordinates of bone point p for the volume (ad:746-753); returns inside flag.
@@ -150,38 +158,87 @@ __device__ __forceinline__ size_t vol_cell_index(int bone, int res, const int (&
   return (size_t)(unsigned)(((bone * s + i0[0]) * s + i0[1]) * s + i0[2]);
 }
 
-// Full skeleton warp of one point with G in shared memory (sg: K*12 floats).
+// Bone transforms in shared memory for warp_point: per bone the 12 floats of G_i
+// (R row-major, t) reordered as [R00 R10 R01 R11 | R02 R12 t0 t1 | R20 R21 R22 t2], so rows
+// 0 and 1 of p = x R^T + t go through one packed f32x2 FMA chain (nibble table below).
+__device__ __forceinline__ void fill_bones_x2(float* sg, const float* g, int n_bones) {
+  for (int i = threadIdx.x; i < n_bones * 12; i += blockDim.x) {
+    const int b = i / 12, k = i % 12;
+    sg[i] = g[b * 12 + (int)((0xB876A9524130ull >> (4 * k)) & 15u)];
+  }
+}
+
+// bone_point on the fill_bones_x2 layout (same per-lane operations, bitwise identical)
+__device__ __forceinline__ void bone_point_x2(const float* g, float x0, float x1, float x2, float (&p)[3]) {
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4 a = g4[0], b = g4[1], c = g4[2];
+  const float2 p01 = __fadd2_rn(__ffma2_rn(make_float2(b.x, b.y), make_float2(x2, x2),
+                                           __ffma2_rn(make_float2(a.z, a.w), make_float2(x1, x1),
+                                                      __fmul2_rn(make_float2(a.x, a.y), make_float2(x0, x0)))),
+                                make_float2(b.z, b.w));
+  p[0] = p01.x;
+  p[1] = p01.y;
+  p[2] = __fadd_rn(__fmaf_rn(c.z, x2, __fmaf_rn(c.y, x1, __fmul_rn(c.x, x0))), c.w);
+}
+
+// v0 + t (v1 - v0) on two lanes; v1 - v0 as fma(v0, -1, v1) (exact product, one rounding),
+// so each lane is bitwise lerp_fma.
+__device__ __forceinline__ float2 lerp_fma2(float2 v0, float2 v1, float2 t) {
+  return __ffma2_rn(t, __ffma2_rn(v0, make_float2(-1.f, -1.f), v1), v0);
+}
+
+// Full skeleton warp of one point with G in shared memory (sg: K*12 floats, fill_bones_x2).
 // Returns L; xs = sum_i w_i p_i / L (0 if L <= eps_w).  Optional per-bone weights out.
+// Per bone, the x/y coordinates of the bone point and grid position, the three lerp levels
+// of the trilinear blend (over x-pairs of corners) and the (s0, s1) accumulation run as
+// packed f32x2 FMAs: each lane performs exactly the scalar operation of bone_point /
+// warp_cell / trilerp8 (oracle.warp), so results are unchanged bit for bit.
 template <bool STORE_W>
 __device__ __forceinline__ float warp_point(const fv_warp& w, const float* sg, float eps_w,
                                             float x0, float x1, float x2, float (&xs)[3],
                                             float* w_out = nullptr, size_t w_stride = 0) {
-  float lik = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f;
+  float lik = 0.f, s2 = 0.f;
+  float2 s01 = make_float2(0.f, 0.f);
   const int K = w.n_bones;
+  const int G = w.vol_res;
+  const float gp1 = (float)(G + 1), gmax = (float)G;
+  const float2 nmin01 = make_float2(-w.wbox_min[0], -w.wbox_min[1]), sc01 = make_float2(w.wscale[0], w.wscale[1]);
+  const float2 one2 = make_float2(1.f, 1.f), mone2 = make_float2(-1.f, -1.f);
+  const float2 X0 = make_float2(x0, x0), X1 = make_float2(x1, x1), X2 = make_float2(x2, x2);
 #pragma unroll 4
   for (int i = 0; i < K; ++i) {
-    float p[3];
-    {
-      const float4* g4 = reinterpret_cast<const float4*>(sg + 12 * i);   // 48-byte rows
-      const float4 a = g4[0], b = g4[1], c = g4[2];
-      const float g[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
-      bone_point(g, x0, x1, x2, p);
-    }
-    int i0[3]; float f[3];
+    const float4* g4 = reinterpret_cast<const float4*>(sg + 12 * i);   // 48-byte rows
+    const float4 a = g4[0], b = g4[1], c = g4[2];
+    // p01 = (x R^T + t)[0..1], p2 (bone_point's FMA chain)
+    const float2 p01 = __fadd2_rn(__ffma2_rn(make_float2(b.x, b.y), X2,
+                                             __ffma2_rn(make_float2(a.z, a.w), X1, __fmul2_rn(make_float2(a.x, a.y), X0))),
+                                  make_float2(b.z, b.w));
+    const float p2 = __fadd_rn(__fmaf_rn(c.z, x2, __fmaf_rn(c.y, x1, __fmul_rn(c.x, x0))), c.w);
+    // grid position (warp_cell): u = (p - min) * scale + 1, inside iff u in [0, G+1]
+    const float2 u01 = __ffma2_rn(__fadd2_rn(p01, nmin01), sc01, one2);
+    const float u2 = __fmaf_rn(__fsub_rn(p2, w.wbox_min[2]), w.wscale[2], 1.0f);
+    const bool inside = (u01.x >= 0.f) && (u01.x <= gp1) && (u01.y >= 0.f) && (u01.y <= gp1) && (u2 >= 0.f) &&
+                        (u2 <= gp1);
     float wi = 0.f;
-    if (warp_cell(w, p, i0, f)) {
-      float cv[8];
-      load_corners(w.d_vol_packed, w.vol_half, vol_cell_index(i, w.vol_res, i0), cv);
-      wi = trilerp8(f, cv);
+    if (inside) {
+      const float f0 = fminf(fmaxf(floorf(u01.x), 0.f), gmax), f1 = fminf(fmaxf(floorf(u01.y), 0.f), gmax);
+      const float fl2 = fminf(fmaxf(floorf(u2), 0.f), gmax);
+      const float2 fr01 = __ffma2_rn(make_float2(f0, f1), mone2, u01);      // u - floor(u)
+      const float fr2 = __fsub_rn(u2, fl2);
+      const int i0[3] = {(int)f0, (int)f1, (int)fl2};
+      float2 z[4];
+      load_corners_x2(w.d_vol_packed, w.vol_half, vol_cell_index(i, G, i0), z);
+      const float2 tz = make_float2(fr2, fr2), ty = make_float2(fr01.y, fr01.y);
+      const float2 q = lerp_fma2(lerp_fma2(z[0], z[1], tz), lerp_fma2(z[2], z[3], tz), ty);   // (c_{a=0}, c_{a=1})
+      wi = lerp_fma(q.x, q.y, fr01.x);
     }
     if (STORE_W) w_out[(size_t)i * w_stride] = wi;
     lik = __fadd_rn(lik, wi);
-    s0 = __fmaf_rn(wi, p[0], s0);
-    s1 = __fmaf_rn(wi, p[1], s1);
-    s2 = __fmaf_rn(wi, p[2], s2);
+    s01 = __ffma2_rn(make_float2(wi, wi), p01, s01);
+    s2 = __fmaf_rn(wi, p2, s2);
   }
   if (lik > eps_w) {
-    xs[0] = __fdiv_rn(s0, lik); xs[1] = __fdiv_rn(s1, lik); xs[2] = __fdiv_rn(s2, lik);
+    xs[0] = __fdiv_rn(s01.x, lik); xs[1] = __fdiv_rn(s01.y, lik); xs[2] = __fdiv_rn(s2, lik);
   } else {
     xs[0] = xs[1] = xs[2] = 0.f;
   }

@@ -7,6 +7,8 @@
 namespace fv {
 
 // W^c (C,G,G,G) -> corner-packed [K][(G+1)^3][8], zero padding of ad:755-756 folded in.
+// Corner order within a cell: x-pairs Z_q = (v[0,b,c], v[1,b,c]) for q = 2b + c, i.e. the
+// a*4+b*2+c indices (0,4, 1,5, 2,6, 3,7), so the blend runs as packed f32x2 lerps.
 template <typename T>
 __global__ void k_warp_pack(const float* __restrict__ vol, int K, int G, T* __restrict__ out) {
   const int s = G + 1;
@@ -32,12 +34,12 @@ __global__ void k_warp_pack(const float* __restrict__ vol, int K, int G, T* __re
     if constexpr (sizeof(T) == 2) {
       __half2 h[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) h[k] = __floats2half2_rn(v[2 * k], v[2 * k + 1]);
+      for (int q = 0; q < 4; ++q) h[q] = __floats2half2_rn(v[q], v[4 + q]);
       reinterpret_cast<uint4*>(out)[e] = *reinterpret_cast<uint4*>(h);
     } else {
       float4* o = reinterpret_cast<float4*>(out) + 2 * e;
-      o[0] = make_float4(v[0], v[1], v[2], v[3]);
-      o[1] = make_float4(v[4], v[5], v[6], v[7]);
+      o[0] = make_float4(v[0], v[4], v[1], v[5]);
+      o[1] = make_float4(v[2], v[6], v[3], v[7]);
     }
   }
 }
@@ -46,7 +48,7 @@ __global__ void k_warp_fwd(fv_warp w, float eps_w, const float* __restrict__ x, 
                            float* __restrict__ xskel, float* __restrict__ lik, uint8_t* __restrict__ fg,
                            float* __restrict__ wout) {
   __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
-  for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
+  fill_bones_x2(sg, w.d_g, w.n_bones);
   __syncthreads();
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
                                                     Compact cmp) {
   __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
   __shared__ int32_t wcount[4], wbase;
-  for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sg[i] = w.d_g[i];
+  fill_bones_x2(sg, w.d_g, w.n_bones);
   __syncthreads();
   const int N = m.n_samples;
   const int64_t total = padded_rays(n_rays) * N;
@@ -165,10 +167,9 @@ __global__ void __launch_bounds__(128) k_warp_bwd(fv_warp w, float eps_w, const 
                                                   float* __restrict__ dg) {
   __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
   __shared__ float sdg[WANT_G ? FV_MAX_BONES * 12 : 1];
-  for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) {
-    sg[i] = w.d_g[i];
-    if (WANT_G) sdg[i] = 0.f;
-  }
+  fill_bones_x2(sg, w.d_g, w.n_bones);
+  if (WANT_G)
+    for (int i = threadIdx.x; i < w.n_bones * 12; i += blockDim.x) sdg[i] = 0.f;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(128) k_warp_bwd(fv_warp w, float eps_w, const 
   const int G = w.vol_res;
   for (int i = 0; i < w.n_bones; ++i) {
     float p[3];
-    bone_point(sg + 12 * i, x0, x1, x2, p);
+    bone_point_x2(sg + 12 * i, x0, x1, x2, p);
     int i0[3]; float f[3];
     const bool in = warp_cell(w, p, i0, f);
     const float dw = (g0 * (p[0] - xsk[0]) + g1 * (p[1] - xsk[1]) + g2 * (p[2] - xsk[2])) * invL;
