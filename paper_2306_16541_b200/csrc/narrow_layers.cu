@@ -83,6 +83,10 @@ __global__ void __launch_bounds__(256) k_narrow_fwd(const float* __restrict__ x,
 
 // dx row of K <= 128 columns (LPR lanes per row, 4 columns each); bits (one uint32 per 32
 // columns) or a float mask zero the ReLU-inactive inputs.
+// A warp handles 32 rows per iteration: lane l stages row l's dz (N floats) and ReLU-bit
+// words in shared memory (one coalesced load batch for the 32 rows, the next batch already
+// in flight), then the rows are written LPR lanes x 4 columns at a time (the kernel is a
+// write stream of K floats per row).
 template <int N, int LPR>
 __global__ void __launch_bounds__(256) k_narrow_dx(const float* __restrict__ dz, int64_t ldz, const float* __restrict__ W,
                                                    int K, const uint32_t* __restrict__ bits,
@@ -90,9 +94,11 @@ __global__ void __launch_bounds__(256) k_narrow_dx(const float* __restrict__ dz,
                                                    float* __restrict__ dx, int64_t lddx, int64_t M) {
   constexpr int RPI = 32 / LPR;
   __shared__ float sW[128 * kMaxN];
+  __shared__ float sdz[8][32 * N];
+  __shared__ uint32_t sbits[8][32 * 4];
   for (int i = threadIdx.x; i < K * N; i += blockDim.x) sW[i] = W[i];
   __syncthreads();
-  const int lane = threadIdx.x & 31, sub = lane / LPR, li = lane % LPR;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, sub = lane / LPR, li = lane % LPR;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int nw = (K + 31) / 32;
@@ -104,30 +110,42 @@ __global__ void __launch_bounds__(256) k_narrow_dx(const float* __restrict__ dz,
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int n = 0; n < N; ++n) w[j][n] = k0 + j < K ? sW[(k0 + j) * N + n] : 0.f;
-  constexpr int STEP = kRowsPerWarp * RPI;
-  for (int64_t r0 = warp * STEP; r0 < M; r0 += nwarps * STEP) {
-    float g[kRowsPerWarp][N];
-    uint32_t mb[kRowsPerWarp];
+  float gn[N];
+  uint32_t bn[4];
+  auto fetch = [&](int64_t g0) {   // lane l: row g0 + l
+    const int64_t r = g0 + lane;
+    const bool ok = r < M;
 #pragma unroll
-    for (int q = 0; q < kRowsPerWarp; ++q) {
-      const int64_t r = r0 + q * RPI + sub;
-      const bool ok = r < M;
+    for (int n = 0; n < N; ++n) gn[n] = ok ? __ldg(dz + r * ldz + n) : 0.f;
 #pragma unroll
-      for (int n = 0; n < N; ++n) g[q][n] = ok ? __ldg(dz + r * ldz + n) : 0.f;
-      mb[q] = (bits && ok && k0 < K) ? __ldg(bits + r * nw + (k0 >> 5)) : 0xFFFFFFFFu;
-    }
+    for (int q = 0; q < 4; ++q) bn[q] = (bits && ok && q < nw) ? __ldg(bits + r * nw + q) : 0xFFFFFFFFu;
+  };
+  int64_t g0 = warp * 32;
+  if (g0 < M) fetch(g0);
+  for (; g0 < M; g0 += nwarps * 32) {
 #pragma unroll
-    for (int q = 0; q < kRowsPerWarp; ++q) {
-      const int64_t r = r0 + q * RPI + sub;
+    for (int n = 0; n < N; ++n) sdz[wib][lane * N + n] = gn[n];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sbits[wib][lane * 4 + q] = bn[q];
+    __syncwarp();
+    if (g0 + nwarps * 32 < M) fetch(g0 + nwarps * 32);   // next batch in flight during the stores
+#pragma unroll 4
+    for (int it = 0; it < 32 / RPI; ++it) {
+      const int rr = it * RPI + sub;
+      const int64_t r = g0 + rr;
       if (r >= M || k0 >= K) continue;
+      float g[N];
+#pragma unroll
+      for (int n = 0; n < N; ++n) g[n] = sdz[wib][rr * N + n];
+      const uint32_t mb = sbits[wib][rr * 4 + (k0 >> 5)];
       float o[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        float a = 0.f;
+        float acc = 0.f;
 #pragma unroll
-        for (int n = 0; n < N; ++n) a = fmaf(g[q][n], w[j][n], a);
-        if (bits && !((mb[q] >> ((k0 + j) & 31)) & 1u)) a = 0.f;
-        o[j] = a;
+        for (int n = 0; n < N; ++n) acc = fmaf(g[n], w[j][n], acc);
+        if (bits && !((mb >> ((k0 + j) & 31)) & 1u)) acc = 0.f;
+        o[j] = acc;
       }
       float* dst = dx + r * lddx + k0;
       if (fmask) {
@@ -144,6 +162,7 @@ __global__ void __launch_bounds__(256) k_narrow_dx(const float* __restrict__ dz,
           if (k0 + j < K) dst[j] = o[j];
       }
     }
+    __syncwarp();
   }
 }
 
@@ -266,7 +285,7 @@ int32_t narrow_fwd(const float* x, int64_t ldx, int K, const float* W, const flo
 int32_t narrow_dx(const float* dz, int64_t ldz, int N, const float* W, int K, const uint32_t* bits,
                   const float* fmask, int64_t ldm, float* dx, int64_t lddx, int64_t M, cudaStream_t st) {
   if (N < 1 || N > kMaxN || K < 1 || K > 128) return set_error(FV_EDIM, "narrow_dx: shape");
-  const int grid = grid_rows(M, K);
+  const int grid = (int)std::min<int64_t>(((M + 31) / 32 + 7) / 8, (int64_t)sms() * 8);
   FV_NARROW_SWITCH(k_narrow_dx, grid, dz, ldz, W, K, bits, fmask, ldm, dx, lddx, M);
   return check_launch("k_narrow_dx");
 }
