@@ -45,6 +45,30 @@ __global__ void __launch_bounds__(128) k_hash_fwd(fv_hash h, const float* __rest
 // issues one float2 atomic per corner (singletons -- most lanes at the fine levels -- add
 // directly).  Summation order inside a group differs from a per-sample scatter by fp32
 // rounding only (the reference's gather0 scatter-add, ad:335-344, is order-free).
+__device__ __forceinline__ void red2(float2* p, float2 v) {
+  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" :: "l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void red4(float2* p, float2 a, float2 b) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"(p), "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y)
+               : "memory");
+}
+// The 8 corner updates of one cell: an x-corner pair whose entries form an aligned 16-byte
+// pair (indices 2k, 2k+1 -- always the case for even x on hashed levels, where x+1 only
+// flips index bit 0) goes out as one v4 reduction instead of two v2.
+__device__ __forceinline__ void scatter8(float2* dt2, const uint32_t (&gi)[8], const float2 (&v)[8], bool v4ok) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t i0 = gi[q], i1 = gi[q + 4];
+    if (v4ok && (i0 ^ i1) == 1u) {
+      if (i0 < i1) red4(dt2 + i0, v[q], v[q + 4]);
+      else red4(dt2 + i1, v[q + 4], v[q]);
+    } else {
+      red2(dt2 + i0, v[q]);
+      red2(dt2 + i1, v[q + 4]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __restrict__ x, int64_t n,
                                                   const float* __restrict__ dfeat, float* __restrict__ dtable,
                                                   float* __restrict__ dx) {
@@ -57,6 +81,7 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
   hash_norm(h, x[3 * p], x[3 * p + 1], x[3 * p + 2], xn, mask);
   const uint32_t maskT = (1u << h.log2_T) - 1u;
   float2* dt2 = reinterpret_cast<float2*>(dtable);
+  const bool v4ok = (reinterpret_cast<uintptr_t>(dtable) & 15) == 0;
   // corner indices + table values of level l+1 are fetched while level l is processed
   auto corners = [&](int l, HashCell& c, uint32_t (&gi)[8], float2 (&tv)[8]) {
     hash_level_cell(xn, h.res[l], c);
@@ -80,8 +105,9 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
   float2 tvn[8];
   corners(0, cn, gin, tvn);
   for (int l = 0; l < h.n_levels; ++l) {
-    const float g0 = valid ? dfeat[p * (2 * h.n_levels) + 2 * l] : 0.f;
-    const float g1 = valid ? dfeat[p * (2 * h.n_levels) + 2 * l + 1] : 0.f;
+    const float2 gg = valid ? *reinterpret_cast<const float2*>(dfeat + p * (2 * h.n_levels) + 2 * l)
+                            : make_float2(0.f, 0.f);
+    const float g0 = gg.x, g1 = gg.y;
     const HashCell c = cn;
     uint32_t gi[8];
     float2 tv[8];
@@ -116,10 +142,7 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
     const unsigned grp = __match_any_sync(0xffffffffu, key);
     const unsigned multi = __ballot_sync(0xffffffffu, grp != (1u << lane));
     if (grp == (1u << lane)) {
-      if (any) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) atomicAdd(dt2 + gi[q], v[q]);
-      }
+      if (any) scatter8(dt2, gi, v, v4ok);
     } else {
 #pragma unroll
       for (int q = 0; q < 8; ++q) scratch[wib][q][lane] = v[q];
@@ -136,8 +159,7 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
             v[q].y += w.y;
           }
         }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) atomicAdd(dt2 + gi[q], v[q]);
+        scatter8(dt2, gi, v, v4ok);
       }
       __syncwarp(multi);
     }
@@ -174,6 +196,8 @@ extern "C" int32_t fv_hash_bwd(const fv_hash* hash, const float* d_x, int64_t n,
   if (int32_t e = check_hash(hash)) return e;
   if (n < 0) return set_error(FV_EDIM, "fv_hash_bwd: n < 0");
   if (n == 0) return FV_OK;
+  if ((reinterpret_cast<uintptr_t>(d_dfeat) & 7) || (reinterpret_cast<uintptr_t>(d_dtable) & 7))
+    return set_error(FV_EDIM, "fv_hash_bwd: d_dfeat / d_dtable must be 8-byte aligned");
   k_hash_bwd<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*hash, d_x, n, d_dfeat, d_dtable, d_dx);
   return check_launch("fv_hash_bwd");
 }
