@@ -126,6 +126,11 @@ int32_t fv_warp_pack(const float* d_vol, int32_t channels, const fv_warp* warp,
 int32_t fv_warp_fwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
                     float* d_xskel, float* d_lik, uint8_t* d_fg, float* d_w, void* stream);
 
+/* sample_bone_channels (reference freeview.autodiff, ad:728-773) on its own: channel i of the
+ * packed W^c at the bone-i points, pts (K,n,3) -> out (K,n), K = warp->n_bones; zero outside
+ * the one-voxel-padded grid.  Same trilinear sample as inside fv_warp_fwd. */
+int32_t fv_sample_bone_channels(const fv_warp* warp, const float* d_pts, int64_t n, float* d_out, void* stream);
+
 /* d x_skel (n,3) -> d W^c (C,G,G,G) fp32 (accumulated, atomics).  ad:775-789 + Eq 9. */
 int32_t fv_warp_bwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
                     const float* d_dxskel, float* d_dvol, void* stream);
@@ -177,6 +182,10 @@ int32_t fv_field_fwd(const fv_field* field, const fv_hash* hash, const float* d_
                      void* stream);
 
 /* ---- compositing (ad:815-837) ---------------------------------------------- */
+
+/* transmittance (reference freeview.autodiff, ad:815-837): alpha (R,N) -> T (R,N+1),
+ * T[r,0] = 1, T[r,i+1] = T[r,i] (1 - alpha[r,i]) in fp32 (exclusive running product). */
+int32_t fv_transmittance(const float* d_alpha, int64_t n_rays, int32_t n_samples, float* d_trans, void* stream);
 
 /* rays r (R), N samples each: rgbs (R*N,4) [rgb, sigma], delta (R*N), lik (R*N)
  * -> rgb (R,3), alpha (R); optional T (R,N+1) for backward.  Sample layout: ray-major

@@ -91,6 +91,8 @@ SIGNATURES = {
     "fv_linear_fwd_tc": (i32, [vp, i64, vp, vp, vp, i64, i64, i32, i32, i32, vp]),
     "fv_linear_bwd_tc": (i32, [vp, i64, vp, vp, i64, vp, i64, vp, vp, vp, i64, i32, i32, vp]),
     "fv_linear_fwd_tc_bits": (i32, [vp, i64, vp, vp, vp, i64, i64, i32, i32, i32, vp, vp]),
+    "fv_sample_bone_channels": (i32, [P(FvWarp), vp, i64, vp, vp]),
+    "fv_transmittance": (i32, [vp, i64, i32, vp, vp]),
     "fv_linear_bwd_tc_bits": (i32, [vp, i64, vp, vp, i64, vp, i64, vp, vp, vp, i64, i32, i32, vp]),
     "fv_posenc_bwd": (i32, [vp, i64, f32, i32, P(f32), vp, i64, vp, vp]),
     "fv_xfinal": (i32, [vp, vp, i64, f32, vp, vp]),

@@ -154,6 +154,33 @@ int32_t composite_bwd(const CompIn& in, const float* trans, int64_t n_rays, int 
 
 using namespace fv;
 
+namespace fv {
+// transmittance (ad:815-837): T[r, 0] = 1, T[r, i + 1] = T[r, i] * (1 - alpha[r, i]) in fp32,
+// the exclusive running product of the per-sample opacities (one thread per ray).
+__global__ void k_transmittance(const float* __restrict__ alpha, int64_t R, int N, float* __restrict__ T) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const float* a = alpha + r * N;
+  float* t = T + r * (N + 1);
+  float acc = 1.f;
+  t[0] = acc;
+  for (int i = 0; i < N; ++i) {
+    acc = __fmul_rn(acc, __fsub_rn(1.f, a[i]));
+    t[i + 1] = acc;
+  }
+}
+}  // namespace fv
+
+extern "C" int32_t fv_transmittance(const float* d_alpha, int64_t n_rays, int32_t n_samples, float* d_trans,
+                                    void* stream) {
+  if (n_rays < 0 || n_samples < 0 || (n_rays > 0 && (!d_alpha || !d_trans)))
+    return set_error(FV_EDIM, "fv_transmittance: bad arguments");
+  if (n_rays == 0) return FV_OK;
+  fv::k_transmittance<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(d_alpha, n_rays, n_samples,
+                                                                                         d_trans);
+  return check_launch("fv_transmittance");
+}
+
 extern "C" int32_t fv_composite_fwd(const float* d_rgbs, const float* d_delta, const float* d_lik, int32_t lik_stride,
                                     int32_t blocked, int64_t n_rays, int32_t n_samples, const float bg[3], float eps_w,
                                     float eps_t, float* d_rgb, float* d_alpha, float* d_trans, void* stream) {

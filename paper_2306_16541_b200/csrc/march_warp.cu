@@ -250,6 +250,25 @@ flush:
   }
 }
 
+// sample_bone_channels (ad:728-773) on its own: channel i of W^c at the bone-i points pts[i]
+// (K,n,3) -> (K,n), the trilinear sample warp_point takes per bone (zero outside the padded
+// grid).
+__global__ void k_sample_bone_channels(fv_warp w, const float* __restrict__ pts, int64_t n, float* __restrict__ out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)w.n_bones * n) return;
+  const int i = (int)(e / n);
+  const float p[3] = {pts[3 * e], pts[3 * e + 1], pts[3 * e + 2]};
+  int i0[3];
+  float f[3];
+  float v = 0.f;
+  if (warp_cell(w, p, i0, f)) {
+    float cv[8];
+    load_corners(w.d_vol_packed, w.vol_half, vol_cell_index(i, w.vol_res, i0), cv);
+    v = trilerp8(f, cv);
+  }
+  out[e] = v;
+}
+
 }  // namespace fv
 
 namespace fv {
@@ -286,6 +305,16 @@ extern "C" int32_t fv_warp_fwd(const fv_warp* warp, float eps_w, const float* d_
   k_warp_fwd<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*warp, eps_w, d_x, n, d_xskel, d_lik,
                                                                              d_fg, d_w);
   return check_launch("fv_warp_fwd");
+}
+
+extern "C" int32_t fv_sample_bone_channels(const fv_warp* warp, const float* d_pts, int64_t n, float* d_out,
+                                           void* stream) {
+  if (!warp || n < 0 || (n > 0 && (!d_pts || !d_out))) return set_error(FV_EDIM, "fv_sample_bone_channels: bad arguments");
+  if (int32_t e = check_warp(warp)) return e;
+  if (n == 0) return FV_OK;
+  const int64_t total = (int64_t)warp->n_bones * n;
+  k_sample_bone_channels<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*warp, d_pts, n, d_out);
+  return check_launch("fv_sample_bone_channels");
 }
 
 extern "C" int32_t fv_warp_bwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,

@@ -203,6 +203,71 @@ def warp_point(nets: FreeviewModel, x: torch.Tensor, eps_w: float = EPS_W):
     return xf, lik
 
 
+def positional_encode(p: torch.Tensor, num_bands: int = 6, alpha: Optional[float] = None) -> torch.Tensor:
+    """SPEC positional_encode: (n,3) -> (n, 3 + 6 num_bands), Hann-windowed bands
+    (alpha defaults to all bands on).  One fv_posenc_fwd launch (autodiff.posenc)."""
+    from .autodiff import posenc
+    return posenc(p, num_bands, alpha)
+
+
+def residual_offset(nets: FreeviewModel, x_skel: torch.Tensor, pose: Optional[Pose] = None,
+                    alpha: Optional[float] = None, stage: bool = True) -> torch.Tensor:
+    """SPEC residual_offset: x_res (n,3) = MLP([posenc_alpha(x_skel), Omega]) with the
+    pose columns folded into layer 0's bias (fv_offset_bias; ``pose`` sets the model's pose
+    first, else the current one is used); exactly zero when the stage is off.  fp32
+    path: the training layer kernels (split-precision 3xTF32 tcgen05, fp32-accurate)."""
+    x = x_skel.float().contiguous()
+    if x.dim() != 2 or x.shape[1] != 3 or not x.is_cuda:
+        raise DimensionError(f"residual_offset: expected CUDA (n, 3), got {tuple(x.shape)}")
+    n = x.shape[0]
+    if not stage or n == 0:
+        return torch.zeros((n, 3), dtype=torch.float32, device=x.device)
+    if pose is not None:
+        nets.set_pose(pose)
+    from .autodiff import posenc
+    from .scene import PE_BANDS
+    pe = posenc(x, PE_BANDS, nets.pe_alpha if alpha is None else alpha)
+    d = pe.shape[1]
+    ld = (d + 3) // 4 * 4
+    a = torch.zeros((n, ld), dtype=torch.float32, device=x.device)
+    a[:, :d] = pe
+    lib, sp, V = nets.lib, _lib.stream_ptr(), nets.views
+    layers = [(V["off_w0"], nets.b0_eff, d, 128, 1)] + [(V[f"off_w{i}"], V[f"off_b{i}"], 128, 128, 1)
+                                                         for i in range(1, 4)] + [(V["off_w4"], V["off_b4"], 128, 3, 0)]
+    k_ld = ld
+    for w, b, k, m_out, act in layers:
+        y = torch.empty((n, m_out), dtype=torch.float32, device=x.device)
+        _lib.check(lib.fv_linear_fwd_tc(a.data_ptr(), k_ld, w.data_ptr(), b.data_ptr(), y.data_ptr(), m_out, n, k,
+                                        m_out, act, sp), "fv_linear_fwd_tc")
+        a, k_ld = y, m_out
+    return a
+
+
+def stratified_sample(nets: FreeviewModel, camera: CameraModel, pix: torch.Tensor, settings: RenderSettings):
+    """SPEC stratified_sample for the rays of pixel ids ``pix`` (int32, CUDA):
+    (x (R,N,3) world sample positions, delta (R,N), count (R) int32 samples per ray -- N if the
+    ray hits the box, else 0).  One fv_march_warp launch (slab, jittered bins, delta rule of
+    DESIGN §3); the kernel's ray-block-major layout is returned ray-major."""
+    if pix.dtype != torch.int32 or not pix.is_cuda:
+        raise DimensionError("stratified_sample: pix must be an int32 CUDA tensor")
+    r, n = pix.numel(), settings.n_samples
+    rp = (r + 31) // 32 * 32
+    xs = torch.empty((rp * n, 4), dtype=torch.float32, device=pix.device)
+    delta = torch.empty(rp * n, dtype=torch.float32, device=pix.device)
+    x = torch.empty((rp * n, 3), dtype=torch.float32, device=pix.device)
+    count = torch.empty(r, dtype=torch.int32, device=pix.device)
+    if r == 0:
+        return x.view(0, n, 3), delta.view(0, n), count
+    m, cs, w = march_struct(settings, pix, None), camera_struct(camera), nets.warp_struct()
+    _lib.check(nets.lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), r, xs.data_ptr(), delta.data_ptr(),
+                                      x.data_ptr(), count.data_ptr(), _lib.stream_ptr()), "fv_march_warp")
+
+    def ray_major(a, tail):
+        return a.view((rp // 32, n, 32) + tail).transpose(1, 2).reshape((rp, n) + tail)[:r]
+
+    return ray_major(x, (3,)), ray_major(delta, ()), count
+
+
 def query_radiance(nets: FreeviewModel, x_final: torch.Tensor):
     """(c (n,3), sigma (n)) of canonical points."""
     n = x_final.shape[0]
