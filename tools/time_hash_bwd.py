@@ -41,3 +41,18 @@ for _ in range(10):
 e1.record()
 torch.cuda.synchronize()
 print(f"hash bwd: {e0.elapsed_time(e1) / 10 * 1e3:.1f} us")
+
+
+def run_fwd():
+    _lib.check(lib.fv_hash_fwd(C.byref(h), tr.xf.data_ptr(), tr.S, tr.feat.data_ptr(), None, sp))
+
+
+for _ in range(3):
+    run_fwd()
+torch.cuda.synchronize()
+e0.record()
+for _ in range(10):
+    run_fwd()
+e1.record()
+torch.cuda.synchronize()
+print(f"hash fwd: {e0.elapsed_time(e1) / 10 * 1e3:.1f} us")
