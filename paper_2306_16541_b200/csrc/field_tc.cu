@@ -100,41 +100,7 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
 }
 
-// One layer of a group of NTHR threads (t = index in the group): make the group's A-operand
-// stores visible to the tensor-core proxy, barrier, one thread issues K/16 MMAs + commit,
-// everyone waits for the commit.
-template <int K, int N, int NTHR = 128>
-__device__ __forceinline__ void layer_mma(const uint8_t* A, const uint8_t* Wt, uint32_t tcol, uint64_t* bar,
-                                          uint32_t& phase, int t, int grp) {
-  tc::fence_proxy_async();
-  tc::fence_before();
-  named_bar(1 + grp, NTHR);
-  if (t == 0) {
-    tc::fence_after();
-    constexpr uint32_t idesc = tc::idesc_f16(128, N);
-    const uint32_t a0 = tc::smem_u32(A), b0 = tc::smem_u32(Wt);
-#pragma unroll
-    for (int k = 0; k < K / 16; ++k) {
-      const uint64_t ad = tc::make_desc(a0 + k * 2 * 128 * 16, 128 * 16, 128);
-      const uint64_t bd = tc::make_desc(b0 + k * 2 * N * 16, N * 16, 128);
-      tc::mma_f16(tcol, ad, bd, idesc, k > 0 ? 1u : 0u);
-    }
-    tc::mma_commit(bar);
-  }
-  __syncwarp();
-  tc::mbar_wait(bar, phase);
-  phase ^= 1u;
-  tc::fence_after();
-}
-
-// TMEM row -> bias + ReLU -> fp16 -> A operand (columns [0, NC)).
-// fp16x2 helpers: (lo, hi) -> packed half2 ; relu(p * 1 + bias) in one instruction
-__device__ __forceinline__ uint32_t cvt_h2(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
-// relu + round + pack in one conversion: (lo, hi) -> half2(max(lo,0), max(hi,0))
+// fp16x2 helper: relu + round + pack in one conversion, (lo, hi) -> half2(max(lo,0), max(hi,0))
 __device__ __forceinline__ uint32_t cvt_relu_h2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

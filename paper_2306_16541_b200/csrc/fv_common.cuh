@@ -144,14 +144,6 @@ __device__ __forceinline__ float trilerp8(const float (&f)[3], const float (&cv)
   return lerp_fma(lerp_fma(c00, c01, f[1]), lerp_fma(c10, c11, f[1]), f[0]);
 }
 
-// p = x @ R^T + t (row convention, sk:171-172), FMA chain of oracle.warp.bone_points
-__device__ __forceinline__ void bone_point(const float* g, float x0, float x1, float x2, float (&p)[3]) {
-#pragma unroll
-  for (int j = 0; j < 3; ++j)
-    p[j] = __fadd_rn(__fmaf_rn(g[3 * j + 2], x2, __fmaf_rn(g[3 * j + 1], x1, __fmul_rn(g[3 * j], x0))),
-                     g[9 + j]);
-}
-
 // <= 32 bones x 129^3 cells fits int32 (fv_warp_pack checks the volume size)
 __device__ __forceinline__ size_t vol_cell_index(int bone, int res, const int (&i0)[3]) {
   const int s = res + 1;
@@ -168,7 +160,8 @@ __device__ __forceinline__ void fill_bones_x2(float* sg, const float* g, int n_b
   }
 }
 
-// bone_point on the fill_bones_x2 layout (same per-lane operations, bitwise identical)
+// p = x @ R^T + t (row convention, sk:171-172) on the fill_bones_x2 layout: the FMA chain of
+// oracle.warp.bone_points, rows 0/1 as packed f32x2 (per lane the scalar operations)
 __device__ __forceinline__ void bone_point_x2(const float* g, float x0, float x1, float x2, float (&p)[3]) {
   const float4* g4 = reinterpret_cast<const float4*>(g);
   const float4 a = g4[0], b = g4[1], c = g4[2];
@@ -191,7 +184,7 @@ __device__ __forceinline__ float2 lerp_fma2(float2 v0, float2 v1, float2 t) {
 // Returns L; xs = sum_i w_i p_i / L (0 if L <= eps_w).  Optional per-bone weights out.
 // Per bone, the x/y coordinates of the bone point and grid position, the three lerp levels
 // of the trilinear blend (over x-pairs of corners) and the (s0, s1) accumulation run as
-// packed f32x2 FMAs: each lane performs exactly the scalar operation of bone_point /
+// packed f32x2 FMAs: each lane performs exactly the scalar operation of bone_point_x2 /
 // warp_cell / trilerp8 (oracle.warp), so results are unchanged bit for bit.
 template <bool STORE_W>
 __device__ __forceinline__ float warp_point(const fv_warp& w, const float* sg, float eps_w,
