@@ -418,6 +418,22 @@ def save_checkpoint(path: str, trainer: "Trainer", iteration: int) -> None:
         json.dump(man, f, indent=1)
 
 
+def load_params(path: str, nets: FreeviewModel) -> int:
+    """Model parameters only (inference / the render service) from a save_checkpoint directory;
+    rebuilds the derived buffers; returns the iteration.  ValueError on a block-table mismatch."""
+    with open(os.path.join(path, "manifest.json")) as f:
+        man = json.load(f)
+    want = {k: [a, b - a] for k, (a, b) in nets.block_ranges.items()}
+    got = {k: [v["offset"], v["size"]] for k, v in man["blocks"].items()}
+    if want != got:
+        raise ValueError("checkpoint block table does not match the model")
+    a = np.fromfile(os.path.join(path, "params.bin"), dtype="<f4")
+    nets.flat.copy_(torch.from_numpy(a.astype(np.float32)).to(nets.flat.device))
+    nets.set_schedule(alpha=man.get("pe_alpha", nets.pe_alpha), residual=man.get("residual", True))
+    nets.refresh()
+    return int(man["iteration"])
+
+
 def load_checkpoint(path: str, trainer: "Trainer") -> int:
     """Restore a save_checkpoint directory into the trainer's model and Adam state; returns
     the iteration.  Raises DimensionError-style ValueError on a block-table mismatch."""

@@ -417,6 +417,13 @@ def test_train_driver_schedule_log_and_checkpoint_roundtrip(tmp_path):
     torch.cuda.synchronize()
     assert torch.equal(img0, img1)
     assert torch.equal(tr2.m, tr.m) and tr2.t == tr.t
+    # parameters only (the render service's loader): same frame bit for bit
+    from paper_2306_16541_b200.train import load_params
+    nets3 = FreeviewModel(sc)
+    assert load_params(str(tmp_path / "ck"), nets3) == 120
+    img2, _ = rnd.render_image(nets3, sc.camera, sc.poses[0], st_r)
+    torch.cuda.synchronize()
+    assert torch.equal(img0, img2)
 
 
 def test_weight_volume_generator_training_chain():
