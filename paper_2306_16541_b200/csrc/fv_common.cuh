@@ -251,13 +251,7 @@ __device__ __forceinline__ bool seg_sum(float (&v)[N], K key, int lane) {
   if (heads == 0xffffffffu) return true;            // all runs of one (fine levels): nothing to sum
   const int start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
   // the longest run bounds the scan depth: skip the shuffle steps no run needs
-  const unsigned tails = (heads >> 1) | 0x80000000u;
-  int longest = 1;
-  for (unsigned h = heads; h; h &= h - 1) {
-    const int s0 = __ffs(h) - 1;
-    const int e0 = __ffs(tails & (0xffffffffu << s0)) - 1;
-    longest = max(longest, e0 - s0 + 1);
-  }
+  const int longest = (int)__reduce_max_sync(0xffffffffu, (unsigned)(lane - start + 1));
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     if (d >= longest) break;
