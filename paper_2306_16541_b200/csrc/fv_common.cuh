@@ -255,10 +255,19 @@ __device__ __forceinline__ bool seg_sum(float (&v)[N], K key, int lane) {
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     if (d >= longest) break;
+    const bool add = lane - d >= start;
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-      const float y = __shfl_up_sync(0xffffffffu, v[j], d);
-      if (lane - d >= start) v[j] += y;
+    for (int j = 0; j + 1 < N; j += 2) {   // pairs of values: one packed f32x2 add
+      const float2 y = make_float2(__shfl_up_sync(0xffffffffu, v[j], d), __shfl_up_sync(0xffffffffu, v[j + 1], d));
+      if (add) {
+        const float2 r = __fadd2_rn(make_float2(v[j], v[j + 1]), y);
+        v[j] = r.x;
+        v[j + 1] = r.y;
+      }
+    }
+    if (N & 1) {
+      const float y = __shfl_up_sync(0xffffffffu, v[N - 1], d);
+      if (add) v[N - 1] += y;
     }
   }
   return lane == 31 || ((heads >> (lane + 1)) & 1u);

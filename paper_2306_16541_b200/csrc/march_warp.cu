@@ -229,7 +229,12 @@ __global__ void __launch_bounds__(128) k_warp_bwd(fv_warp w, float eps_w, const 
     const float wx[2] = {1.f - f[0], f[0]}, wy[2] = {1.f - f[1], f[1]}, wz[2] = {1.f - f[2], f[2]};
     float v[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = wx[c >> 2] * wy[(c >> 1) & 1] * wz[c & 1] * dw;
+    for (int q = 0; q < 4; ++q) {   // ((wx wy) wz) dw, the z-pair of each (x, y) corner as f32x2
+      const float t = wx[q >> 1] * wy[q & 1];
+      const float2 p = __fmul2_rn(__fmul2_rn(make_float2(t, t), make_float2(wz[0], wz[1])), make_float2(dw, dw));
+      v[2 * q] = p.x;
+      v[2 * q + 1] = p.y;
+    }
     const uint32_t key = any ? (uint32_t)vol_cell_index(i, G, i0) : (0xFFFFFFFFu - (uint32_t)lane);
     const bool lead = seg_sum<8>(v, key, lane) && any;
     if (lead) {
