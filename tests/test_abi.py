@@ -4,6 +4,8 @@ import ctypes
 import os
 import re
 
+import pytest
+
 from paper_2306_16541_b200 import _lib
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -41,3 +43,24 @@ def test_error_codes_map_to_reference_exceptions():
     lib = _lib.load()
     with pytest.raises(DimensionError):
         _lib.check(lib.fv_linear_fwd(None, None, None, None, -1, 0, 0, 0, None), "fv_linear_fwd")
+
+
+def test_no_cpu_fallback_missing_library_and_cpu_tensors(monkeypatch):
+    """The product path fails loudly: a missing libfvcuda.so raises (no silent CPU path), and
+    the operators refuse CPU tensors instead of computing on the host."""
+    import torch
+    from paper_2306_16541_b200 import autodiff, fused
+    from paper_2306_16541_b200.errors import DimensionError
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libfvcuda.so")
+    with pytest.raises(RuntimeError, match="not built"):
+        _lib.load()
+    monkeypatch.undo()
+    with pytest.raises(DimensionError):
+        autodiff.posenc(torch.zeros((4, 3)), 6)
+    with pytest.raises(DimensionError):
+        autodiff.transmittance(torch.zeros((2, 3)))
+    with pytest.raises(DimensionError):
+        fused.fused_forward(fused.FusedMlp([torch.zeros((3, 2))], [torch.zeros(2)]), torch.zeros((4, 3)))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.ptr(torch.zeros(3))
