@@ -29,6 +29,9 @@
 #ifndef FV_OFF_LEAD
 #define FV_OFF_LEAD 2
 #endif
+#ifndef FV_RAD_NL
+#define FV_RAD_NL 2   // hash levels per gather batch in k_radiance_tc
+#endif
 namespace fv {
 
 // ---- weight pack layout (bytes) ------------------------------------------------------
@@ -384,7 +387,7 @@ constexpr uint32_t RA_TCOLS_WG = 128;                    // TMEM columns per war
 // K_ACT activations (K_ACT/16 steps from A words 0..) + the bias step (A words 32..39).
 template <int K_ACT, int N>
 __device__ __forceinline__ void layer_mma_rad(uint32_t tcol, const uint8_t* Wt, uint64_t* bar, uint32_t& phase,
-                                              int t, int wg) {
+                                              int t, int wg, uint32_t bias_a) {
   tc::tmem_st_wait();
   tc::fence_before();
   named_bar(1 + wg, 128);
@@ -394,7 +397,7 @@ __device__ __forceinline__ void layer_mma_rad(uint32_t tcol, const uint8_t* Wt, 
     const uint32_t b0 = tc::smem_u32(Wt);
 #pragma unroll
     for (int k = 0; k <= K_ACT / 16; ++k) {
-      const uint32_t a = tcol + RA_TA + (k < K_ACT / 16 ? k * 8 : 32);
+      const uint32_t a = k < K_ACT / 16 ? tcol + RA_TA + k * 8 : bias_a;
       tc::mma_f16_ts(tcol, a, tc::make_desc(b0 + k * 2 * N * 16, N * 16, 128), idesc, k > 0 ? 1u : 0u);
     }
     tc::mma_commit(bar);
@@ -409,7 +412,10 @@ template <int NWG>
 __global__ void __launch_bounds__(NWG * 128, 1)
     k_radiance_tc(fv_field f, fv_hash h, const float4* __restrict__ xf, int64_t n, float eps_w,
                   float4* __restrict__ rgbs, const int32_t* __restrict__ d_count, const int32_t* __restrict__ idx) {
-  static_assert(NWG * RA_TCOLS_WG <= 512, "TMEM");
+  // <= 4 warpgroups: 128 columns each (D 64 | A 32 | own bias group 8); 5: 96 each (D | A)
+  // and one bias group shared by all at column 480 (it is the same constant in every row)
+  constexpr uint32_t WGC = NWG <= 4 ? RA_TCOLS_WG : 96;
+  static_assert(NWG * WGC + (NWG <= 4 ? 0 : 8) <= 512, "TMEM");
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[NWG];
   __shared__ uint32_t tmem_base;
@@ -419,13 +425,20 @@ __global__ void __launch_bounds__(NWG * 128, 1)
   tc_prologue_sync();
 
   const int warp = threadIdx.x >> 5, wg = threadIdx.x >> 7, t = threadIdx.x & 127;
-  const uint32_t tcol = tmem_base + wg * RA_TCOLS_WG;
+  const uint32_t tcol = tmem_base + wg * WGC;
   const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
   const uint32_t trow = tcol + lane;              // this thread's accumulator row
   const uint32_t arow = tcol + lane + RA_TA;      // ... and its A-operand row
-  {
+  const uint32_t bias_a = NWG <= 4 ? tcol + RA_TA + 32 : tmem_base + 480;
+  if (NWG <= 4 || wg == 0) {
     const uint32_t ones[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    tc::tmem_st8(arow + 32, ones);
+    tc::tmem_st8(NWG <= 4 ? arow + 32 : tmem_base + lane + 480, ones);
+  }
+  if (NWG > 4) {   // the shared bias group is written by warpgroup 0, read by every MMA
+    tc::tmem_st_wait();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
   }
   uint64_t* bar = &bars[wg];
   uint32_t phase = 0;
@@ -448,24 +461,28 @@ __global__ void __launch_bounds__(NWG * 128, 1)
       if (idx) onext = idx[s + tstep * 128];
     }
     const bool fg = s < n && v.w > eps_w;
-    {  // hash-grid features -> A words 0..15 (4 levels = 4 words per batch)
+    {  // hash-grid features -> A words 0..15 (NL levels = NL words per batch)
       float xn[3]; bool msk[3];
       hash_norm(h, fg ? v.x : 0.f, fg ? v.y : 0.f, fg ? v.z : 0.f, xn, msk);
+      constexpr int NL = FV_RAD_NL;       // levels whose 8 NL gathers per lane are in flight together
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float2 fv4[4];
-        hash_4levels_paired(h, 4 * c, xn, fv4);
-        uint32_t w[4];
+      for (int c = 0; c < 16 / NL; ++c) {
+        float2 fv[NL];
+        hash_levels_paired<NL>(h, NL * c, xn, fv);
+        uint32_t w[NL];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) w[q] = tc::pack_half2(fg ? fv4[q].x : 0.f, fg ? fv4[q].y : 0.f);
-        tc::tmem_st4(arow + 4 * c, w);
+        for (int q = 0; q < NL; ++q) w[q] = tc::pack_half2(fg ? fv[q].x : 0.f, fg ? fv[q].y : 0.f);
+        if constexpr (NL == 1) tc::tmem_st1(arow + NL * c, w);
+        else if constexpr (NL == 2) tc::tmem_st2(arow + NL * c, w);
+        else if constexpr (NL == 4) tc::tmem_st4(arow + NL * c, w);
+        else tc::tmem_st8(arow + NL * c, w);
       }
     }
-    layer_mma_rad<32, 64>(tcol, smem + (PK_RAD0 - PK_RAD0), bar, phase, t, wg);
+    layer_mma_rad<32, 64>(tcol, smem + (PK_RAD0 - PK_RAD0), bar, phase, t, wg, bias_a);
     epi_relu64_ts(trow, arow);
-    layer_mma_rad<64, 64>(tcol, smem + (PK_RAD1 - PK_RAD0), bar, phase, t, wg);
+    layer_mma_rad<64, 64>(tcol, smem + (PK_RAD1 - PK_RAD0), bar, phase, t, wg, bias_a);
     epi_relu64_ts(trow, arow);
-    layer_mma_rad<64, 16>(tcol, smem + (PK_RAD2 - PK_RAD0), bar, phase, t, wg);
+    layer_mma_rad<64, 16>(tcol, smem + (PK_RAD2 - PK_RAD0), bar, phase, t, wg, bias_a);
     float o[16];
     tc::tmem_ld16(trow, o);
     tc::tmem_ld_wait();
@@ -483,7 +500,10 @@ __global__ void __launch_bounds__(NWG * 128, 1)
 // Tuned configuration (round-1 sweeps on B200, SS4): residual MLP with 2
 // 8-warp teams per SM (all 512 TMEM columns; 124 KB of weights in smem), hash+radiance
 // with 4 warpgroups and 4-level batched gathers.
-constexpr int OFF_TEAMS = 2, RAD_NWG = 4;
+#ifndef FV_RAD_NWG
+#define FV_RAD_NWG 5   // warpgroups per CTA in k_radiance_tc (5 x 96 TMEM columns + shared bias group)
+#endif
+constexpr int OFF_TEAMS = 2, RAD_NWG = FV_RAD_NWG;
 
 static int sm_count() {
   int dev = 0, n_sm = 148;

@@ -353,18 +353,19 @@ __device__ __forceinline__ float2 hash_level_feat(const fv_hash& h, int l, const
   return acc;
 }
 
-// Lane-paired gathers of four levels (fp16 or fp32 table): lanes (2p, 2p+1) serve the
+// Lane-paired gathers of NL levels (fp16 or fp32 table): lanes (2p, 2p+1) serve the
 // samples of both lanes; lane parity a = lane & 1 fetches the x-corner a of each sample.  A
 // cell's two x-corners differ only in low index bits (same 128-byte line ~99% of the time),
 // so in one warp instruction 16 samples x 2 corners touch 16 lines instead of 32 -- half
-// the L1 wavefronts of the per-sample form at the same load count.  32 independent gathers
+// the L1 wavefronts of the per-sample form at the same load count.  8 NL independent gathers
 // are in flight per thread before any is consumed.  Corner indices are strength-reduced
 // (y+1 -> +PRIME_Y or +s, z+1 -> +PRIME_Z or +s^2, same uint32 arithmetic as hash_index)
 // and each lane blends its four corners as lerps (z, then y) scaled by its x weight; one
 // shuffle per feature adds the partner's partial.  The blend order differs from the
 // oracle's (a,b,c) sum by fp32 rounding only: used where features are rounded to fp16.
-__device__ __forceinline__ void hash_4levels_paired(const fv_hash& h, int l0, const float (&xn_self)[3],
-                                                    float2 (&out)[4]) {
+template <int NL>
+__device__ __forceinline__ void hash_levels_paired(const fv_hash& h, int l0, const float (&xn_self)[3],
+                                                   float2 (&out)[NL]) {
   const uint32_t maskT = (1u << h.log2_T) - 1u;
   const uint32_t a = threadIdx.x & 1u;
   // A = the even lane's sample, B = the odd lane's, for both lanes of a pair: each load
@@ -377,11 +378,11 @@ __device__ __forceinline__ void hash_4levels_paired(const fv_hash& h, int l0, co
     xB[j] = a ? xn_self[j] : other;
   }
   const float wsgn = a ? 1.f : -1.f, wbase = a ? 0.f : 1.f;   // w_x(a) = wbase + wsgn * f_x
-  uint32_t iA[16], iB[16];
-  uint32_t lofs[4];
-  float fA[4][3], fB[4][3];
+  uint32_t iA[4 * NL], iB[4 * NL];
+  uint32_t lofs[NL];
+  float fA[NL][3], fB[NL][3];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < NL; ++q) {
     const int l = l0 + q < h.n_levels ? l0 + q : h.n_levels - 1;
     const int res = h.res[l];
     lofs[q] = h.offset[l];
@@ -408,10 +409,10 @@ __device__ __forceinline__ void hash_4levels_paired(const fv_hash& h, int l0, co
       iB[q * 4 + 2] = (xb ^ yB1 ^ zB0) & maskT; iB[q * 4 + 3] = (xb ^ yB1 ^ zB1) & maskT;
     }
   }
-  float2 vA[16], vB[16];
+  float2 vA[4 * NL], vB[4 * NL];
   if (h.table_half) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NL; ++q) {
       const __half2* t = reinterpret_cast<const __half2*>(h.d_table) + lofs[q];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -421,14 +422,14 @@ __device__ __forceinline__ void hash_4levels_paired(const fv_hash& h, int l0, co
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NL; ++q) {
       const float2* t = reinterpret_cast<const float2*>(h.d_table) + lofs[q];
 #pragma unroll
       for (int k = 0; k < 4; ++k) { vA[q * 4 + k] = __ldg(t + iA[q * 4 + k]); vB[q * 4 + k] = __ldg(t + iB[q * 4 + k]); }
     }
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < NL; ++q) {
     // corners k = 2b + c of this lane's x-corner a: lerp in z (c), then y (b), scale by w_x(a)
     const float2* va = vA + q * 4;
     const float2* vb = vB + q * 4;
