@@ -377,9 +377,11 @@ __global__ void __launch_bounds__(TEAMS * 256, 1)
 // and the biases ride in the GEMM, so the only shared-memory traffic is the tensor core
 // reading the 17 KB of weights: the L1 data pipe is left to the table gathers, which
 // bound this kernel.  (The smem-A version spent ~25% of the pipe's wavefronts on the
-// MLP's STS/LDS.)  TMEM per warpgroup: D = columns [0, 64), A = [64, 104): features
-// (words 0..15) or hidden activations (words 0..31), then the shared bias group
-// (words 32..39 = (1, 1), 0, ...) that every layer's last K step reads.
+// MLP's STS/LDS.)  TMEM per warpgroup: D = columns [0, 64), A = [64, 96): features
+// (words 0..15) or hidden activations (words 0..31); the bias group (8 columns = (1, 1),
+// 0, ...) that every layer's last K step reads is one block at column 480 shared by all
+// warpgroups (5 x 96 + 8 <= 512; with <= 4 warpgroups each keeps its own at A + 32).
+// 5 warpgroups gathering 2 levels per batch beat 4 gathering 4 (more warps, 96 registers).
 constexpr uint32_t RA_SMEM = PK_WEND - PK_RAD0;          // 19456 B of weights
 constexpr uint32_t RA_TA = 64;                           // A-operand column offset
 constexpr uint32_t RA_TCOLS_WG = 128;                    // TMEM columns per warpgroup (104 used)
