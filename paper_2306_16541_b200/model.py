@@ -81,6 +81,7 @@ class FreeviewModel:
         self.g = torch.zeros((k, 12), device=self.device, dtype=torch.float32)
         self.pose_dev = torch.zeros(3 * k, device=self.device, dtype=torch.float32)
         self.b0_eff = torch.zeros(128, device=self.device, dtype=torch.float32)
+        self._pin, self._pin_ev, self._pin_slot = None, None, 0   # pinned pose-upload ring
         self.pe_alpha = float(PE_BANDS)
         self.offset_enabled = True
         self._pose: Optional[Pose] = None
@@ -164,19 +165,42 @@ class FreeviewModel:
         _lib.check(self.lib.fv_warp_pack(self.vol.data_ptr(), self.n_bones + 1, C.byref(w),
                                          self.vol_packed.data_ptr(), st), "fv_warp_pack")
 
+    def _upload_pose(self, g_packed: np.ndarray, pose_vec: np.ndarray, stream=None) -> None:
+        """G_i and the pose vector -> device through a 2-slot pinned staging ring with
+        asynchronous copies: the host computes the next frame's motion bases while the GPU
+        still renders the current one (a pageable copy would wait for it)."""
+        if self._pin is None:
+            self._pin = [torch.empty(self.g.numel() + self.pose_dev.numel(), dtype=torch.float32,
+                                     pin_memory=True) for _ in range(2)]
+            self._pin_ev = [None, None]
+        k = self._pin_slot
+        self._pin_slot ^= 1
+        if self._pin_ev[k] is not None:
+            self._pin_ev[k].synchronize()          # the copy that last used this slot is done
+        buf = self._pin[k]
+        ng = self.g.numel()
+        buf[:ng].numpy()[:] = g_packed.reshape(-1)
+        buf[ng:].numpy()[:] = pose_vec.reshape(-1)
+        st = torch.cuda.current_stream() if stream is None else stream
+        with torch.cuda.stream(st):
+            self.g.view(-1).copy_(buf[:ng], non_blocking=True)
+            self.pose_dev.copy_(buf[ng:], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+        self._pin_ev[k] = ev
+
     def set_pose(self, pose: Pose, stream=None) -> None:
         """Upload the frame's motion bases G_i and fold the pose into the residual bias."""
         g_r, g_t = motion_basis(self.scene.skeleton, pose)
-        self.g.copy_(torch.from_numpy(pack_g(g_r, g_t)), non_blocking=False)
-        self.pose_dev.copy_(torch.from_numpy(pose.flat().astype(np.float32)))
+        self._upload_pose(pack_g(g_r, g_t), pose.flat().astype(np.float32), stream)
         self._pose = pose
         self._fold_pose(_lib.stream_ptr(stream))
 
     def set_pose_bases(self, g_r: np.ndarray, g_t: np.ndarray, pose_vec: np.ndarray, stream=None) -> None:
         """Upload given motion bases and pose vector (e.g. of a refined pose) and fold the
         pose into the residual bias; the refined pose is remembered for refresh()."""
-        self.g.copy_(torch.from_numpy(pack_g(np.asarray(g_r), np.asarray(g_t))), non_blocking=False)
-        self.pose_dev.copy_(torch.from_numpy(np.asarray(pose_vec, np.float32).reshape(-1)))
+        self._upload_pose(pack_g(np.asarray(g_r), np.asarray(g_t)), np.asarray(pose_vec, np.float32).reshape(-1),
+                          stream)
         self._pose = Pose(np.asarray(pose_vec, np.float64).reshape(-1, 3), np.zeros(3))
         self._fold_pose(_lib.stream_ptr(stream))
 
