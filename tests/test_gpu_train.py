@@ -14,7 +14,7 @@ from oracle import pipeline as opipe
 from oracle import warp as owarp
 from oracle.adapter import settings as osettings
 from paper_2306_16541_b200 import _lib
-from paper_2306_16541_b200.errors import TrainingError
+from paper_2306_16541_b200.errors import DimensionError, TrainingError
 from paper_2306_16541_b200.model import FreeviewModel
 from paper_2306_16541_b200.render import RenderSettings
 from paper_2306_16541_b200.scene import target_image
@@ -171,6 +171,16 @@ def test_hash_bwd_matches_oracle():
     rtab, rdx = oenc.hash_encode_bwd(osc["hash_spec"], x, osc["wbox_min"], cinv, osc["table"], g)
     _close(dtab.cpu().numpy(), rtab, 1e-5, "dtable")
     _close(dx.cpu().numpy(), rdx, 1e-4, "dx")
+    # a table-gradient buffer only 8-byte aligned takes the v2-reduction path (no v4 pairs)
+    buf = torch.zeros(dtab.numel() + 2, device=DEV)
+    dtab8 = buf[2:]
+    assert (dtab8.data_ptr() % 16) == 8
+    _lib.check(nets.lib.fv_hash_bwd(C.byref(h), _t(x).data_ptr(), 4000, _t(g).data_ptr(), dtab8.data_ptr(),
+                                    dx.data_ptr(), _lib.stream_ptr()))
+    _close(dtab8.cpu().numpy(), rtab.reshape(-1), 1e-5, "dtable (8-byte aligned)")
+    with pytest.raises(DimensionError):      # 4-byte aligned gradient buffer: refused
+        _lib.check(nets.lib.fv_hash_bwd(C.byref(h), _t(x).data_ptr(), 4000, _t(g).data_ptr(),
+                                        buf[1:].data_ptr(), dx.data_ptr(), _lib.stream_ptr()))
 
 
 def test_warp_bwd_matches_oracle():
