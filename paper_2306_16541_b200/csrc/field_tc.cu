@@ -196,14 +196,28 @@ __device__ __forceinline__ void layer_mma_ts(uint32_t tcol, const uint8_t* Wt, u
 }
 
 // 64 accumulator columns -> ReLU -> fp16 pairs -> 32 A-operand columns
+// WIDE: two 32-column loads (offset kernel) instead of four 16-column ones (the radiance
+// kernel at 96 registers spills with the wide form)
+template <bool WIDE = false>
 __device__ __forceinline__ void epi_relu64_ts(uint32_t dsrc, uint32_t adst) {
-  float v[4][16];
+  if constexpr (!WIDE) {
+    float v[4][16];
 #pragma unroll
-  for (int g = 0; g < 4; ++g) tc::tmem_ld16(dsrc + g * 16, v[g]);
+    for (int g = 0; g < 4; ++g) tc::tmem_ld16(dsrc + g * 16, v[g]);
+    tc::tmem_ld_wait();
+    uint32_t w[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) w[j] = cvt_relu_h2(v[j >> 3][2 * (j & 7)], v[j >> 3][2 * (j & 7) + 1]);
+    tc::tmem_st32(adst, w);
+    return;
+  }
+  float v[2][32];
+  tc::tmem_ld32(dsrc, v[0]);
+  tc::tmem_ld32(dsrc + 32, v[1]);
   tc::tmem_ld_wait();
   uint32_t w[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) w[j] = cvt_relu_h2(v[j >> 3][2 * (j & 7)], v[j >> 3][2 * (j & 7) + 1]);
+  for (int j = 0; j < 32; ++j) w[j] = cvt_relu_h2(v[j >> 4][2 * (j & 15)], v[j >> 4][2 * (j & 15) + 1]);
   tc::tmem_st32(adst, w);
 }
 
@@ -336,7 +350,7 @@ __global__ void __launch_bounds__(TEAMS * 256, 1)
     });
     lead();
     if (sprev >= 0 && half == 0) emit(vprev, sprev);
-    epi_relu64_ts(dsrc, adst);
+    epi_relu64_ts<true>(dsrc, adst);
     layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF1, bar, phase, tt, team, [&] {
       const int64_t s1 = s + tstep * 128, s2 = s1 + tstep * 128;
       uint32_t pw[12];
@@ -347,13 +361,13 @@ __global__ void __launch_bounds__(TEAMS * 256, 1)
       vnext = s2 < n ? xs[s2] : zero4;
     });
     lead();
-    epi_relu64_ts(dsrc, adst);
+    epi_relu64_ts<true>(dsrc, adst);
     layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF2, bar, phase, tt, team);
     lead();
-    epi_relu64_ts(dsrc, adst);
+    epi_relu64_ts<true>(dsrc, adst);
     layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF3, bar, phase, tt, team);
     lead();
-    epi_relu64_ts(dsrc, adst);
+    epi_relu64_ts<true>(dsrc, adst);
     const bool fg = s < n && v.w > eps_w;
     vprev = fg ? v : make_float4(0.f, 0.f, 0.f, v.w);
     sprev = s;
