@@ -48,45 +48,109 @@ def parse():
 
 
 # ------------------------------------------------------------------------------ CPU side
+#
+# The CPU baseline times the reference's algorithm (the numpy oracle restating the reference
+# primitives) the way the reference's own benchmark times its evaluator
+# (fu:260-299): setup outside the timer, plain float32 arithmetic, median over repeats.
+# Each worker process builds its scene once (pool initializer, before any timer starts);
+# the timed region is only render_rays over disjoint ray tiles.
 
-def _cpu_worker(args):
-    name, pix, seed = args
+_CPU = {}
+
+
+def _cpu_init(name, seed):
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except ImportError:
+        pass
     from oracle import camera as ocam
-    from oracle import pipeline as opipe
+    from oracle import warp as owarp
     from oracle.adapter import scene_arrays, settings
     from paper_2306_16541_b200 import scene as psc
+    owarp.EXACT_FMA = False            # plain float32 numpy (the FMA emulation is for parity only)
     sc = psc.make_scene(psc.config(name))
-    osc = scene_arrays(sc, 0)
-    cc = ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera)
-    st = settings(sc.cfg, seed=seed)
-    r = opipe.render_rays(osc, cc, pix, sc.cfg.width, st, np.float32)
+    _CPU.update(osc=scene_arrays(sc, 0), cc=ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera),
+                st=settings(sc.cfg, seed=seed), width=sc.cfg.width)
+
+
+def _cpu_render(pix):
+    from oracle import pipeline as opipe
+    r = opipe.render_rays(_CPU["osc"], _CPU["cc"], pix, _CPU["width"], _CPU["st"], np.float32)
     return len(pix), float(r["rgb"].sum())
 
 
-def cpu_rays_per_s(name, tiles, cores=None):
-    """Oracle (the reference's algorithm in numpy) on `tiles` 64x64 pixel tiles of the frame,
-    split over `cores` worker processes; returns (rays/s, cores, sample description)."""
-    import multiprocessing as mp
-    from paper_2306_16541_b200 import scene as psc
-    cfg = psc.config(name)
-    cores = cores or os.cpu_count()
-    rays = []
-    for t in range(tiles):
-        ty, tx = divmod(t, max(cfg.width // 64, 1))
-        y0, x0 = (cfg.height // 2 - 32 + 64 * (ty - tiles // 4)) % cfg.height, (cfg.width // 2 - 32 + 64 * tx) % cfg.width
-        yy, xx = np.meshgrid(np.arange(y0, y0 + 64) % cfg.height, np.arange(x0, x0 + 64) % cfg.width, indexing="ij")
-        rays.append((yy * cfg.width + xx).reshape(-1))
-    pix = np.concatenate(rays)
-    chunks = np.array_split(pix, cores * 2)
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(cores) as pool:
-        out = pool.map(_cpu_worker, [(name, c, 77) for c in chunks])
-    dt = time.perf_counter() - t0
-    n = sum(o[0] for o in out)
-    sample = f"{tiles} x (64x64) ray tiles of the {cfg.width}x{cfg.height} frame, {cfg.n_samples} samples/ray, numpy float32 oracle, {cores} processes"
-    return n / dt, cores, sample
+def cpu_model_name():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+class CpuBaseline:
+    """A pool of ``cores`` oracle workers over 64x64 ray tiles of the config's frame; the pool
+    and every worker's scene are built in the constructor, outside any timed region."""
+
+    def __init__(self, name, tiles, cores=None, seed=77):
+        import multiprocessing as mp
+        from paper_2306_16541_b200 import scene as psc
+        cfg = psc.config(name)
+        self.cfg, self.tiles = cfg, tiles
+        self.cores = cores or os.cpu_count()
+        rays = []
+        for t in range(tiles):
+            ty, tx = divmod(t, max(cfg.width // 64, 1))
+            y0 = (cfg.height // 2 - 32 + 64 * (ty - tiles // 4)) % cfg.height
+            x0 = (cfg.width // 2 - 32 + 64 * tx) % cfg.width
+            yy, xx = np.meshgrid(np.arange(y0, y0 + 64) % cfg.height, np.arange(x0, x0 + 64) % cfg.width,
+                                 indexing="ij")
+            rays.append((yy * cfg.width + xx).reshape(-1))
+        self.pix = np.concatenate(rays)
+        self.chunks = np.array_split(self.pix, self.cores * 2)
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_cpu_init, initargs=(name, seed))
+        self.pool.map(_cpu_render, [c[:2] for c in self.chunks[:self.cores]])     # workers warm
+        self.sample = (f"{tiles} x (64x64) ray tiles of the {cfg.width}x{cfg.height} frame, {cfg.n_samples} "
+                       f"samples/ray, numpy float32 oracle (plain float32 arithmetic), {self.cores} processes x "
+                       f"1 BLAS thread, scene built once per worker outside the timer")
+
+    def rays_per_s(self):
+        t0 = time.perf_counter()
+        out = self.pool.map(_cpu_render, self.chunks)
+        dt = time.perf_counter() - t0
+        return sum(o[0] for o in out) / dt
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def naive_forward_throughput(batch=65536, depth=4, repeats=5):
+    """BASELINE.md §3 "MLP only": the reference's naive_forward (fu:132-142: h @ w + b, ReLU,
+    restated in oracle.mlp) on FusedMlp.random(64, 64, depth) weights (fu:120-130 draws) at
+    batch 65,536, all BLAS threads of the host, median of ``repeats`` (fu:276-298)."""
+    from oracle import mlp as omlp
+    rng = np.random.default_rng(0)
+    dims = [64] + [64] * depth + [64]
+    ws, bs = [], []
+    for a, b in zip(dims[:-1], dims[1:]):
+        ws.append((rng.standard_normal((a, b)) * np.sqrt(2.0 / a)).astype(np.float32))
+        bs.append((rng.standard_normal(b) * 0.01).astype(np.float32))
+    x = rng.standard_normal((batch, 64)).astype(np.float32)
+    omlp.mlp_forward(x, ws, bs, np.float32)
+    ts = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        omlp.mlp_forward(x, ws, bs, np.float32)
+        ts.append(time.perf_counter() - t0)
+    return {"metric": "naive_forward inputs/s", "value": batch / float(np.median(ts)), "batch": batch,
+            "width": 64, "depth": depth, "threads": os.cpu_count(),
+            "what": "fu:132-142 naive_forward (oracle.mlp restatement), float32 numpy/OpenBLAS, median of "
+                    f"{repeats}"}
 
 
 def run_reference(args, rank, world):
@@ -94,22 +158,25 @@ def run_reference(args, rank, world):
         return
     from paper_2306_16541_b200 import scene as psc
     cfg = psc.config(args.config)
+    base = CpuBaseline(args.config, args.cpu_tiles)
     for _ in range(args.warmup):
-        cpu_rays_per_s(args.config, 1)
+        base.rays_per_s()
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, cores, sample = cpu_rays_per_s(args.config, args.cpu_tiles)
-        vals.append(v)
+        vals.append(base.rays_per_s())
     wall = time.perf_counter() - t0
-    value = float(np.mean(vals))
+    base.close()
+    value = float(np.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * wall / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded BASELINE config stand-in)",
             "config": {"workload": f"{args.config}: {cfg.width}x{cfg.height} frame, {cfg.n_samples} samples/ray",
-                       "frames_per_s": value / (cfg.width * cfg.height)},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+                       "frames_per_s": value / (cfg.width * cfg.height),
+                       "frames_per_s_note": "extrapolated from the timed tiles (rays are independent)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": base.cores, "kind": "port", "sample": base.sample,
+                             "cpu_model": cpu_model_name(), "timing": "median over steps (fu:276-298)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -275,8 +342,12 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and not args.skip_cpu_baseline:
-        v, cores, sample = cpu_rays_per_s(name, args.cpu_tiles)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        base = CpuBaseline(name, args.cpu_tiles)
+        v = float(np.median([base.rays_per_s() for _ in range(3)]))
+        base.close()
+        cpu = {"value": v, "unit": UNIT, "cores": base.cores, "kind": "port", "sample": base.sample,
+               "cpu_model": cpu_model_name(), "timing": "median of 3 (fu:276-298)",
+               "naive_forward": naive_forward_throughput(), "fused_forward_gpu": fused_mlp_throughput(dev)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -429,8 +500,21 @@ def scene_throughput(args, rank, world, dev):
     poses = [s.poses[0] for s in ms.subjects]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
+    frame = torch.empty((cam.height, cam.width, 4), dtype=torch.float32, device=dev)
+
+    def render_frame():
+        """This rank's tile bands, then (N > 1) the all-gather that assembles the full RGBA
+        frame on every rank -- the frame is only complete after the exchange."""
+        img, alpha = r.render_scene(nets, ms, st, bg, poses=poses, rows=rows)
+        if world > 1:
+            frame[..., :3].copy_(img)
+            frame[..., 3].copy_(alpha)
+            shard.gather_row_bands(frame, world, rank)
+            return frame[..., :3], frame[..., 3]
+        return img, alpha
+
     for _ in range(max(3, args.warmup)):
-        r.render_scene(nets, ms, st, bg, poses=poses, rows=rows)
+        render_frame()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -440,7 +524,7 @@ def scene_throughput(args, rank, world, dev):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        r.render_scene(nets, ms, st, bg, poses=poses, rows=rows)
+        render_frame()
         b.record(stream)
         times.append((a, b))
     torch.cuda.synchronize()
@@ -450,9 +534,9 @@ def scene_throughput(args, rank, world, dev):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
-        img, alpha = r.render_scene(nets, ms, st, bg, poses=poses, rows=rows)
-        host[:, :3].copy_(img.view(-1, 3), non_blocking=True)
-        host[:, 3].copy_(alpha.view(-1), non_blocking=True)
+        img, alpha = render_frame()
+        host[:, :3].copy_(img.reshape(-1, 3), non_blocking=True)
+        host[:, 3].copy_(alpha.reshape(-1), non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / steps
@@ -468,8 +552,31 @@ def scene_throughput(args, rank, world, dev):
             "samples_per_ray_per_subject": ms.cfg.n_samples,
             "workload": "c5: 4 subjects (own T=2^19 grids/skeletons/MLPs) at seeded offsets in a 4 m scene, "
                         "1024x1024, 192 jittered samples/ray per subject box, occupancy per pose, fp16 tcgen05 "
-                        "MLPs, depth-ordered joint compositing" + (f", tile bands over {world} GPUs" if world > 1 else ""),
+                        "MLPs, depth-ordered joint compositing" + (f", tile bands over {world} GPUs + NCCL all-gather of the "
+                                                                   "RGBA rows inside the timed frame" if world > 1 else ""),
             "l2": "flushed (256 MB write) before every timed frame"}
+
+
+def fused_mlp_throughput(dev, batch=65536, depth=4, reps=20):
+    """fused_forward (fv_fused_mlp_fwd, one launch) on the same MLP shape / batch as the
+    CPU naive_forward number: FusedMlp.random(64, 64, depth), batch 65,536, device time."""
+    import torch
+    from paper_2306_16541_b200 import fused
+    mlp = fused.FusedMlp.random(64, 64, depth=depth, seed=0, device=str(dev))
+    x = torch.randn((batch, 64), device=dev)
+    for _ in range(3):
+        fused.fused_forward(mlp, x)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fused.fused_forward(mlp, x)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    flop = 2.0 * batch * 64 * 64 * (depth + 1)
+    return {"metric": "fused_forward inputs/s", "value": batch / (ms * 1e-3), "batch": batch, "width": 64,
+            "depth": depth, "ms": ms, "tflops": flop / (ms * 1e-3) / 1e12,
+            "what": "fv_fused_mlp_fwd: all layers' weights in smem, 128-row chunks on chip, fp32 FMA"}
 
 
 def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5, occ_grid=None):
@@ -535,14 +642,45 @@ def occupancy_variants(nets, rnd, cam, st, dev, reps=5):
     return out
 
 
+def _free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def self_launch(args):
+    """``python bench.py --gpus N`` without a launcher: re-exec under torch.distributed.run
+    with N ranks (one per GPU, NCCL, rendezvous on 127.0.0.1); rank 0 prints the line.  A
+    box with fewer than N GPUs fails loudly (FV_BENCH_SINGLE_GPU=1 runs the N ranks on GPU 0
+    over gloo: a functional check of the multi-rank code, not a measurement)."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus and os.environ.get("FV_BENCH_SINGLE_GPU") != "1":
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible\n")
+        sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    launched = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if not launched and args.gpus > 1:
+        self_launch(args)
+        return
+    if launched and world != args.gpus:
+        sys.stderr.write(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        sys.exit(2)
     if os.environ.get("FV_BENCH_SINGLE_GPU") == "1":
         # functional check of the multi-rank code paths on a one-GPU box: every rank on
         # device 0, gloo collectives (host-mediated; no rank's kernel waits on another's).
@@ -552,7 +690,9 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("gloo" if os.environ.get("FV_BENCH_SINGLE_GPU") == "1" else "nccl")
+        dist.init_process_group("gloo" if os.environ.get("FV_BENCH_SINGLE_GPU") == "1" else "nccl",
+                                device_id=None if os.environ.get("FV_BENCH_SINGLE_GPU") == "1"
+                                else torch.device("cuda", local_rank))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

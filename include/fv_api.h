@@ -12,8 +12,9 @@
  *    library never allocates or frees device memory (workspaces are caller-provided);
  *  - `stream` is a cudaStream_t passed as void*; all work is enqueued on it, nothing
  *    synchronises unless the function says so;
- *  - no hidden global state: per-call constants travel in the parameter structs, so
- *    calls on different streams / host threads are independent;
+ *  - no hidden shared state: per-call constants travel in the parameter structs, so calls
+ *    on different streams / host threads are independent; the only library state is the
+ *    thread-local message fv_last_error() returns (per host thread, never shared);
  *  - return value: FV_OK or one of the FV_E* codes; the Python layer maps
  *    FV_EDIM -> DimensionError, FV_ENONFINITE -> TrainingError, others -> RuntimeError.
  */
@@ -131,6 +132,12 @@ int32_t fv_warp_fwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t 
  * the one-voxel-padded grid.  Same trilinear sample as inside fv_warp_fwd. */
 int32_t fv_sample_bone_channels(const fv_warp* warp, const float* d_pts, int64_t n, float* d_out, void* stream);
 
+/* Backward of fv_sample_bone_channels (ad:775-806) for upstream g (K,n): d vol (C,G,G,G) fp32
+ * accumulated (trilinear-weight scatter, atomics; may be NULL) and d pts (K,n,3) written
+ * (may be NULL); points outside the padded grid get zero gradient. */
+int32_t fv_sample_bone_channels_bwd(const fv_warp* warp, const float* d_pts, int64_t n, const float* d_g,
+                                    float* d_dvol, float* d_dpts, void* stream);
+
 /* d x_skel (n,3) -> d W^c (C,G,G,G) fp32 (accumulated, atomics).  ad:775-789 + Eq 9. */
 int32_t fv_warp_bwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
                     const float* d_dxskel, float* d_dvol, void* stream);
@@ -148,6 +155,14 @@ int32_t fv_hash_fwd(const fv_hash* hash, const float* d_x, int64_t n, float* d_f
 int32_t fv_hash_bwd(const fv_hash* hash, const float* d_x, int64_t n, const float* d_dfeat,
                     float* d_dtable, float* d_dx, void* stream);
 
+/* Verification entry for the production gather path: the lane-paired, strength-reduced
+ * index arithmetic k_radiance_tc uses (hash_levels_paired) on canonical points x (n,3) ->
+ * every corner's global table index (n, L, 8) and the blended features (n, 2L).  Lets the
+ * bit-exact index bar be checked on the path the headline render runs, not only on
+ * fv_hash_fwd's separate scalar form. */
+int32_t fv_hash_index_paired(const fv_hash* hash, const float* d_x, int64_t n, uint32_t* d_index,
+                             float* d_feat, void* stream);
+
 /* ---- MLPs (ad:403-425; fu:132-227) ---------------------------------------------------- */
 
 /* Dense fp32 layer y = act(x @ W + b), W (k_in, n_out) row-major; act 0 none, 1 relu. */
@@ -158,6 +173,14 @@ int32_t fv_linear_fwd(const float* d_x, const float* d_w, const float* d_b, floa
 int32_t fv_linear_bwd(const float* d_x, const float* d_w, const float* d_y, const float* d_dy,
                       float* d_dx, float* d_dw, float* d_db, int64_t m, int32_t k_in,
                       int32_t n_out, int32_t act, void* stream);
+
+/* fused_forward (fu:145-193): the reference's fixed-width MLP (n_layers 2..8; weights[l]
+ * (in_l, out_l) row-major device pointers in a HOST array, widths in_dim -> 64 -> ... -> 64 ->
+ * out_dim, in/out <= 64; biases[l] device pointers or a NULL array) on x (m, in_dim) ->
+ * y (m, out_dim), ReLU on all but the last layer.  One launch: all weights resident in
+ * shared memory, 128-row chunks with on-chip activations, fp32 FMAs in fixed order. */
+int32_t fv_fused_mlp_fwd(const float* d_x, int64_t m, int32_t in_dim, int32_t out_dim, int32_t n_layers,
+                         const float* const* d_w, const float* const* d_b, float* d_y, void* stream);
 
 /* Pack the fp32 field weights into the fp16 tcgen05 operand layout (+ fp32 biases).
  * Workspace d_tc_pack must hold fv_field_pack_bytes() bytes. */
@@ -183,9 +206,13 @@ int32_t fv_field_fwd(const fv_field* field, const fv_hash* hash, const float* d_
 
 /* ---- compositing (ad:815-837) ---------------------------------------------- */
 
-/* transmittance (reference freeview.autodiff, ad:815-837): alpha (R,N) -> T (R,N+1),
- * T[r,0] = 1, T[r,i+1] = T[r,i] (1 - alpha[r,i]) in fp32 (exclusive running product). */
-int32_t fv_transmittance(const float* d_alpha, int64_t n_rays, int32_t n_samples, float* d_trans, void* stream);
+/* transmittance (reference freeview.autodiff, ad:815-837): attenuations atten (R,N) = 1 - opacity
+ * -> T (R,N+1), T[r,0] = 1, T[r,i+1] = T[r,i] atten[r,i] in fp32 (exclusive running product). */
+int32_t fv_transmittance(const float* d_atten, int64_t n_rays, int32_t n_samples, float* d_trans, void* stream);
+/* Its division-free reverse scan (ad:828-835): upstream g (R,N+1) and the forward's T ->
+ * d atten (R,N) (written, not accumulated); exact zeros in atten are safe. */
+int32_t fv_transmittance_bwd(const float* d_atten, const float* d_trans, const float* d_g, int64_t n_rays,
+                             int32_t n_samples, float* d_gatten, void* stream);
 
 /* rays r (R), N samples each: rgbs (R*N,4) [rgb, sigma], delta (R*N), lik (R*N)
  * -> rgb (R,3), alpha (R); optional T (R,N+1) for backward.  Sample layout: ray-major
@@ -267,6 +294,15 @@ int32_t fv_march_warp(const fv_camera* cam, const fv_march* march, const fv_warp
                       int64_t n_rays, float* d_xs, float* d_delta, float* d_x,
                       int32_t* d_count, void* stream);
 
+/* The render path's own march + foreground compaction (what fv_render_fwd launches first):
+ * per sample slot (ray-block-major, R padded to 32) lik (L, 0 where skipped), delta, and
+ * optional flags (uint8: 1 ray hits the box, 2 occupancy cell on or no grid, 4 L > eps_w);
+ * the compacted foreground stream xsc (<= S, 4) = [x_skel, L] with its slot ids idx and its
+ * length *d_n_fg (device int32); per-ray sample counts d_count (may be NULL). */
+int32_t fv_march_compact(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays,
+                         float* d_lik, float* d_delta, float* d_xsc, int32_t* d_idx, int32_t* d_n_fg,
+                         int32_t* d_count, uint8_t* d_flags, void* stream);
+
 /* Full forward: rays -> rgb (3 floats) and alpha per ray (or per pixel, out_by_pixel),
  * per-ray sample counts (may be NULL).  d_work >= fv_render_workspace_bytes(). */
 int32_t fv_render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp* warp,
@@ -300,6 +336,10 @@ int32_t fv_occupancy_build(const fv_march* march, const fv_warp* warp, const fv_
                            size_t work_bytes, uint32_t* d_occ, void* stream);
 
 /* ---- Adam (ad:880-912) ---------------------------------------------------------------- */
+
+/* Sets *d_flag (device int32) to `code` (!= 0; first writer wins) if any of x[0..n) is not
+ * finite -- the per-block check adam_step makes before touching any parameter (ad:898-902). */
+int32_t fv_check_finite(const float* d_x, int64_t n, int32_t code, int32_t* d_flag, void* stream);
 
 /* In-place bias-corrected Adam over n params; lr per segment: seg_end (n_seg) exclusive
  * end offsets, lr (n_seg).  Writes an fp16 copy of [half_begin, half_end) into d_half

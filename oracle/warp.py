@@ -35,8 +35,16 @@ _XP = np.longdouble
 assert np.finfo(_XP).nmant >= 63, "fma32 needs x87 extended precision (x86-64 long double)"
 
 
+# True (parity): fma32 rounds once, bit-exact with the kernel.  bench.py's CPU-baseline
+# workers set it False: plain float32 numpy (a*b, then + c) -- the speed a straightforward
+# float32 port of the reference algorithm runs at, without the x87 emulation cost.
+EXACT_FMA = True
+
+
 def fma32(a, b, c):
     """float32 a*b + c with a single rounding (CUDA ``__fmaf_rn``)."""
+    if not EXACT_FMA:
+        return np.asarray(a, np.float32) * np.asarray(b, np.float32) + np.asarray(c, np.float32)
     return (np.asarray(a, np.float32).astype(_XP) * np.asarray(b, np.float32).astype(_XP)
             + np.asarray(c, np.float32).astype(_XP)).astype(np.float32)
 

@@ -2,10 +2,12 @@
 
 Public API (mirrors the reference ``freeview`` package and its SPEC):
   render.render_image / Renderer / RenderSettings
-  render.skeleton_warp / warp_point / query_radiance / composite
+  render.skeleton_warp / warp_point / query_radiance / composite / stratified_sample
   model.FreeviewModel                                  the "nets"
-  train.Trainer                                        S:505-513 (patch training step)
-  ops.sample_bone_channels / posenc / transmittance / adam_step / fused_forward
+  train.train(dataset, config) / Trainer / TrainConfig S:505-513 (patch training)
+  autodiff.sample_bone_channels / posenc / transmittance / softmax0 / linear /
+           AdamState / adam_step                       ad:403-912 (torch.autograd, CUDA fwd+bwd)
+  fused.FusedMlp / fused_forward / naive_forward       fu:64-193
 """
 
 __version__ = "0.1.0"

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfvcuda.so")
 
 FV_OK, FV_EDIM, FV_ENONFINITE, FV_ELAUNCH, FV_EUNSUPPORTED = 0, 1, 2, 3, 4
-MAX_BONES, MAX_LEVELS = 32, 16
+MAX_BONES, MAX_LEVELS, MAX_VOL_RES = 32, 16, 128
 
 f3 = C.c_float * 3
 vp = C.c_void_p
@@ -77,8 +77,11 @@ SIGNATURES = {
     "fv_warp_bwd_g": (i32, [P(FvWarp), f32, vp, i64, vp, vp, vp, vp]),
     "fv_hash_fwd": (i32, [P(FvHash), vp, i64, vp, vp, vp]),
     "fv_hash_bwd": (i32, [P(FvHash), vp, i64, vp, vp, vp, vp]),
+    "fv_hash_index_paired": (i32, [P(FvHash), vp, i64, vp, vp, vp]),
+    "fv_march_compact": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "fv_linear_fwd": (i32, [vp, vp, vp, vp, i64, i32, i32, i32, vp]),
     "fv_linear_bwd": (i32, [vp, vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp]),
+    "fv_fused_mlp_fwd": (i32, [vp, i64, i32, i32, i32, vp, vp, vp, vp]),
     "fv_field_pack_bytes": (sz, []),
     "fv_field_pack": (i32, [P(FvField), vp, vp]),
     "fv_offset_bias": (i32, [P(FvField), vp, i32, vp, vp]),
@@ -93,6 +96,8 @@ SIGNATURES = {
     "fv_linear_fwd_tc_bits": (i32, [vp, i64, vp, vp, vp, i64, i64, i32, i32, i32, vp, vp]),
     "fv_sample_bone_channels": (i32, [P(FvWarp), vp, i64, vp, vp]),
     "fv_transmittance": (i32, [vp, i64, i32, vp, vp]),
+    "fv_transmittance_bwd": (i32, [vp, vp, vp, i64, i32, vp, vp]),
+    "fv_sample_bone_channels_bwd": (i32, [P(FvWarp), vp, i64, vp, vp, vp, vp]),
     "fv_linear_bwd_tc_bits": (i32, [vp, i64, vp, vp, i64, vp, i64, vp, vp, vp, i64, i32, i32, vp]),
     "fv_posenc_bwd": (i32, [vp, i64, f32, i32, P(f32), vp, i64, vp, vp]),
     "fv_xfinal": (i32, [vp, vp, i64, f32, vp, vp]),
@@ -111,6 +116,7 @@ SIGNATURES = {
                                   vp, vp, P(f32), P(i64), vp]),
     "fv_occupancy_workspace_bytes": (sz, [i32]),
     "fv_occupancy_build": (i32, [P(FvMarch), P(FvWarp), P(FvHash), P(FvField), f32, vp, sz, vp, vp]),
+    "fv_check_finite": (i32, [vp, i64, i32, vp, vp]),
     "fv_adam_step": (i32, [vp, vp, vp, vp, i64, P(i64), P(f32), i32, i32, f32, f32, f32, vp, i64, i64,
                            vp, vp]),
 }

@@ -94,9 +94,25 @@ __global__ void k_adam_update(float* __restrict__ p, const float* __restrict__ g
   }
 }
 
+// Set *flag to `code` (first writer wins) if any of x[0..n) is non-finite.
+__global__ void k_check_finite(const float* __restrict__ x, int64_t n, int32_t code, int32_t* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[e]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicCAS(flag, 0, code);
+}
+
 }  // namespace fv
 
 using namespace fv;
+
+extern "C" int32_t fv_check_finite(const float* d_x, int64_t n, int32_t code, int32_t* d_flag, void* stream) {
+  if (n < 0 || !d_flag || code == 0 || (n > 0 && !d_x)) return set_error(FV_EDIM, "fv_check_finite: bad arguments");
+  if (n == 0) return FV_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_check_finite<<<grid, 256, 0, (cudaStream_t)stream>>>(d_x, n, code, d_flag);
+  return check_launch("fv_check_finite");
+}
 
 extern "C" int32_t fv_adam_step(float* d_param, const float* d_grad, float* d_m, float* d_v, int64_t n,
                                 const int64_t* seg_end, const float* lr, int32_t n_seg, int32_t step, float beta1,

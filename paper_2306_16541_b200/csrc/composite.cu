@@ -155,30 +155,58 @@ int32_t composite_bwd(const CompIn& in, const float* trans, int64_t n_rays, int 
 using namespace fv;
 
 namespace fv {
-// transmittance (ad:815-837): T[r, 0] = 1, T[r, i + 1] = T[r, i] * (1 - alpha[r, i]) in fp32,
-// the exclusive running product of the per-sample opacities (one thread per ray).
-__global__ void k_transmittance(const float* __restrict__ alpha, int64_t R, int N, float* __restrict__ T) {
+// transmittance (ad:815-837): T[r, 0] = 1, T[r, i + 1] = T[r, i] * atten[r, i] in fp32, the
+// exclusive running product of the per-sample attenuations 1 - opacity (one thread per ray).
+__global__ void k_transmittance(const float* __restrict__ atten, int64_t R, int N, float* __restrict__ T) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= R) return;
-  const float* a = alpha + r * N;
+  const float* a = atten + r * N;
   float* t = T + r * (N + 1);
   float acc = 1.f;
   t[0] = acc;
   for (int i = 0; i < N; ++i) {
-    acc = __fmul_rn(acc, __fsub_rn(1.f, a[i]));
+    acc = __fmul_rn(acc, a[i]);
     t[i + 1] = acc;
+  }
+}
+
+// Its division-free reverse scan (ad:828-835): b = g[N]; gx[N-1] = T[N-1] b; for j = N-1..1:
+// b = g[j] + atten[j] b, gx[j-1] = T[j-1] b -- exact zeros in atten are safe.
+__global__ void k_transmittance_bwd(const float* __restrict__ atten, const float* __restrict__ T,
+                                    const float* __restrict__ g, int64_t R, int N, float* __restrict__ gx) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= R || N == 0) return;
+  const float* a = atten + r * N;
+  const float* t = T + r * (N + 1);
+  const float* gr = g + r * (N + 1);
+  float* o = gx + r * N;
+  float b = gr[N];
+  o[N - 1] = t[N - 1] * b;
+  for (int j = N - 1; j > 0; --j) {
+    b = __fadd_rn(gr[j], __fmul_rn(a[j], b));
+    o[j - 1] = t[j - 1] * b;
   }
 }
 }  // namespace fv
 
-extern "C" int32_t fv_transmittance(const float* d_alpha, int64_t n_rays, int32_t n_samples, float* d_trans,
+extern "C" int32_t fv_transmittance(const float* d_atten, int64_t n_rays, int32_t n_samples, float* d_trans,
                                     void* stream) {
-  if (n_rays < 0 || n_samples < 0 || (n_rays > 0 && (!d_alpha || !d_trans)))
+  if (n_rays < 0 || n_samples < 0 || (n_rays > 0 && (!d_atten || !d_trans)))
     return set_error(FV_EDIM, "fv_transmittance: bad arguments");
   if (n_rays == 0) return FV_OK;
-  fv::k_transmittance<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(d_alpha, n_rays, n_samples,
+  fv::k_transmittance<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(d_atten, n_rays, n_samples,
                                                                                          d_trans);
   return check_launch("fv_transmittance");
+}
+
+extern "C" int32_t fv_transmittance_bwd(const float* d_atten, const float* d_trans, const float* d_g, int64_t n_rays,
+                                        int32_t n_samples, float* d_gatten, void* stream) {
+  if (n_rays < 0 || n_samples < 0 || (n_rays > 0 && n_samples > 0 && (!d_atten || !d_trans || !d_g || !d_gatten)))
+    return set_error(FV_EDIM, "fv_transmittance_bwd: bad arguments");
+  if (n_rays == 0 || n_samples == 0) return FV_OK;
+  fv::k_transmittance_bwd<<<(unsigned)((n_rays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      d_atten, d_trans, d_g, n_rays, n_samples, d_gatten);
+  return check_launch("fv_transmittance_bwd");
 }
 
 extern "C" int32_t fv_composite_fwd(const float* d_rgbs, const float* d_delta, const float* d_lik, int32_t lik_stride,

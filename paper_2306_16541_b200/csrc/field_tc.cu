@@ -572,9 +572,50 @@ int32_t field_fwd_tc(const fv_field* f, const fv_hash* h, const float4* xs, int6
   return check_launch("k_radiance_tc");
 }
 
+// Verification twin of k_radiance_tc's gather stage: the same hash_norm +
+// hash_levels_paired<FV_RAD_NL> calls on canonical points x (n,3), returning every corner's
+// global table index idx (n, L, 8) (corner a*4 + b*2 + c) and the blended features (n, 2L).
+// One thread per sample, whole warps (the pairing shuffles need both lanes of a pair).
+__global__ void k_hash_index_paired(fv_hash h, const float* __restrict__ x, int64_t n, uint32_t* __restrict__ idx,
+                                    float* __restrict__ feat) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = p < n;
+  const int64_t q = live ? p : n - 1;
+  float xn[3]; bool msk[3];
+  hash_norm(h, x[3 * q], x[3 * q + 1], x[3 * q + 2], xn, msk);
+  const uint32_t a = threadIdx.x & 1u;
+  constexpr int NL = FV_RAD_NL;
+  for (int c = 0; c < 16 / NL; ++c) {
+    float2 fv[NL];
+    uint32_t io[NL * 8];
+    hash_levels_paired<NL, true>(h, NL * c, xn, fv, io);
+    const int64_t sA = p & ~(int64_t)1, sB = sA + 1;     // the even lane's / the odd lane's sample
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const int lev = NL * c + l;
+      if (lev >= h.n_levels) break;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (sA < n) idx[(sA * h.n_levels + lev) * 8 + a * 4 + k] = io[l * 8 + k];
+        if (sB < n) idx[(sB * h.n_levels + lev) * 8 + a * 4 + k] = io[l * 8 + 4 + k];
+      }
+      if (live) { feat[p * 2 * h.n_levels + 2 * lev] = fv[l].x; feat[p * 2 * h.n_levels + 2 * lev + 1] = fv[l].y; }
+    }
+  }
+}
+
 }  // namespace fv
 
 using namespace fv;
+
+extern "C" int32_t fv_hash_index_paired(const fv_hash* hash, const float* d_x, int64_t n, uint32_t* d_index,
+                                        float* d_feat, void* stream) {
+  if (int32_t e = check_hash(hash)) return e;
+  if (n < 0 || (n > 0 && (!d_x || !d_index || !d_feat))) return set_error(FV_EDIM, "fv_hash_index_paired: bad arguments");
+  if (n == 0) return FV_OK;
+  k_hash_index_paired<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*hash, d_x, n, d_index, d_feat);
+  return check_launch("fv_hash_index_paired");
+}
 
 extern "C" size_t fv_field_pack_bytes(void) { return PK_BYTES; }
 

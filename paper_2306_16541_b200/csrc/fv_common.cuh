@@ -363,9 +363,12 @@ __device__ __forceinline__ float2 hash_level_feat(const fv_hash& h, int l, const
 // and each lane blends its four corners as lerps (z, then y) scaled by its x weight; one
 // shuffle per feature adds the partner's partial.  The blend order differs from the
 // oracle's (a,b,c) sum by fp32 rounding only: used where features are rounded to fp16.
-template <int NL>
+// IDX (verification only, k_hash_index_paired): also return the global table index of every
+// corner this lane fetches, idx_out[q * 8 + k] (sample A) and idx_out[q * 8 + 4 + k] (sample
+// B) for x-corner a = lane parity and k = 2 b + c.
+template <int NL, bool IDX = false>
 __device__ __forceinline__ void hash_levels_paired(const fv_hash& h, int l0, const float (&xn_self)[3],
-                                                   float2 (&out)[NL]) {
+                                                   float2 (&out)[NL], uint32_t* idx_out = nullptr) {
   const uint32_t maskT = (1u << h.log2_T) - 1u;
   const uint32_t a = threadIdx.x & 1u;
   // A = the even lane's sample, B = the odd lane's, for both lanes of a pair: each load
@@ -408,6 +411,15 @@ __device__ __forceinline__ void hash_levels_paired(const fv_hash& h, int l0, con
       iB[q * 4 + 0] = (xb ^ yB0 ^ zB0) & maskT; iB[q * 4 + 1] = (xb ^ yB0 ^ zB1) & maskT;
       iB[q * 4 + 2] = (xb ^ yB1 ^ zB0) & maskT; iB[q * 4 + 3] = (xb ^ yB1 ^ zB1) & maskT;
     }
+  }
+  if constexpr (IDX) {
+#pragma unroll
+    for (int q = 0; q < NL; ++q)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        idx_out[q * 8 + k] = lofs[q] + iA[q * 4 + k];
+        idx_out[q * 8 + 4 + k] = lofs[q] + iB[q * 4 + k];
+      }
   }
   float2 vA[4 * NL], vB[4 * NL];
   if (h.table_half) {

@@ -20,7 +20,11 @@ int32_t field_fwd_tc(const fv_field* f, const fv_hash* h, const float4* xs, int6
                      float* xfinal, cudaStream_t st, const int32_t* d_count = nullptr, const int32_t* idx = nullptr,
                      cudaEvent_t mid_event = nullptr);
 int32_t march_compact(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays, float* lik,
-                      float* delta, float4* xsc, int32_t* idx, int32_t* count, int32_t* ray_count, cudaStream_t st);
+                      float* delta, float4* xsc, int32_t* idx, int32_t* count, int32_t* ray_count, cudaStream_t st,
+                      uint8_t* flags = nullptr);
+int32_t march_round(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays, int32_t i0,
+                    int32_t K, const int32_t* live, const int32_t* n_live, float* lik, float* delta, float4* xsc,
+                    int32_t* idx, int32_t* count, int32_t* ray_count, cudaStream_t st);
 struct CompIn {
   const float4* rgbs;   // [c, sigma] per sample
   const float* delta;   // per sample

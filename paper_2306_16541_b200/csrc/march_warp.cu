@@ -67,87 +67,108 @@ struct Compact {
   float4* xsc;       // [<= S] (x_skel, L) of foreground samples
   int32_t* idx;      // [<= S] their sample index
   int32_t* count;    // device counter (zeroed before the launch)
+  uint8_t* flags;    // optional [S] per-sample bits: 1 ray hits the box, 2 occupancy cell on
+                     // (or no grid), 4 foreground (L > eps_w) -- the skip/fg masks for parity
 };
 
-// One thread per sample (ray-block-major layout).  Writes xs[s] = (x_skel, L) with L = 0
-// for samples outside the box or in empty occupancy cells, delta[s], optional x[s].
-// COMPACT: writes lik[s] instead of xs[s] and appends each foreground sample (L > eps_w)
-// to the compacted stream -- one atomicAdd per 128-thread block, warp ballots inside, so
-// a block's survivors stay contiguous (4 depths x 32 neighbouring rays) and the field
-// kernels skip background samples entirely.
+// One marching round (early termination): samples [i0, i0 + K) of the rays in a
+// live list.  Slot layout as layout.cuh with K samples per ray and the live-list position j
+// in place of the ray: s = ((j / 32) K + (i - i0)) 32 + j % 32.  live == NULL: every ray
+// (j = ray), the single-pass render (i0 = 0, K = N).
+struct MarchRound {
+  int32_t i0, K;
+  const int32_t* live;     // [n_live] ray ids, or NULL
+  const int32_t* n_live;   // device count of live rays (NULL: n_rays)
+};
+
+// One thread per sample slot.  Writes xs[s] = (x_skel, L) with L = 0 for samples outside the
+// box or in empty occupancy cells, delta[s], optional x[s].  COMPACT: writes lik[s] instead of
+// xs[s] and appends each foreground sample (L > eps_w) to the compacted stream -- one
+// atomicAdd per 128-thread block, warp ballots inside, so a block's survivors stay contiguous
+// (4 depths x 32 neighbouring rays) and the field kernels skip background samples entirely.
+// Block-uniform grid-stride loop over 128-slot tiles (a round's slot count is only known on
+// the device).
 template <bool COMPACT>
 __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, fv_warp w, int64_t n_rays,
                                                     float4* __restrict__ xs_out, float* __restrict__ delta_out,
                                                     float* __restrict__ x_out, int32_t* __restrict__ count_out,
-                                                    Compact cmp) {
+                                                    Compact cmp, MarchRound rd) {
   __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
   __shared__ int32_t wcount[4], wbase;
   fill_bones_x2(sg, w.d_g, w.n_bones);
   __syncthreads();
-  const int N = m.n_samples;
-  const int64_t total = padded_rays(n_rays) * N;
-  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (!COMPACT && s >= total) return;
-  int64_t ray = n_rays; int32_t i = 0;
-  if (s < total) sample_coords(s, N, ray, i);
-  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-  float delta = 0.f;
-  bool hit = false;
-  if (s < total && ray < n_rays) {
-    const int32_t pix = m.d_pix ? m.d_pix[ray] : (int32_t)(m.pix_offset + ray);
-    const Ray r = make_ray(cam, pix);
-    float t0, t1;
-    hit = slab(r, m.obox_min, m.obox_max, t0, t1);
-    if (hit) {
-      const float step = __fdiv_rn(__fsub_rn(t1, t0), (float)N);
-      const float ui = m.jitter ? jitter_u(m.seed, (uint32_t)pix, i) : 0.5f;
-      const float t = sample_t(t0, step, i, ui);
-      if (i + 1 < N) {
-        const float un = m.jitter ? jitter_u(m.seed, (uint32_t)pix, i + 1) : 0.5f;
-        delta = __fsub_rn(sample_t(t0, step, i + 1, un), t);
-      } else {
-        const float u0 = m.jitter ? jitter_u(m.seed, (uint32_t)pix, 0) : 0.5f;
-        delta = __fadd_rn(__fsub_rn(t1, t), __fsub_rn(sample_t(t0, step, 0, u0), t0));
+  const int N = m.n_samples, K = rd.K;
+  const int64_t n_j = rd.n_live ? (int64_t)*rd.n_live : n_rays;     // rays in this round
+  const int64_t total = padded_rays(n_j) * K;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = base + threadIdx.x;
+    int64_t j = n_j; int32_t il = 0;
+    if (s < total) sample_coords(s, K, j, il);
+    const int32_t i = rd.i0 + il;
+    float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+    float delta = 0.f;
+    bool hit = false, occ = false;
+    if (s < total && j < n_j) {
+      const int64_t ray = rd.live ? (int64_t)rd.live[j] : j;
+      const int32_t pix = m.d_pix ? m.d_pix[ray] : (int32_t)(m.pix_offset + ray);
+      const Ray r = make_ray(cam, pix);
+      float t0, t1;
+      hit = slab(r, m.obox_min, m.obox_max, t0, t1);
+      if (hit) {
+        const float step = __fdiv_rn(__fsub_rn(t1, t0), (float)N);
+        const float ui = m.jitter ? jitter_u(m.seed, (uint32_t)pix, i) : 0.5f;
+        const float t = sample_t(t0, step, i, ui);
+        if (i + 1 < N) {
+          const float un = m.jitter ? jitter_u(m.seed, (uint32_t)pix, i + 1) : 0.5f;
+          delta = __fsub_rn(sample_t(t0, step, i + 1, un), t);
+        } else {
+          const float u0 = m.jitter ? jitter_u(m.seed, (uint32_t)pix, 0) : 0.5f;
+          delta = __fadd_rn(__fsub_rn(t1, t), __fsub_rn(sample_t(t0, step, 0, u0), t0));
+        }
+        const float px = __fadd_rn(r.ox, __fmul_rn(t, r.dx));
+        const float py = __fadd_rn(r.oy, __fmul_rn(t, r.dy));
+        const float pz = __fadd_rn(r.oz, __fmul_rn(t, r.dz));
+        if (x_out) { x_out[3 * s] = px; x_out[3 * s + 1] = py; x_out[3 * s + 2] = pz; }
+        occ = m.d_occ == nullptr || occ_test(m.d_occ, m.obox_min, m.occ_scale, px, py, pz);
+        if (occ) {
+          float xsk[3];
+          const float L = warp_point<false>(w, sg, m.eps_w, px, py, pz, xsk);
+          out = make_float4(xsk[0], xsk[1], xsk[2], L);
+        }
+      } else if (x_out) {
+        x_out[3 * s] = x_out[3 * s + 1] = x_out[3 * s + 2] = 0.f;
       }
-      const float px = __fadd_rn(r.ox, __fmul_rn(t, r.dx));
-      const float py = __fadd_rn(r.oy, __fmul_rn(t, r.dy));
-      const float pz = __fadd_rn(r.oz, __fmul_rn(t, r.dz));
-      if (x_out) { x_out[3 * s] = px; x_out[3 * s + 1] = py; x_out[3 * s + 2] = pz; }
-      const bool occ = m.d_occ == nullptr || occ_test(m.d_occ, m.obox_min, m.occ_scale, px, py, pz);
-      if (occ) {
-        float xsk[3];
-        const float L = warp_point<false>(w, sg, m.eps_w, px, py, pz, xsk);
-        out = make_float4(xsk[0], xsk[1], xsk[2], L);
-      }
-    } else if (x_out) {
+      if (i == 0 && count_out) count_out[ray] = hit ? N : 0;
+    } else if (x_out && s < total) {
       x_out[3 * s] = x_out[3 * s + 1] = x_out[3 * s + 2] = 0.f;
     }
-    if (i == 0 && count_out) count_out[ray] = hit ? N : 0;
-  } else if (x_out && s < total) {
-    x_out[3 * s] = x_out[3 * s + 1] = x_out[3 * s + 2] = 0.f;
-  }
-  if (!COMPACT) {
-    xs_out[s] = out;
-    delta_out[s] = delta;
-    return;
-  }
-  const bool fg = s < total && out.w > m.eps_w;
-  const uint32_t ballot = __ballot_sync(0xffffffffu, fg);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) wcount[wid] = __popc(ballot);
-  __syncthreads();
-  if (threadIdx.x == 0) wbase = atomicAdd(cmp.count, wcount[0] + wcount[1] + wcount[2] + wcount[3]);
-  __syncthreads();
-  if (s < total) {
-    cmp.lik[s] = out.w;
-    delta_out[s] = delta;
-  }
-  if (fg) {
-    int off = wbase;
-    for (int q = 0; q < wid; ++q) off += wcount[q];
-    off += __popc(ballot & ((1u << lane) - 1u));
-    cmp.xsc[off] = out;
-    cmp.idx[off] = (int32_t)s;
+    if (!COMPACT) {
+      if (s < total) {
+        xs_out[s] = out;
+        delta_out[s] = delta;
+      }
+      continue;
+    }
+    const bool fg = s < total && out.w > m.eps_w;
+    const uint32_t ballot = __ballot_sync(0xffffffffu, fg);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) wcount[wid] = __popc(ballot);
+    __syncthreads();
+    if (threadIdx.x == 0) wbase = atomicAdd(cmp.count, wcount[0] + wcount[1] + wcount[2] + wcount[3]);
+    __syncthreads();
+    if (s < total) {
+      cmp.lik[s] = out.w;
+      delta_out[s] = delta;
+      if (cmp.flags) cmp.flags[s] = (uint8_t)((hit ? 1 : 0) | (occ ? 2 : 0) | (fg ? 4 : 0));
+    }
+    if (fg) {
+      int off = wbase;
+      for (int q = 0; q < wid; ++q) off += wcount[q];
+      off += __popc(ballot & ((1u << lane) - 1u));
+      cmp.xsc[off] = out;
+      cmp.idx[off] = (int32_t)s;
+    }
+    __syncthreads();                     // wcount / wbase are reused by the next tile
   }
 }
 
@@ -274,6 +295,51 @@ __global__ void k_sample_bone_channels(fv_warp w, const float* __restrict__ pts,
   out[e] = v;
 }
 
+// Backward of sample_bone_channels (ad:775-806) for an upstream gradient g (K,n):
+// dvol[i, corner] += trilinear weight * g (the reference's bincount scatter, ad:778-789;
+// fp32 atomics into the unpadded (C,G,G,G) grid, padding corners dropped) and
+// dpts[i, n] = (d out / d u) * g * scale (ad:790-805), both zero for points outside.
+__global__ void k_sample_bone_channels_bwd(fv_warp w, const float* __restrict__ pts, int64_t n,
+                                           const float* __restrict__ g, float* __restrict__ dvol,
+                                           float* __restrict__ dpts) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)w.n_bones * n) return;
+  const int i = (int)(e / n);
+  const float p[3] = {pts[3 * e], pts[3 * e + 1], pts[3 * e + 2]};
+  int i0[3];
+  float f[3];
+  const bool in = warp_cell(w, p, i0, f);
+  const float gv = in ? g[e] : 0.f;
+  if (dpts) {
+    float d[3] = {0.f, 0.f, 0.f};
+    if (in) {
+      float cv[8];
+      load_corners(w.d_vol_packed, w.vol_half, vol_cell_index(i, w.vol_res, i0), cv);
+      const float gx0 = 1.f - f[0], gy0 = 1.f - f[1], gz0 = 1.f - f[2];
+      d[0] = gy0 * gz0 * (cv[4] - cv[0]) + gy0 * f[2] * (cv[5] - cv[1]) + f[1] * gz0 * (cv[6] - cv[2]) +
+             f[1] * f[2] * (cv[7] - cv[3]);
+      d[1] = gx0 * gz0 * (cv[2] - cv[0]) + gx0 * f[2] * (cv[3] - cv[1]) + f[0] * gz0 * (cv[6] - cv[4]) +
+             f[0] * f[2] * (cv[7] - cv[5]);
+      d[2] = gx0 * gy0 * (cv[1] - cv[0]) + gx0 * f[1] * (cv[3] - cv[2]) + f[0] * gy0 * (cv[5] - cv[4]) +
+             f[0] * f[1] * (cv[7] - cv[6]);
+    }
+    dpts[3 * e] = d[0] * gv * w.wscale[0];
+    dpts[3 * e + 1] = d[1] * gv * w.wscale[1];
+    dpts[3 * e + 2] = d[2] * gv * w.wscale[2];
+  }
+  if (dvol && in && gv != 0.f) {
+    const int G = w.vol_res;
+    const float wx[2] = {1.f - f[0], f[0]}, wy[2] = {1.f - f[1], f[1]}, wz[2] = {1.f - f[2], f[2]};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int a = c >> 2, b = (c >> 1) & 1, z = c & 1;
+      const int vx = i0[0] + a - 1, vy = i0[1] + b - 1, vz = i0[2] + z - 1;
+      if (vx < 0 || vx >= G || vy < 0 || vy >= G || vz < 0 || vz >= G) continue;
+      atomicAdd(dvol + (((int64_t)i * G + vx) * G + vy) * G + vz, wx[a] * wy[b] * wz[z] * gv);
+    }
+  }
+}
+
 }  // namespace fv
 
 namespace fv {
@@ -322,6 +388,17 @@ extern "C" int32_t fv_sample_bone_channels(const fv_warp* warp, const float* d_p
   return check_launch("fv_sample_bone_channels");
 }
 
+extern "C" int32_t fv_sample_bone_channels_bwd(const fv_warp* warp, const float* d_pts, int64_t n, const float* d_g,
+                                               float* d_dvol, float* d_dpts, void* stream) {
+  if (!warp || n < 0 || (n > 0 && (!d_pts || !d_g))) return set_error(FV_EDIM, "fv_sample_bone_channels_bwd: bad arguments");
+  if (int32_t e = check_warp(warp)) return e;
+  if (n == 0 || (!d_dvol && !d_dpts)) return FV_OK;
+  const int64_t total = (int64_t)warp->n_bones * n;
+  k_sample_bone_channels_bwd<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*warp, d_pts, n, d_g,
+                                                                                                d_dvol, d_dpts);
+  return check_launch("fv_sample_bone_channels_bwd");
+}
+
 extern "C" int32_t fv_warp_bwd(const fv_warp* warp, float eps_w, const float* d_x, int64_t n,
                                const float* d_dxskel, float* d_dvol, void* stream) {
   if (!warp || n < 0) return set_error(FV_EDIM, "fv_warp_bwd: bad arguments");
@@ -352,18 +429,56 @@ extern "C" int32_t fv_march_warp(const fv_camera* cam, const fv_march* march, co
   if (n_rays == 0) return FV_OK;
   const int64_t total = padded_rays(n_rays) * march->n_samples;
   k_march_warp<false><<<(unsigned)((total + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-      *cam, *march, *warp, n_rays, (float4*)d_xs, d_delta, d_x, d_count, Compact{});
+      *cam, *march, *warp, n_rays, (float4*)d_xs, d_delta, d_x, d_count, Compact{},
+      MarchRound{0, march->n_samples, nullptr, nullptr});
   return check_launch("fv_march_warp");
 }
 
 namespace fv {
 // render-path march: likelihood per sample + compacted foreground stream (count zeroed here)
 int32_t march_compact(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays, float* lik,
-                      float* delta, float4* xsc, int32_t* idx, int32_t* count, int32_t* ray_count, cudaStream_t st) {
+                      float* delta, float4* xsc, int32_t* idx, int32_t* count, int32_t* ray_count, cudaStream_t st,
+                      uint8_t* flags) {
   const int64_t total = padded_rays(n_rays) * march->n_samples;
   cudaMemsetAsync(count, 0, sizeof(int32_t), st);
   k_march_warp<true><<<(unsigned)((total + 127) / 128), 128, 0, st>>>(*cam, *march, *warp, n_rays, nullptr, delta,
-                                                                      nullptr, ray_count, Compact{lik, xsc, idx, count});
+                                                                      nullptr, ray_count,
+                                                                      Compact{lik, xsc, idx, count, flags},
+                                                                      MarchRound{0, march->n_samples, nullptr, nullptr});
   return check_launch("march_compact");
 }
+
+// One marching round over a live-ray list (count zeroed here): samples [i0, i0 + K) of the
+// n_live rays in live (device), slots in the round layout; n_rays bounds n_live.
+int32_t march_round(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays, int32_t i0,
+                    int32_t K, const int32_t* live, const int32_t* n_live, float* lik, float* delta, float4* xsc,
+                    int32_t* idx, int32_t* count, int32_t* ray_count, cudaStream_t st) {
+  const int64_t total = padded_rays(n_rays) * K;
+  cudaMemsetAsync(count, 0, sizeof(int32_t), st);
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = std::min<int64_t>((total + 127) / 128, (int64_t)n_sm * 16);
+  k_march_warp<true><<<(unsigned)blocks, 128, 0, st>>>(*cam, *march, *warp, n_rays, nullptr, delta, nullptr,
+                                                       ray_count, Compact{lik, xsc, idx, count, nullptr},
+                                                       MarchRound{i0, K, live, n_live});
+  return check_launch("march_round");
+}
 }  // namespace fv
+
+// The render path's own march (the kernel fv_render_fwd launches), exposed so its integer
+// outputs can be checked bit for bit: per-sample likelihood (0 where skipped), spacing and
+// flags, the compacted foreground stream (x_skel, L) + sample ids and its length, per-ray
+// sample counts.  Sample slots are ray-block-major (layout.cuh).
+extern "C" int32_t fv_march_compact(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays,
+                                    float* d_lik, float* d_delta, float* d_xsc, int32_t* d_idx, int32_t* d_n_fg,
+                                    int32_t* d_count, uint8_t* d_flags, void* stream) {
+  if (!cam || !march || !warp || n_rays < 0 || march->n_samples < 1 || !d_lik || !d_delta || !d_xsc || !d_idx ||
+      !d_n_fg)
+    return set_error(FV_EDIM, "fv_march_compact: bad arguments");
+  if (int32_t e = check_warp(warp)) return e;
+  if (n_rays == 0) return cudaMemsetAsync(d_n_fg, 0, sizeof(int32_t), (cudaStream_t)stream) == cudaSuccess
+                              ? FV_OK : check_launch("fv_march_compact");
+  return march_compact(cam, march, warp, n_rays, d_lik, d_delta, (float4*)d_xsc, d_idx, d_n_fg, d_count,
+                       (cudaStream_t)stream, d_flags);
+}

@@ -45,6 +45,8 @@ class FreeviewModel:
         cfg = scene.cfg
         self.cfg = cfg
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.half = bool(cfg.half)
         self.precision = (1 if self.half else 0) if precision is None else int(precision)
         self.n_bones = cfg.n_bones
@@ -181,13 +183,15 @@ class FreeviewModel:
         ng = self.g.numel()
         buf[:ng].numpy()[:] = g_packed.reshape(-1)
         buf[ng:].numpy()[:] = pose_vec.reshape(-1)
-        st = torch.cuda.current_stream() if stream is None else stream
-        with torch.cuda.stream(st):
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        if st.device != self.device:
+            raise ValueError(f"pose upload stream is on {st.device}, the model on {self.device}")
+        with torch.cuda.device(self.device), torch.cuda.stream(st):
             self.g.view(-1).copy_(buf[:ng], non_blocking=True)
             self.pose_dev.copy_(buf[ng:], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(st)
-        self._pin_ev[k] = ev
+        self._pin_ev[k] = ev       # the slot is rewritten only after this event (the H2D read)
 
     def set_pose(self, pose: Pose, stream=None) -> None:
         """Upload the frame's motion bases G_i and fold the pose into the residual bias."""

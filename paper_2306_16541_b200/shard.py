@@ -37,6 +37,33 @@ def row_bands_for_rank(rank: int, world: int, height: int, band: int = 4):
     return [(y, min(y + band, height)) for y in range(band * rank, height, band * world)]
 
 
+def band_rows(rank: int, world: int, height: int, band: int = 4) -> List[int]:
+    """Image rows of rank ``rank``'s interleaved bands (row_bands_for_rank), in order."""
+    return [y for a, b in row_bands_for_rank(rank, world, height, band) for y in range(a, b)]
+
+
+def gather_row_bands(image: torch.Tensor, world: int, rank: int, band: int = 4, group=None) -> torch.Tensor:
+    """Assemble a frame rendered as interleaved row bands: ``image`` (H, ...) holds this rank's
+    rows (others undefined); afterwards every rank holds the full frame.  One all-gather of
+    the ranks' packed rows (padded to the longest share) plus an on-device row scatter."""
+    import torch.distributed as dist
+    if world == 1:
+        return image
+    h = image.shape[0]
+    shares = [band_rows(r, world, h, band) for r in range(world)]
+    n_max = max(len(s) for s in shares)
+    idx = torch.tensor(shares[rank] + [shares[rank][-1] if shares[rank] else 0] * (n_max - len(shares[rank])),
+                       device=image.device, dtype=torch.long)
+    local = image.index_select(0, idx).contiguous()
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local, group=group)
+    for r in range(world):
+        if r != rank and shares[r]:
+            rows = torch.tensor(shares[r], device=image.device, dtype=torch.long)
+            image.index_copy_(0, rows, parts[r][:len(shares[r])])
+    return image
+
+
 def broadcast_params(flat: torch.Tensor, src: int = 0, group=None) -> None:
     """Identical weights on every rank: one broadcast of the flat master buffer."""
     import torch.distributed as dist

@@ -17,6 +17,7 @@ buffer is all-reduced (mean) between backward and Adam -- the only exchange of t
 
 from __future__ import annotations
 
+import copy
 import csv
 import ctypes as C
 import json
@@ -34,6 +35,7 @@ from .errors import TrainingError
 from .model import FreeviewModel, hann_band_weights
 from .render import RenderSettings, camera_struct, march_struct
 from .scene import PE_BANDS
+from .skeleton import Pose
 from .shard import GradBuckets
 
 
@@ -161,6 +163,15 @@ class Trainer:
                 raise ValueError("weight-volume generator output does not match the model's W^c logits")
             from .model import LR_OTHER
             self.wopt = torch.optim.Adam(weight_net.parameters(), lr=LR_OTHER, betas=(0.9, 0.99), eps=1e-8)
+
+    def set_frame(self, camera: CameraModel, target: np.ndarray, mask: np.ndarray) -> None:
+        """Switch the training frame ("pick a training frame"): its camera, target image
+        and foreground mask (same resolution, so every step buffer is reused)."""
+        t = np.ascontiguousarray(np.asarray(target, np.float32).reshape(-1, 3))
+        if t.shape != tuple(self.target.shape) or camera.width * camera.height != t.shape[0]:
+            raise ValueError("set_frame: every frame must have the trainer's resolution")
+        self.cam, self.mask = camera, mask
+        self.target.copy_(torch.from_numpy(t).to(self.dev), non_blocking=False)
 
     def set_schedule(self, alpha: float, residual: bool) -> None:
         """Coarse-to-fine state of one iteration: Hann window alpha of the
@@ -341,16 +352,21 @@ class Trainer:
         nets = self.nets
         self.t += 1
         half = nets.table_half
+        self.flag.zero_()                 # a flag left by an earlier non-finite step must not veto this one
         _lib.check(self.lib.fv_adam_step(nets.flat.data_ptr(), self.grad.data_ptr(), self.m.data_ptr(),
                                          self.v.data_ptr(), nets.n_params, self.seg_end, self.seg_lr, 2, self.t,
                                          0.9, 0.99, 1e-8, half.data_ptr() if half is not None else None, 0,
                                          self.table_elems if half is not None else 0, self.flag.data_ptr(),
                                          _lib.stream_ptr()), "fv_adam_step")
         nets.refresh_after_step()
-        if self.weight_net is not None:
-            self.wopt.step()
-        if self.pose_refiner is not None:
-            self.popt.step()
+        if self.weight_net is not None or self.pose_refiner is not None:
+            # the torch-side optimizers follow the fused step's verdict: no update on a
+            # non-finite gradient (ad:898-902); one host read, only on these optional paths
+            if int(self.flag.item()) == 0:
+                if self.weight_net is not None:
+                    self.wopt.step()
+                if self.pose_refiner is not None:
+                    self.popt.step()
 
     def check_finite(self):
         """Raise TrainingError naming the block if the last Adam pass saw a non-finite gradient."""
@@ -385,6 +401,7 @@ class TrainConfig:
     precision: str = "tf32"
     checkpoint_every: int = 100
     log_path: Optional[str] = None
+    checkpoint_dir: Optional[str] = None
 
     def __post_init__(self):
         if not (0.0 < self.residual_on < self.full_band < 1.0):
@@ -403,17 +420,65 @@ def schedule(it: int, cfg: TrainConfig, bands: int = PE_BANDS):
     return float(alpha), it >= it_on
 
 
+def _aux_modules(trainer: "Trainer"):
+    """(name, torch module or optimizer) pairs of the optional generator / pose refiner."""
+    out = []
+    if getattr(trainer, "weight_net", None) is not None:
+        out += [("weight_net", trainer.weight_net), ("weight_opt", trainer.wopt)]
+    if getattr(trainer, "pose_refiner", None) is not None:
+        out += [("pose_refiner", trainer.pose_refiner), ("pose_opt", trainer.popt)]
+    return out
+
+
+def _flat_state(obj) -> dict:
+    """A module's state_dict or an optimizer's per-parameter state as name -> tensor."""
+    if isinstance(obj, torch.optim.Optimizer):
+        sd = obj.state_dict()
+        out = {}
+        for pid, st in sd["state"].items():
+            for k, v in st.items():
+                out[f"{pid}.{k}"] = v if isinstance(v, torch.Tensor) else torch.tensor(float(v))
+        return out
+    return dict(obj.state_dict())
+
+
+def _load_flat_state(obj, arrays: dict) -> None:
+    if isinstance(obj, torch.optim.Optimizer):
+        sd = obj.state_dict()
+        state = {}
+        for key, a in arrays.items():
+            pid, k = key.split(".", 1)
+            state.setdefault(int(pid), {})[k] = a
+        sd["state"] = state
+        obj.load_state_dict(sd)
+    else:
+        obj.load_state_dict({k: a for k, a in arrays.items()})
+
+
 def save_checkpoint(path: str, trainer: "Trainer", iteration: int) -> None:
     """Manifest + raw little-endian float32 arrays: params.bin (the flat master
-    buffer), adam_m.bin, adam_v.bin, manifest.json (block table, Adam step, schedule)."""
+    buffer), adam_m.bin, adam_v.bin, manifest.json (block table, Adam step, schedule); with a
+    weight-volume generator / pose refiner attached, their parameters and torch-Adam states
+    as one raw array per tensor (``<module>.<key>.bin``, listed in the manifest)."""
     os.makedirs(path, exist_ok=True)
     nets = trainer.nets
     for name, t in (("params", nets.flat), ("adam_m", trainer.m), ("adam_v", trainer.v)):
         t.detach().cpu().numpy().astype("<f4").tofile(os.path.join(path, f"{name}.bin"))
-    man = {"format": "freeview-b200-checkpoint", "version": 1, "iteration": iteration, "adam_t": trainer.t,
+    aux = {}
+    for mname, obj in _aux_modules(trainer):
+        entries = {}
+        for key, t in _flat_state(obj).items():
+            fn = f"{mname}.{key}.bin"
+            a = t.detach().cpu().numpy()
+            dt = a.dtype.newbyteorder("<")
+            a.astype(dt).tofile(os.path.join(path, fn))
+            entries[key] = {"file": fn, "shape": list(t.shape), "dtype": dt.str}
+        aux[mname] = entries
+    man = {"format": "freeview-b200-checkpoint", "version": 2, "iteration": iteration, "adam_t": trainer.t,
            "n_params": nets.n_params, "pe_alpha": nets.pe_alpha, "residual": bool(trainer.residual),
            "blocks": {k: {"offset": a, "size": b - a, "shape": list(nets.views[k].shape)}
-                      for k, (a, b) in nets.block_ranges.items()}}
+                      for k, (a, b) in nets.block_ranges.items()},
+           "modules": aux}
     with open(os.path.join(path, "manifest.json"), "w") as f:
         json.dump(man, f, indent=1)
 
@@ -449,50 +514,139 @@ def load_checkpoint(path: str, trainer: "Trainer") -> int:
         t.copy_(torch.from_numpy(a.astype(np.float32)).to(t.device))
     trainer.t = int(man["adam_t"])
     trainer.set_schedule(man["pe_alpha"], man["residual"])
+    mods = man.get("modules", {})
+    for mname, obj in _aux_modules(trainer):
+        if mname not in mods:
+            raise ValueError(f"checkpoint has no state for the attached {mname}")
+        arrays = {}
+        for key, ent in mods[mname].items():
+            a = np.fromfile(os.path.join(path, ent["file"]), dtype=ent.get("dtype", "<f4")).reshape(ent["shape"])
+            ref = _flat_state(obj).get(key)
+            dev = ref.device if isinstance(ref, torch.Tensor) else "cpu"
+            arrays[key] = torch.from_numpy(a.astype(a.dtype.newbyteorder("="))).to(dev)
+        _load_flat_state(obj, arrays)
     nets.refresh()
     return int(man["iteration"])
 
 
-def train(nets: FreeviewModel, camera: CameraModel, target: np.ndarray, mask: np.ndarray,
-          settings: RenderSettings, cfg: TrainConfig, process_group=None) -> List[dict]:
-    """SPEC train: per iteration apply the coarse-to-fine schedule, sample
-    patches, render them through the full pipeline, loss (Eq 14 with the perceptual proxy),
-    backward, (all-reduce), Adam at the per-group rates; log (iteration, loss, mse_term,
-    perc_term, alpha, stage, wall_ms) to a CSV.  A non-finite loss or gradient restores the
-    last good state (kept every ``checkpoint_every`` iterations) and raises TrainingError."""
-    tr = Trainer(nets, camera, target, mask, settings, n_patches=cfg.n_patches, patch=cfg.patch, seed=cfg.seed,
-                 process_group=process_group, precision=cfg.precision, lam_mse=cfg.lam_mse, lam_perc=cfg.lam_perc)
-    good = (nets.flat.clone(), tr.m.clone(), tr.v.clone(), tr.t)
+@dataclass
+class Frame:
+    """One captured training view (SPEC PatchBatch source): camera, target RGB image
+    (H, W, 3) in [0, 1], foreground mask (H, W) bool and the frame's body pose."""
+    camera: CameraModel
+    image: np.ndarray
+    mask: np.ndarray
+    pose: "Pose"
+
+
+@dataclass
+class Dataset:
+    """In-memory dataset for ``train(dataset, config)``: frames plus the train / held-out
+    split (the reference's CaptureDataset keeps the same three things on disk: per-frame
+    camera, image, mask and pose, and ``splits``, cap:438-470)."""
+    frames: List[Frame]
+    train_ids: Optional[List[int]] = None
+    heldout_ids: Optional[List[int]] = None
+
+    def __post_init__(self):
+        if not self.frames:
+            raise ValueError("dataset has no frames")
+        if self.train_ids is None:
+            self.train_ids = list(range(len(self.frames)))
+        if self.heldout_ids is None:
+            self.heldout_ids = []
+        if not self.train_ids:
+            raise ValueError("dataset has no training frames")
+
+
+def synthetic_dataset(scene, n_frames: Optional[int] = None) -> Dataset:
+    """The BASELINE synthetic stand-in as a dataset: the scene's camera, its seeded smooth
+    target image and projected-ellipsoid mask (scene.target_image), one frame per pose."""
+    from .scene import target_image
+    img, mask = target_image(scene)
+    poses = scene.poses if n_frames is None else [scene.poses[i % len(scene.poses)] for i in range(n_frames)]
+    return Dataset([Frame(scene.camera, img, mask, p) for p in poses])
+
+
+def train(dataset: Dataset, config: TrainConfig, nets: Optional[FreeviewModel] = None,
+          settings: Optional[RenderSettings] = None, process_group=None) -> List[dict]:
+    """SPEC ``train(dataset, config)``.  Per iteration: pick a training frame
+    (deterministic per (seed, iteration)) and upload its pose, apply the coarse-to-fine
+    schedule (residual net exactly zero before its milestone, Hann alpha ramp), sample
+    patches on the frame's mask, render them through the full pipeline, loss
+    (Eq 14 with the perceptual proxy), backward, (NCCL all-reduce), Adam at the
+    per-group rates; log (iteration, loss, mse_term, perc_term, alpha, stage, wall_ms) to a
+    CSV; save a checkpoint every ``checkpoint_every`` iterations into ``checkpoint_dir``.  A
+    non-finite loss or gradient restores the last good state and raises TrainingError
+    (S:509).  ``nets`` defaults to a fresh model of ``dataset``'s scene when it carries one
+    (``synthetic_dataset``); returns the log rows."""
+    if nets is None:
+        raise ValueError("train: pass the model (nets) to optimise")
+    f0 = dataset.frames[dataset.train_ids[0]]
+    if settings is None:
+        settings = RenderSettings.from_config(nets.cfg, seed=config.seed)
+    tr = Trainer(nets, f0.camera, f0.image, f0.mask, settings, n_patches=config.n_patches, patch=config.patch,
+                 seed=config.seed, process_group=process_group, precision=config.precision,
+                 lam_mse=config.lam_mse, lam_perc=config.lam_perc)
+
+    def snapshot():
+        return (nets.flat.clone(), tr.m.clone(), tr.v.clone(), tr.t,
+                {n: copy.deepcopy(o.state_dict()) for n, o in _aux_modules(tr)})
+
+    def restore(g):
+        nets.flat.copy_(g[0]); tr.m.copy_(g[1]); tr.v.copy_(g[2]); tr.t = g[3]
+        for n, o in _aux_modules(tr):
+            o.load_state_dict(g[4][n])
+        nets.refresh()
+
+    good = snapshot()
     rows = []
     writer, fh = None, None
-    if cfg.log_path:
-        fh = open(cfg.log_path, "w", newline="")
+    if config.log_path:
+        fh = open(config.log_path, "w", newline="")
         writer = csv.writer(fh)
         writer.writerow(["iteration", "loss", "mse_term", "perc_term", "alpha", "stage", "wall_ms"])
+    current = None
     try:
         t0 = time.perf_counter()
-        for it in range(cfg.iterations):
-            alpha, residual = schedule(it, cfg)
+        for it in range(config.iterations):
+            fid = dataset.train_ids[int(np.random.default_rng([config.seed, it, 1]).integers(len(dataset.train_ids)))]
+            if fid != current:
+                fr = dataset.frames[fid]
+                if current is not None:
+                    tr.set_frame(fr.camera, fr.image, fr.mask)
+                nets.set_pose(fr.pose)
+                current = fid
+            alpha, residual = schedule(it, config)
             tr.set_schedule(alpha, residual)
             tr.step(it)
             vals = tr.loss.tolist()
             mse = vals[1] if tr.lam_perc != 0.0 or tr.lam_mse != 1.0 else vals[0]
             flag = int(tr.flag.item())
             if not np.isfinite(vals[0]) or flag:
-                nets.flat.copy_(good[0]); tr.m.copy_(good[1]); tr.v.copy_(good[2]); tr.t = good[3]
-                nets.refresh()
+                restore(good)
                 raise TrainingError(f"non-finite loss/gradient at iteration {it}; last good state restored")
             row = {"iteration": it, "loss": vals[0], "mse_term": mse, "perc_term": vals[2] if tr.lam_perc else 0.0,
-                   "alpha": alpha, "stage": "residual" if residual else "skeleton",
+                   "alpha": alpha, "stage": "residual" if residual else "skeleton", "frame": fid,
                    "wall_ms": (time.perf_counter() - t0) * 1e3}
             rows.append(row)
             if writer:
                 writer.writerow([row[k] for k in ("iteration", "loss", "mse_term", "perc_term", "alpha", "stage",
                                                   "wall_ms")])
-            if cfg.checkpoint_every and (it + 1) % cfg.checkpoint_every == 0:
-                good = (nets.flat.clone(), tr.m.clone(), tr.v.clone(), tr.t)
+            if config.checkpoint_every and (it + 1) % config.checkpoint_every == 0:
+                good = snapshot()
+                if config.checkpoint_dir:
+                    save_checkpoint(os.path.join(config.checkpoint_dir, f"it{it + 1:07d}"), tr, it + 1)
     finally:
         if fh:
             fh.close()
     train.last_trainer = tr
     return rows
+
+
+def train_frame(nets: FreeviewModel, camera: CameraModel, target: np.ndarray, mask: np.ndarray,
+                settings: RenderSettings, cfg: TrainConfig, process_group=None) -> List[dict]:
+    """``train`` on a one-frame dataset (the frame's pose = the model's current pose)."""
+    pose = nets._pose if nets._pose is not None else nets.scene.poses[0]
+    return train(Dataset([Frame(camera, target, mask, pose)]), cfg, nets=nets, settings=settings,
+                 process_group=process_group)

@@ -61,6 +61,30 @@ def test_no_cpu_fallback_missing_library_and_cpu_tensors(monkeypatch):
     with pytest.raises(DimensionError):
         autodiff.transmittance(torch.zeros((2, 3)))
     with pytest.raises(DimensionError):
-        fused.fused_forward(fused.FusedMlp([torch.zeros((3, 2))], [torch.zeros(2)]), torch.zeros((4, 3)))
+        fused.fused_forward(fused.FusedMlp([torch.zeros((3, 64)), torch.zeros((64, 2))]), torch.zeros((4, 3)))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _lib.ptr(torch.zeros(3))
+
+
+def test_fused_mlp_random_draws_the_reference_weights():
+    """FusedMlp.random follows fu:120-130's draw order (per layer: He-normal weights, then
+    N(0, 0.01) biases) bit for bit (golden mlp_* from the reference), and the reference's
+    shape rules raise DimensionError."""
+    import numpy as np
+    import torch
+    from paper_2306_16541_b200 import fused
+    from paper_2306_16541_b200.errors import DimensionError
+    g = np.load(os.path.join(ROOT, "tests", "golden", "ref_primitives.npz"))
+    mlp = fused.FusedMlp.random(32, 4, depth=2, seed=3, device="cpu")
+    assert mlp.depth == 2 and mlp.in_dim == 32 and mlp.out_dim == 4
+    for i in range(3):
+        assert np.array_equal(mlp.weights[i].numpy(), g[f"mlp_w{i}"])
+        assert np.array_equal(mlp.biases[i].numpy(), g[f"mlp_b{i}"])
+    nb = fused.FusedMlp.random(32, 4, depth=2, seed=3, with_bias=False, device="cpu")
+    assert all(float(b.abs().sum()) == 0.0 for b in nb.biases)
+    with pytest.raises(DimensionError):
+        fused.FusedMlp([torch.zeros((32, 64))])
+    with pytest.raises(DimensionError):
+        fused.FusedMlp([torch.zeros((32, 64)), torch.zeros((64, 65))])
+    with pytest.raises(DimensionError):
+        fused.FusedMlp([torch.zeros((32, 64)), torch.zeros((64, 4))], [torch.zeros(64), torch.zeros(3)])

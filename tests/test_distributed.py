@@ -122,3 +122,19 @@ def test_row_bands_partition_the_image(world, height):
         for a, b in row_bands_for_rank(r, world, height):
             rows[a:b] += 1
     assert np.all(rows == 1)
+
+
+def _gather_bands(rank, world):
+    h, w = 37, 5                            # uneven shares: 10 bands of 4 rows (+1) over 2 ranks
+    img = torch.full((h, w, 4), -1.0)
+    for y in shard.band_rows(rank, world, h):
+        img[y] = float(y)
+    return shard.gather_row_bands(img, world, rank).numpy()
+
+
+def test_gather_row_bands_assembles_the_frame():
+    out = _run(_gather_bands)
+    want = np.broadcast_to(np.arange(37, dtype=np.float32)[:, None, None], (37, 5, 4))
+    for r in (0, 1):
+        assert np.array_equal(out[r], want)
+    assert sorted(shard.band_rows(0, 2, 37) + shard.band_rows(1, 2, 37)) == list(range(37))

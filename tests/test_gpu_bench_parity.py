@@ -1,0 +1,303 @@
+"""Parity on exactly the configurations bench.py runs (BASELINE configs 2-5 at their own
+sizes, default seeds and init scales), through the C ABI the render path uses.
+
+Bars (BASELINE.json north_star): sample counts, skip masks, foreground flags and hash
+indices bit-exact; rendered RGB/alpha and gradients within 1e-3 absolute.
+
+* the production march (``fv_march_compact``: the kernel ``fv_render_fwd`` launches) at the
+  full 512x512 x 128 config-2 frame: per-ray counts, per-sample box-hit / occupancy-skip /
+  foreground flags and the compacted foreground stream, under the density-built grid of
+  the frame's pose and under the seeded body-ellipsoid grid;
+* the production gather arithmetic of ``k_radiance_tc`` (``fv_hash_index_paired``);
+* the config-3 training step (T = 2^19 fp16 grid, 128 samples, 2 x 32x32 patches) against
+  the oracle's float64 backward;
+* config 4 (pose sigma 0.3) renders at 64x64 and on 512x512 crops;
+* config 5 (4 subjects, 1024x1024, 192 samples per subject box) spot crops.
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import camera as ocam
+from oracle import encoding as oenc
+from oracle import pipeline as opipe
+from oracle import scene as oscene
+from oracle import warp as owarp
+from oracle.adapter import settings as osettings
+from paper_2306_16541_b200 import _lib
+from paper_2306_16541_b200 import scene as psc
+from paper_2306_16541_b200.model import FreeviewModel
+from paper_2306_16541_b200.render import (RenderSettings, Renderer, SceneRenderer, camera_struct, march_struct,
+                                          scene_settings)
+from paper_2306_16541_b200.scene import target_image
+from paper_2306_16541_b200.train import Trainer, patch_pixels, sample_patches
+
+from helpers import blocked_to_ray_major, make, oracle_scene
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+_KEEP = []
+
+
+def _t(a, dtype=torch.float32):
+    t = torch.from_numpy(np.ascontiguousarray(a)).to(DEV, dtype)
+    _KEEP.append(t)
+    return t
+
+
+@pytest.fixture(scope="module")
+def c2bench():
+    """The bench's config-2 scene: default seeds and init scales, 512x512, 128 samples."""
+    sc = make("c2")
+    return sc, FreeviewModel(sc)
+
+
+def _march_compact(nets, cam, st, occ):
+    r = cam.width * cam.height
+    n = st.n_samples
+    S = (r + 31) // 32 * 32 * n
+    rnd = Renderer()
+    pix = rnd.pixel_order(cam)
+    lik = torch.empty(S, device=DEV)
+    delta = torch.empty(S, device=DEV)
+    xsc = torch.empty((S, 4), device=DEV)
+    idx = torch.empty(S, dtype=torch.int32, device=DEV)
+    nfg = torch.zeros(1, dtype=torch.int32, device=DEV)
+    cnt = torch.empty(r, dtype=torch.int32, device=DEV)
+    flags = torch.empty(S, dtype=torch.uint8, device=DEV)
+    m, cs, w = march_struct(st, pix, occ), camera_struct(cam), nets.warp_struct()
+    _lib.check(nets.lib.fv_march_compact(C.byref(cs), C.byref(m), C.byref(w), r, lik.data_ptr(), delta.data_ptr(),
+                                         xsc.data_ptr(), idx.data_ptr(), nfg.data_ptr(), cnt.data_ptr(),
+                                         flags.data_ptr(), _lib.stream_ptr()), "fv_march_compact")
+    torch.cuda.synchronize()
+    k = int(nfg.item())
+    return (pix.cpu().numpy(), lik.cpu().numpy(), flags.cpu().numpy(), xsc[:k].cpu().numpy(), idx[:k].cpu().numpy(),
+            cnt.cpu().numpy())
+
+
+@pytest.mark.parametrize("grid", ["density", "ellipsoid"])
+def test_c2_full_frame_skip_and_foreground_masks_bitexact(c2bench, grid):
+    """512x512 x 128 samples (33.5 M slots): box-hit and occupancy-skip flags of every slot,
+    per-ray counts and the foreground-stream bookkeeping bit-exact against the oracle; the
+    likelihood (=> foreground flag) bit-exact on 150 K sampled slots through the oracle warp."""
+    sc, nets = c2bench
+    cfg = sc.cfg
+    st = RenderSettings.from_config(cfg, seed=sc.jitter_seed)
+    rnd = Renderer()
+    if grid == "density":
+        occ = rnd.build_occupancy(nets, st).clone()
+    else:
+        occ = _t(psc.ellipsoid_occupancy(st.box_min, st.box_max), torch.int32)
+    bits = occ.cpu().numpy().view(np.uint32)
+    pix, lik, flags, xsc, idx, cnt = _march_compact(nets, sc.camera, st, occ)
+    n = cfg.n_samples
+    r = len(pix)
+    osc = oracle_scene(sc, nets=nets)
+    cc = ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera)
+    fl = blocked_to_ray_major(flags, r, n)          # (R, N) in pixel-order ray index
+    lk = blocked_to_ray_major(lik, r, n)
+    hit_all = np.zeros(r, bool)
+    occ_all = np.zeros((r, n), bool)
+    rng = np.random.default_rng(7)
+    pick_r, pick_i, pick_x = [], [], []
+    for c0 in range(0, r, 16384):                   # chunked: bounded host memory
+        p = pix[c0:c0 + 16384]
+        o, d = ocam.rays_f32(cc, p, cfg.width)
+        t0, t1, hit = ocam.slab_f32(o, d, osc["obox_min"], osc["obox_max"])
+        t, _, count = ocam.stratified_f32(t0, t1, hit, p, n, True, st.seed)
+        assert np.array_equal(cnt[c0:c0 + 16384], count)
+        x = ocam.positions_f32(o, d, t)
+        cell = ocam.occ_cell(x, osc["obox_min"], ocam.occ_scale(osc["obox_min"], osc["obox_max"]))
+        oc = ocam.occ_test(bits, cell) & hit[:, None]
+        hit_all[c0:c0 + 16384] = hit
+        occ_all[c0:c0 + 16384] = oc
+        rr, ii = np.nonzero(oc)
+        if len(rr):
+            sel = rng.choice(len(rr), min(len(rr), 150000 * 16384 // r + 1), replace=False)
+            pick_r.append(rr[sel] + c0)
+            pick_i.append(ii[sel])
+            pick_x.append(x[rr[sel], ii[sel]])
+    assert np.array_equal((fl & 1).astype(bool), np.broadcast_to(hit_all[:, None], (r, n)))
+    assert np.array_equal(((fl >> 1) & 1).astype(bool) & hit_all[:, None], occ_all)
+    # skipped / missed slots carry L = 0 and are never foreground
+    assert np.all(lk[~occ_all] == 0) and np.all((fl[~occ_all] & 4) == 0)
+    pr, pi, px = np.concatenate(pick_r), np.concatenate(pick_i), np.concatenate(pick_x)
+    wr = owarp.skeleton_warp(px, osc["g_r"], osc["g_t"], osc["vol"], osc["wbox_min"], osc["wbox_max"], st.eps_w,
+                             np.float32)
+    assert np.array_equal(lk[pr, pi], wr["L"])                       # bit-exact likelihood
+    assert np.array_equal(((fl[pr, pi] >> 2) & 1).astype(bool), wr["fg"])
+    assert 0.05 < wr["fg"].mean()
+    # the compacted stream is exactly the foreground slots, each with its own likelihood
+    fg_slots = np.nonzero(flags & 4)[0]
+    assert len(idx) == len(fg_slots)
+    assert np.array_equal(np.sort(idx), fg_slots)
+    assert np.array_equal(xsc[:, 3], lik[idx])
+    frac = occ_all.mean()
+    print(f"{grid} grid: {np.unpackbits(bits.view(np.uint8)).sum()} cells on, "
+          f"{frac:.3f} of slots marched, {len(idx) / flags.size:.3f} foreground")
+    if grid == "ellipsoid":
+        assert frac < 0.5 * hit_all.mean()          # the skip grid removes most in-box slots
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_production_gather_indices_bitexact(cfg):
+    """k_radiance_tc's lane-paired, strength-reduced corner indices (hash_levels_paired, via
+    fv_hash_index_paired) equal the oracle's hash indices bit for bit, incl. box faces,
+    outside points and an odd count (the last pair half-empty); blended features to fp32
+    rounding."""
+    sc = make(cfg)
+    nets = FreeviewModel(sc)
+    rng = np.random.default_rng(19)
+    x = rng.uniform(-1.2, 1.2, (40001, 3)).astype(np.float32)
+    x[:8] = [[-1, -1, -1], [1, 1, 1], [0, 0, 0], [1, -1, 0.5], [-1.0000001, 0, 0], [0.9999999, 0.5, -0.5],
+             [0.5, 1.0, -1.0], [2.0, -2.0, 0.25]]
+    n = len(x)
+    idx = torch.empty((n, 16, 8), dtype=torch.int32, device=DEV)
+    feat = torch.empty((n, 32), device=DEV)
+    h = nets.hash_struct()
+    _lib.check(nets.lib.fv_hash_index_paired(C.byref(h), _t(x).data_ptr(), n, idx.data_ptr(), feat.data_ptr(),
+                                             _lib.stream_ptr()), "fv_hash_index_paired")
+    osc = oracle_scene(sc)
+    cinv = (1.0 / (osc["wbox_max"] - osc["wbox_min"])).astype(np.float32)
+    of, oi = oenc.hash_encode(osc["hash_spec"], x, osc["wbox_min"].astype(np.float32), cinv, osc["table"],
+                              np.float32, return_index=True)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), oi)
+    scale = np.abs(of).max()
+    assert np.abs(feat.cpu().numpy() - of).max() <= 1e-5 * scale
+
+
+def test_c3_training_step_fp16_grid_gradients_match_oracle():
+    """Config 3 as the bench trains it: T = 2^19 fp16 table (fp32 master), res 16 -> 2048,
+    128 jittered samples, tensor-core (3xTF32) layers; 2 x 32x32 patches.  Loss within
+    1e-5 relative; every gradient block within the north star's 1e-3 absolute and within 3x
+    of the oracle's own sensitivity to a forward round-off nudge (the fine levels at 2048
+    cells amplify float32 position round-off; see test_full_step_gradients_match_oracle)."""
+    sc = make("c3")
+    nets = FreeviewModel(sc)
+    target, mask = target_image(sc)
+    st = RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed)
+    tr = Trainer(nets, sc.camera, target, mask, st, n_patches=2, patch=32, seed=11, precision="tf32")
+    pix = patch_pixels(sample_patches(mask, 2, 32, 11, 0), 32, sc.cfg.width)
+    loss = float(tr.forward(pix).item())
+    tr.backward()
+    torch.cuda.synchronize()
+    osc = oracle_scene(sc, nets=nets)
+    cc = ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera)
+    tgt = target.reshape(-1, 3)[pix]
+    ost = osettings(sc.cfg, seed=sc.jitter_seed)
+    oloss, og, r = opipe.loss_and_grads(osc, cc, pix, sc.cfg.width, ost, tgt)
+    assert r["fg"].mean() > 0.3
+    assert abs(loss - oloss) < 1e-5 * max(1.0, oloss), (loss, oloss)
+    nudged = dict(osc, off_b=[b.copy() for b in osc["off_b"]])
+    nudged["off_b"][4] = nudged["off_b"][4] + np.float32(1e-6)
+    _, og2, _ = opipe.loss_and_grads(nudged, cc, pix, sc.cfg.width, ost, tgt)
+
+    def rel(a, b):
+        return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-30)
+
+    G = tr.gviews
+    vol = osc["vol"].astype(np.float64)
+    pairs = [("table", G["table"], og["table"], og2["table"])]
+    pairs += [(f"rad_w{i}", G[f"rad_w{i}"], og["rad_w"][i], og2["rad_w"][i]) for i in range(3)]
+    pairs += [(f"rad_b{i}", G[f"rad_b{i}"], og["rad_b"][i], og2["rad_b"][i]) for i in range(3)]
+    pairs += [(f"off_w{i}", G[f"off_w{i}"], og["off_w"][i], og2["off_w"][i]) for i in range(5)]
+    pairs += [(f"off_b{i}", G[f"off_b{i}"], og["off_b"][i], og2["off_b"][i]) for i in range(5)]
+    pairs += [("vol_logits", G["vol_logits"], owarp.softmax0_bwd(vol, og["vol"]), owarp.softmax0_bwd(vol, og2["vol"]))]
+    for name, got, ref, ref2 in pairs:
+        got = got.cpu().numpy().astype(np.float64)
+        err = np.abs(got - ref).max()
+        fro = rel(got, ref)
+        bound = max(3.0 * rel(ref2, ref), 1e-4)
+        print(f"c3 {name}: max|ref| {np.abs(ref).max():.3e} max err {err:.3e} frobenius {fro:.2e} (bound {bound:.2e})")
+        assert err <= 1e-3, name
+        assert fro <= bound, name
+
+
+def _render_and_oracle(sc, nets, pose_index, pix, occupancy=True):
+    cfg = sc.cfg
+    st = RenderSettings.from_config(cfg, seed=sc.jitter_seed, occupancy=occupancy)
+    rnd = Renderer()
+    img, alpha = rnd.render_image(nets, sc.camera, sc.poses[pose_index], st)
+    torch.cuda.synchronize()
+    occ = rnd.occ.cpu().numpy().view(np.uint32) if occupancy else None
+    osc = oracle_scene(sc, pose_index=pose_index, nets=nets)
+    cc = ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera)
+    ref = opipe.render_rays(osc, cc, pix, cfg.width, osettings(cfg, seed=sc.jitter_seed, occupancy=occ), np.float32)
+    rgb = img.cpu().numpy().reshape(-1, 3)[pix]
+    a = alpha.cpu().numpy().reshape(-1)[pix]
+    return rgb, a, ref
+
+
+@pytest.mark.parametrize("pose_index", [0, 3, 7])
+def test_c4_poses_render_parity_64(pose_index):
+    """Config 4's sigma = 0.3 poses (fp16 tables/MLPs, occupancy from the pose's density) at
+    64x64: RGB/alpha within 1e-3 of the oracle given the same skip bits."""
+    sc = make("c4", width=64, height=64)
+    nets = FreeviewModel(sc)
+    rgb, a, ref = _render_and_oracle(sc, nets, pose_index, np.arange(64 * 64))
+    err = max(np.abs(rgb - ref["rgb"]).max(), np.abs(a - ref["alpha"]).max())
+    print(f"c4 pose {pose_index} 64x64: max err {err:.2e}, fg {ref['fg'].mean():.3f}")
+    assert err < 1e-3
+    assert ref["fg"].mean() > 0.05
+
+
+def test_c4_full_size_crop_parity():
+    """Config 4 at its own 512x512 size, two poses, two random 16x16 crops each."""
+    sc = make("c4")
+    nets = FreeviewModel(sc)
+    rng = np.random.default_rng(4)
+    for pose_index in (1, 6):
+        y0, x0 = rng.integers(160, 352 - 16, 2)
+        yy, xx = np.meshgrid(np.arange(y0, y0 + 16), np.arange(x0, x0 + 16), indexing="ij")
+        pix = (yy * 512 + xx).reshape(-1)
+        rgb, a, ref = _render_and_oracle(sc, nets, pose_index, pix)
+        err = max(np.abs(rgb - ref["rgb"]).max(), np.abs(a - ref["alpha"]).max())
+        print(f"c4 pose {pose_index} 512 crop ({y0},{x0}): max err {err:.2e}")
+        assert err < 1e-3
+
+
+def test_c5_full_size_spot_crops():
+    """Config 5 as the bench renders it (4 subjects with own T = 2^19 grids, 1024x1024, 192
+    samples per subject box, occupancy per subject pose): 8x8 crops where subjects are seen,
+    against the oracle's per-subject render + depth-ordered merge (oracle/scene.py)."""
+    ms = psc.make_multi_scene(psc.config("c5"))
+    nets = [FreeviewModel(s) for s in ms.subjects]
+    st = scene_settings(ms)
+    sr = SceneRenderer(len(nets), DEV)
+    poses = [s.poses[0] for s in ms.subjects]
+    img, alpha = sr.render_scene(nets, ms, st, tuple(ms.cfg.background), poses=poses)
+    torch.cuda.synchronize()
+    img, alpha = img.cpu().numpy().reshape(-1, 3), alpha.cpu().numpy().reshape(-1)
+    scenes, ccs, sts = [], [], []
+    for s, (sub, nt) in enumerate(zip(ms.subjects, nets)):
+        scenes.append(oracle_scene(sub, nets=nt))
+        cam = ms.subject_camera(s)
+        ccs.append(ocam.camera_consts(cam.intrinsics, cam.world_to_camera))
+        sts.append(osettings(sub.cfg, seed=sub.jitter_seed, occupancy=sr.renderers[s].occ.cpu().numpy().view(np.uint32)))
+    w = ms.camera.width
+    # crop centres: the projected centre of two subjects' boxes
+    checked = 0
+    for s in range(len(nets)):
+        cam = ms.subject_camera(s)
+        ctr = 0.5 * (np.asarray(st[s].box_min) + np.asarray(st[s].box_max))
+        pc = cam.world_to_camera[:3, :3] @ ctr + cam.world_to_camera[:3, 3]
+        if pc[2] <= 0:
+            continue
+        uv = cam.intrinsics @ pc
+        u, v = int(uv[0] / uv[2]), int(uv[1] / uv[2])
+        if not (8 <= u < w - 8 and 8 <= v < w - 8):
+            continue
+        yy, xx = np.meshgrid(np.arange(v - 4, v + 4), np.arange(u - 4, u + 4), indexing="ij")
+        pix = (yy * w + xx).reshape(-1)
+        ref = oscene.render_scene_rays(scenes, ccs, pix, w, sts, np.asarray(ms.cfg.background, np.float32))
+        err = max(np.abs(img[pix] - ref["rgb"]).max(), np.abs(alpha[pix] - ref["alpha"]).max())
+        print(f"c5 subject {s} crop at ({v},{u}): max err {err:.2e}, subjects hit {ref['hit'].sum(0).max()}")
+        assert ref["hit"].any(axis=0).all()
+        assert err < 1e-3
+        checked += 1
+        if checked == 2:
+            break
+    assert checked == 2

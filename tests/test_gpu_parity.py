@@ -139,8 +139,30 @@ def test_field_fp32_parity(c1):
     assert np.all(out.cpu().numpy()[~wr["fg"]] == 0)
 
 
-def test_field_tc_fp16_parity(c2s):
-    sc, nets, osc = c2s
+def _field_at(osc, xf):
+    """Oracle hash grid + radiance MLP + heads at given canonical points (float32)."""
+    from oracle import mlp as omlp
+    cinv = (1.0 / (osc["wbox_max"] - osc["wbox_min"])).astype(np.float32)
+    feat = oenc.hash_encode(osc["hash_spec"], xf, osc["wbox_min"].astype(np.float32), cinv, osc["table"], np.float32)
+    h = omlp.mlp_forward(feat, osc["rad_w"], osc["rad_b"], np.float32)
+    return omlp.radiance_heads(h)
+
+
+@pytest.mark.parametrize("table", ["bench", "stress"])
+def test_field_tc_fp16_parity(c2s, table):
+    """fp16 tensor-core field (k_offset_tc + k_radiance_tc) vs the fp32 oracle, maxima over
+    20 K points.  "bench": the config-2 model exactly as bench.py renders it -- x_final, c and
+    sigma all within the north star's 1e-3.  "stress": a +-0.5 random table (5000x the
+    BASELINE init): x_final stays within 1e-3, but the finest levels (2048 cells over 2 m)
+    turn its fp16 round-off into feature changes of up to ~0.5 x (x_final error / cell), so c
+    and sigma are held to 1e-3 against the oracle evaluated at the GPU's own x_final (the
+    radiance stage alone) and to a mean bound against the end-to-end oracle."""
+    if table == "bench":
+        sc = make("c2", width=64, height=64)
+        nets = FreeviewModel(sc)
+        osc = oracle_scene(sc, nets=nets)
+    else:
+        sc, nets, osc = c2s
     rng = np.random.default_rng(4)
     x = rng.uniform(-1.0, 1.0, (20000, 3)).astype(np.float32)
     wr = owarp.skeleton_warp(x, osc["g_r"], osc["g_t"], osc["vol"], osc["wbox_min"], osc["wbox_max"], 1e-4,
@@ -150,12 +172,22 @@ def test_field_tc_fp16_parity(c2s):
     out, xf = _field(nets, _t(xs4), 1e-4, True, want_xfinal=True)
     of = opipe._field(osc, wr["x_skel"][wr["fg"]], osettings(sc.cfg), np.float32)
     got = out.cpu().numpy()[wr["fg"]]
-    ex = np.abs(xf.cpu().numpy()[wr["fg"]] - of["x_final"])
+    xfg = xf.cpu().numpy()[wr["fg"]]
+    ex = np.abs(xfg - of["x_final"])
     ec = np.abs(got[:, :3] - of["c"])
     es = np.abs(got[:, 3] - of["sigma"])
-    print(f"tc field: x_final max {ex.max():.2e} mean {ex.mean():.2e}; c max {ec.max():.2e}; sigma max {es.max():.2e}")
-    assert np.mean(ex) < 2e-3 and np.mean(ec) < 2e-3 and np.mean(es) < 2e-3
+    print(f"tc field ({table}): x_final max {ex.max():.2e} mean {ex.mean():.2e}; c max {ec.max():.2e}; "
+          f"sigma max {es.max():.2e}")
+    assert ex.max() < 1e-3
     assert np.all(out.cpu().numpy()[~wr["fg"]] == 0)
+    if table == "bench":
+        assert ec.max() < 1e-3 and es.max() < 1e-3
+    else:
+        c_at, s_at = _field_at(osc, xfg)
+        ec2, es2 = np.abs(got[:, :3] - c_at), np.abs(got[:, 3] - s_at)
+        print(f"  at the GPU's x_final: c max {ec2.max():.2e}; sigma max {es2.max():.2e}")
+        assert ec2.max() < 1e-3 and es2.max() < 1e-3
+        assert ec.mean() < 2e-3 and es.mean() < 2e-3
 
 
 def _render_both(sc, nets, osc, settings_kw, res=None):
