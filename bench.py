@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--train-steps", type=int, default=20)
     p.add_argument("--no-scene", action="store_true", help="skip the config-5 multi-subject measurement")
     p.add_argument("--no-occ-variants", action="store_true", help="skip the dense / ellipsoid-occupancy runs")
+    p.add_argument("--no-trained", action="store_true", help="skip the trained-model occupancy / early-termination runs")
     return p.parse_args()
 
 
@@ -333,10 +334,20 @@ def run_ours(args, rank, world, local_rank):
     stages = stage_times(nets, rnd, cam, st, dev, occ_on, reps=max(3, min(args.steps, 10)))
     n_samples_launch = ((n_rays + 31) // 32 * 32) * cfg.n_samples
     roofs = stage_rooflines(stages, cfg, n_samples_launch, stages.get("fg_samples", n_samples_launch))
+    gather = gather_rates(nets, rnd, cam, st, dev) if rank == 0 else None
+    if gather is not None and "radiance" in roofs:
+        # the gather-bound kernel against the measured L2-resident gather ceiling too
+        ceil = gather["random_points"]["useful_GBps"]
+        ach = 512.0 * stages["fg_samples"] / (stages["radiance"] * 1e-3) / 1e9
+        roofs["radiance"]["l2_gather"] = {"achieved_useful_GBps": ach, "peak_useful_GBps": ceil, "frac": ach / ceil,
+                                          "peak_source": "fv_gather_probe mode 1 (random points, same pattern), "
+                                                         "measured in this run",
+                                          "gather_only_real_stream_ms": gather["real_stream"]["ms"]}
     dominant = max(roofs, key=lambda k: stages.get(k, 0.0))
     roof = dict(roofs[dominant])
 
     occ_var = occupancy_variants(nets, rnd, cam, st, dev) if rank == 0 and not args.no_occ_variants else None
+    trained = subject_variants(args, dev) if rank == 0 and not args.no_trained else None
     train = None if args.no_train else train_throughput(args, rank, world, dev)
     multi = None if args.no_scene else scene_throughput(args, rank, world, dev)
 
@@ -366,6 +377,8 @@ def run_ours(args, rank, world, local_rank):
             "multi_subject": multi,
             "stages_ms": stages,
             "occupancy_variants": occ_var,
+            "skip_and_termination": trained,
+            "gather_probe": gather,
             "roofline": roof,
             "stage_rooflines": roofs,
             "cpu_baseline": cpu,
@@ -388,7 +401,8 @@ def stage_rooflines(stages, cfg, n_all, n_fg):
     The march and compositor touch every sample slot; the field kernels run on the compacted
     foreground stream (n_fg samples)."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    peaks = json.load(open(path)) if os.path.exists(path) else {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0}
+    peaks = json.load(open(path)) if os.path.exists(path) else {"hbm_gbs": 6650.0, "bf16_tflops": 2250.0,
+                                                                "bf16_tflops_sustained": 1400.0}
     src = "MEASURED_PEAKS.json" if os.path.exists(path) else "fallback (B200_PROFILING.md)"
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
@@ -399,8 +413,11 @@ def stage_rooflines(stages, cfg, n_all, n_fg):
         sec = stages[key] * 1e-3
         n_samples = n_fg if key in ("offset", "radiance") else n_all
         if bound == "tensor":
-            ach, pk, u = n_samples * unit / sec / 1e12, peaks.get("bf16_tflops_sustained", 1394.7), "TFLOP/s"
-            psrc = src + " bf16_tflops_sustained (fp16 MMA assumed equal)"
+            # graded against the BURST peak: the kernel runs ~3 ms inside a 10 ms frame at the
+            # full 1965 MHz (the bench's clock sampler), while the "sustained" figure was taken
+            # power-capped at a 1350 MHz median over 4 s of back-to-back 8192^3 GEMMs
+            ach, pk, u = n_samples * unit / sec / 1e12, peaks.get("bf16_tflops", 1630.4), "TFLOP/s"
+            psrc = src + " bf16_tflops (burst; fp16 MMA assumed equal)"
         else:
             if key == "march_warp" and not cfg.half:
                 unit = 796.0
@@ -410,6 +427,8 @@ def stage_rooflines(stages, cfg, n_all, n_fg):
         out[key] = {"kernel": kname, "bound": bound, "achieved": ach, "peak": pk, "unit": u, "frac": ach / pk,
                     "traffic": tr, "ms": stages[key], "algorithmic": f"{algo} x {n_samples} samples/launch",
                     "peak_source": psrc}
+        if bound == "tensor":
+            out[key]["frac_vs_sustained"] = ach / peaks.get("bf16_tflops_sustained", 1394.7)
     return out
 
 
@@ -621,6 +640,112 @@ def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5, occ_grid=None):
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
         out["occupancy_build"] = float(np.median(ts))
+    return out
+
+
+def _skip_variants(nets, sc, dev, reps=5):
+    """A model's 512x512 x 128 frame rendered (a) dense, (b) with the 32^3 occupancy grid
+    rebuilt from its density for the pose, (c) grid + early termination (eps_t = 1e-3,
+    marching rounds of 32 samples): device time, frames/s, the fraction of sample slots the
+    field evaluated, marched-and-evaluated work per stage."""
+    from paper_2306_16541_b200.render import RenderSettings, Renderer
+    rnd = Renderer(str(dev))
+    cam = sc.camera
+    n_rays = cam.width * cam.height
+    out = {}
+    for name, occ, eps_t in (("dense", False, 0.0), ("occupancy", True, 0.0), ("occupancy_early_term", True, 1e-3)):
+        st = RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed, occupancy=occ, eps_t=eps_t, round_samples=32)
+        s = stage_times(nets, rnd, cam, st, dev, occ, reps=reps)
+        out[name] = {"render_ms": s["render_total"], "frames_per_s": 1000.0 / s["render_total"],
+                     "rays_per_s": n_rays / (s["render_total"] / 1000.0), "evaluated_fraction": s["fg_fraction"],
+                     "stages_ms": {k: round(s[k], 4) for k in ("march_warp", "offset", "radiance", "composite")},
+                     "eps_t": eps_t}
+        if occ:
+            out[name]["occupancy_build_ms"] = s.get("occupancy_build")
+            out[name]["occupied_cells"] = int(sum(bin(int(v) & 0xFFFFFFFF).count("1") for v in rnd.occ.cpu().numpy()))
+    _, alpha = rnd.render_image(nets, cam, None, RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed,
+                                                                            occupancy=False))
+    out["alpha_mean"] = float(alpha.mean().item())
+    out["opaque_ray_fraction"] = float((alpha > 0.999).float().mean().item())
+    return out
+
+
+def subject_variants(args, dev, iters=1500, reps=5):
+    """North star (1) -- occupancy skipping and early termination -- on density fields with
+    structure, which random-init weights lack (their density is flat, every cell on):
+      * "opaque_subject": the config-2 model with a body density (scene.opaque_subject: ~90/m
+        inside a canonical ellipsoid, ~0 outside, seen through the skinning warp and residual
+        offsets) -- the stand-in for trained subject weights;
+      * "trained": the config-3 model after ``iters`` iterations of the bench's training step
+        on its single-view 2-D target (a single view does not pin down 3-D opacity, so this
+        field stays semi-transparent: reported for completeness)."""
+    import torch
+    from paper_2306_16541_b200 import scene as psc
+    from paper_2306_16541_b200.model import FreeviewModel
+    from paper_2306_16541_b200.render import RenderSettings
+    from paper_2306_16541_b200.train import Trainer
+    out = {}
+    sc = psc.opaque_subject(psc.make_scene(psc.config("c2")))
+    out["opaque_subject"] = _skip_variants(FreeviewModel(sc, device=str(dev)), sc, dev, reps)
+    sc = psc.make_scene(psc.config("c3"))
+    nets = FreeviewModel(sc, device=str(dev))
+    target, mask = psc.target_image(sc)
+    tr = Trainer(nets, sc.camera, target, mask, RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed),
+                 n_patches=6, patch=32, seed=3)
+    t0 = time.perf_counter()
+    for i in range(iters):
+        tr.step(i)
+    torch.cuda.synchronize()
+    train_s = time.perf_counter() - t0
+    tr.check_finite()
+    out["trained"] = _skip_variants(nets, sc, dev, reps)
+    out["trained"]["what"] = f"config-3 model after {iters} training iterations ({train_s:.1f} s)"
+    out["trained"]["final_loss"] = float(tr.loss[0].item())
+    return out
+
+
+def gather_rates(nets, rnd, cam, st, dev, reps=5):
+    """The radiance kernel's gather stage alone (fv_gather_probe) on (a) the frame's real
+    foreground x_final stream and (b) as many uniformly random box points (compulsory L1
+    misses from the L2-resident table, same lane-paired access pattern): the measured gather
+    ceiling the radiance kernel is graded against besides HBM."""
+    import ctypes as C
+    import torch
+    from paper_2306_16541_b200 import _lib
+    from paper_2306_16541_b200.render import camera_struct, march_struct
+    lib = nets.lib
+    sp = torch.cuda.current_stream().cuda_stream
+    pix = rnd.pixel_order(cam)
+    r = pix.numel()
+    S = (r + 31) // 32 * 32 * st.n_samples
+    occ = rnd.build_occupancy(nets, st) if st.occupancy else None
+    lik = torch.empty(S, device=dev)
+    delta = torch.empty(S, device=dev)
+    xsc = torch.empty((S, 4), device=dev)
+    idx = torch.empty(S, dtype=torch.int32, device=dev)
+    nfg = torch.zeros(1, dtype=torch.int32, device=dev)
+    m, cs, w = march_struct(st, pix, occ), camera_struct(cam), nets.warp_struct()
+    _lib.check(lib.fv_march_compact(C.byref(cs), C.byref(m), C.byref(w), r, lik.data_ptr(), delta.data_ptr(),
+                                    xsc.data_ptr(), idx.data_ptr(), nfg.data_ptr(), None, None, sp), "fv_march_compact")
+    n = int(nfg.item())
+    xf = torch.empty((n, 4), device=dev)
+    f, h = nets.field_struct(), nets.hash_struct()
+    _lib.check(lib.fv_residual_offset(C.byref(f), xsc.data_ptr(), n, st.eps_w, xf.data_ptr(), sp), "fv_residual_offset")
+    del lik, delta, xsc, idx
+    sink = torch.empty(256 * 148 * 8, device=dev)
+    out = {"samples": n}
+    for name, mode in (("real_stream", 0), ("random_points", 1)):
+        ts = []
+        for _ in range(reps + 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            _lib.check(lib.fv_gather_probe(C.byref(h), xf.data_ptr(), n, mode, sink.data_ptr(), sink.numel(), sp),
+                       "fv_gather_probe")
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms = float(np.median(ts[1:]))
+        out[name] = {"ms": ms, "useful_GBps": 512.0 * n / (ms * 1e-3) / 1e9, "samples_per_s": n / (ms * 1e-3)}
     return out
 
 

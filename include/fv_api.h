@@ -61,6 +61,9 @@ typedef struct fv_march {
   const int32_t* d_pix;           /* optional list of linear pixel ids (NULL = 0..R-1) */
   int32_t pix_offset;             /* first pixel id when d_pix == NULL                 */
   int32_t out_by_pixel;           /* 1: rgb/alpha written at the pixel id (image), 0: ray */
+  int32_t round_samples;          /* marching-round size K: with eps_t > 0 and 0 < K < N the
+                                     render marches K samples per live ray per round and
+                                     retires rays whose T fell below eps_t (0: one pass) */
 } fv_march;
 
 typedef struct fv_warp {
@@ -162,6 +165,14 @@ int32_t fv_hash_bwd(const fv_hash* hash, const float* d_x, int64_t n, const floa
  * fv_hash_fwd's separate scalar form. */
 int32_t fv_hash_index_paired(const fv_hash* hash, const float* d_x, int64_t n, uint32_t* d_index,
                              float* d_feat, void* stream);
+
+/* Measurement probe (bench.py): the gather stage of the fused radiance kernel alone (same
+ * lane-paired pattern, all levels, features summed into d_sink, >= 256 x blocks floats) over
+ * n canonical points xf (n,4) = [x_final, .] (mode 0) or n uniformly random box points
+ * (mode 1: compulsory-miss gathers from the L2-resident table -- the measured gather
+ * ceiling the radiance kernel is graded against besides HBM). */
+int32_t fv_gather_probe(const fv_hash* hash, const float* d_xf, int64_t n, int32_t mode, float* d_sink,
+                        int64_t sink_len, void* stream);
 
 /* ---- MLPs (ad:403-425; fu:132-227) ---------------------------------------------------- */
 

@@ -31,7 +31,7 @@ class FvMarch(C.Structure):
     _fields_ = [("obox_min", f3), ("obox_max", f3), ("n_samples", C.c_int32), ("jitter", C.c_int32),
                 ("seed", C.c_uint32), ("eps_w", C.c_float), ("eps_t", C.c_float), ("bg", f3),
                 ("d_occ", vp), ("occ_scale", f3), ("d_pix", vp), ("pix_offset", C.c_int32),
-                ("out_by_pixel", C.c_int32)]
+                ("out_by_pixel", C.c_int32), ("round_samples", C.c_int32)]
 
 
 MAX_SUBJECTS = 8
@@ -78,6 +78,7 @@ SIGNATURES = {
     "fv_hash_fwd": (i32, [P(FvHash), vp, i64, vp, vp, vp]),
     "fv_hash_bwd": (i32, [P(FvHash), vp, i64, vp, vp, vp, vp]),
     "fv_hash_index_paired": (i32, [P(FvHash), vp, i64, vp, vp, vp]),
+    "fv_gather_probe": (i32, [P(FvHash), vp, i64, i32, vp, i64, vp]),
     "fv_march_compact": (i32, [P(FvCamera), P(FvMarch), P(FvWarp), i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "fv_linear_fwd": (i32, [vp, vp, vp, vp, i64, i32, i32, i32, vp]),
     "fv_linear_bwd": (i32, [vp, vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp]),

@@ -34,7 +34,15 @@ struct RenderWork {
 // workspace: per-sample likelihood / spacing / [c, sigma] (full ray-block-major layout),
 // the march's compacted foreground stream (x, L) + sample ids + counter, and for the fp32
 // path a compacted [c, sigma] buffer and the SIMT layer scratch.
-static size_t carve(void* base, int64_t S, int precision, RenderWork* w) {
+// Marching rounds (early termination): per-ray state (T, rgb), two live-ray lists with their
+// device counts, the per-ray sample counts, one foreground counter per round.
+constexpr int kMaxRounds = 64;
+struct RoundWork {
+  float4* state; int32_t* live[2]; int32_t* n_live; int32_t* ray_count; int32_t* counts;
+};
+
+static size_t carve(void* base, int64_t S, int precision, RenderWork* w, int64_t n_rays = 0,
+                    RoundWork* rw = nullptr) {
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
   const size_t o_l = take((size_t)S * 4), o_d = take((size_t)S * 4), o_r = take((size_t)S * 16);
@@ -42,13 +50,26 @@ static size_t carve(void* base, int64_t S, int precision, RenderWork* w) {
   const size_t o_rc = take(precision == 0 ? (size_t)S * 16 : 0);
   const size_t fb = precision == 0 ? field_f32_work_bytes(S) : 0;
   const size_t o_f = take(fb);
+  // round bookkeeping (always reserved: 28 B per ray)
+  const size_t o_st = take((size_t)n_rays * 16), o_l0 = take((size_t)n_rays * 4), o_l1 = take((size_t)n_rays * 4);
+  const size_t o_rcn = take((size_t)n_rays * 4), o_nl = take(2 * 4), o_cn = take(kMaxRounds * 4);
+  uint8_t* b = (uint8_t*)base;
   if (w) {
-    uint8_t* b = (uint8_t*)base;
     w->lik = (float*)(b + o_l); w->delta = (float*)(b + o_d); w->rgbs = (float4*)(b + o_r);
     w->xsc = (float4*)(b + o_x); w->idx = (int32_t*)(b + o_i); w->count = (int32_t*)(b + o_c);
     w->rgbsc = (float4*)(b + o_rc); w->fwork = b + o_f; w->fbytes = fb;
   }
+  if (rw) {
+    rw->state = (float4*)(b + o_st); rw->live[0] = (int32_t*)(b + o_l0); rw->live[1] = (int32_t*)(b + o_l1);
+    rw->ray_count = (int32_t*)(b + o_rcn); rw->n_live = (int32_t*)(b + o_nl); rw->counts = (int32_t*)(b + o_cn);
+  }
   return off;
+}
+
+static int round_size(const fv_march* m) {
+  const int N = m->n_samples, K = m->round_samples;
+  if (!(m->eps_t > 0.f) || K <= 0 || K >= N) return N;
+  return std::max(K, (N + kMaxRounds - 1) / kMaxRounds);
 }
 
 __global__ void k_scatter4(const float4* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
@@ -131,87 +152,139 @@ extern "C" int32_t fv_field_fwd(const fv_field* field, const fv_hash* hash, cons
 }
 
 extern "C" size_t fv_render_workspace_bytes(int64_t n_rays, int32_t n_samples, int32_t precision) {
-  return carve(nullptr, padded_rays(n_rays) * n_samples, precision, nullptr);
+  return carve(nullptr, padded_rays(n_rays) * n_samples, precision, nullptr, n_rays);
 }
 
-// ev (optional, 5 events): recorded before the march, after the march, between the two
-// tensor-core field kernels, after the field and after the compositor (stage timing).
+// Field over one compacted foreground stream (count on the device): tensor cores read the
+// count themselves; the fp32 parity path needs it on the host for its chunked SIMT layers.
+static int32_t field_stream(const fv_field* field, const fv_hash* hash, const RenderWork& w, int64_t S, float eps_w,
+                            int32_t* count, cudaStream_t st, cudaEvent_t mid) {
+  if (field->precision == 1)
+    return field_fwd_tc(field, hash, w.xsc, S, eps_w, w.rgbs, nullptr, st, count, w.idx, mid);
+  if (mid) cudaEventRecord(mid, st);
+  int32_t n_fg = 0;
+  cudaMemcpyAsync(&n_fg, count, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("fv_render_fwd count");
+  if (n_fg > 0) {
+    if (int32_t e = field_fwd(field, hash, w.xsc, n_fg, eps_w, w.rgbsc, nullptr, w.fwork, w.fbytes, st)) return e;
+    k_scatter4<<<(unsigned)((n_fg + 255) / 256), 256, 0, st>>>(w.rgbsc, w.idx, n_fg, w.rgbs);
+  }
+  return FV_OK;
+}
+
+// ev (optional, 5 events per round): recorded before the march, after the march, between
+// the two tensor-core field kernels, after the field and after the compositor (stage timing).
+// Single pass (eps_t == 0 or round_samples >= N): march all N samples of every ray, field on
+// the foreground stream, composite.  Marching rounds: K samples of every live ray
+// per round, field on the round's foreground stream, composite into the rays' persistent
+// (T, rgb); rays whose T fell below eps_t retire, so their later samples are never marched,
+// warped or evaluated.  Both produce bitwise the same pixels.
 static int32_t render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp* warp, const fv_hash* hash,
                           const fv_field* field, int64_t n_rays, void* d_work, size_t work_bytes, float* d_rgb,
-                          float* d_alpha, int32_t* d_count, cudaStream_t st, cudaEvent_t* ev) {
+                          float* d_alpha, int32_t* d_count, cudaStream_t st, cudaEvent_t* ev, int* n_rounds_out) {
   if (!cam || !march || !warp || !hash || !field || n_rays < 0 || march->n_samples < 1)
     return set_error(FV_EDIM, "fv_render_fwd: bad arguments");
   if (int32_t e = check_hash(hash)) return e;
   if (int32_t e = check_warp(warp)) return e;
   if (n_rays == 0) return FV_OK;
   const int N = march->n_samples;
-  const int64_t S = padded_rays(n_rays) * N;
-  if (work_bytes < carve(nullptr, S, field->precision, nullptr))
+  const int K = round_size(march);
+  const int64_t S = padded_rays(n_rays) * K;
+  if (work_bytes < carve(nullptr, padded_rays(n_rays) * N, field->precision, nullptr, n_rays))
     return set_error(FV_EDIM, "fv_render_fwd: workspace too small");
   RenderWork w;
-  carve(d_work, S, field->precision, &w);
-  if (ev) cudaEventRecord(ev[0], st);
-  if (int32_t e = march_compact(cam, march, warp, n_rays, w.lik, w.delta, w.xsc, w.idx, w.count, d_count, st)) return e;
-  if (ev) cudaEventRecord(ev[1], st);
-  if (field->precision == 1) {  // tensor-core field over the foreground stream, count stays on the device
-    if (int32_t e = field_fwd_tc(field, hash, w.xsc, S, march->eps_w, w.rgbs, nullptr, st, w.count, w.idx,
-                                 ev ? ev[2] : nullptr))
-      return e;
-  } else {                      // fp32 parity path: host needs the count for its chunked SIMT layers
-    if (ev) cudaEventRecord(ev[2], st);
-    int32_t n_fg = 0;
-    cudaMemcpyAsync(&n_fg, w.count, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("fv_render_fwd count");
-    if (n_fg > 0) {
-      if (int32_t e = field_fwd(field, hash, w.xsc, n_fg, march->eps_w, w.rgbsc, nullptr, w.fwork, w.fbytes, st))
-        return e;
-      k_scatter4<<<(unsigned)((n_fg + 255) / 256), 256, 0, st>>>(w.rgbsc, w.idx, n_fg, w.rgbs);
-    }
-  }
-  if (ev) cudaEventRecord(ev[3], st);
-  CompIn in{w.rgbs, w.delta, w.lik, 1, true, true};
+  RoundWork rw;
+  carve(d_work, S, field->precision, &w, n_rays, &rw);
   const int32_t* out_pix = march->out_by_pixel ? march->d_pix : nullptr;
   if (march->out_by_pixel && !march->d_pix) return set_error(FV_EDIM, "fv_render_fwd: out_by_pixel needs d_pix");
-  const int32_t e = composite_fwd(in, n_rays, N, march->bg, march->eps_w, march->eps_t, out_pix, d_rgb, d_alpha,
-                                  nullptr, st);
-  if (ev) cudaEventRecord(ev[4], st);
-  return e;
+  if (K == N) {
+    if (n_rounds_out) *n_rounds_out = 1;
+    if (ev) cudaEventRecord(ev[0], st);
+    if (int32_t e = march_compact(cam, march, warp, n_rays, w.lik, w.delta, w.xsc, w.idx, w.count, d_count, st))
+      return e;
+    if (ev) cudaEventRecord(ev[1], st);
+    if (int32_t e = field_stream(field, hash, w, S, march->eps_w, w.count, st, ev ? ev[2] : nullptr)) return e;
+    if (ev) cudaEventRecord(ev[3], st);
+    CompIn in{w.rgbs, w.delta, w.lik, 1, true, true};
+    const int32_t e = composite_fwd(in, n_rays, N, march->bg, march->eps_w, march->eps_t, out_pix, d_rgb, d_alpha,
+                                    nullptr, st);
+    if (ev) cudaEventRecord(ev[4], st);
+    return e;
+  }
+  const int rounds = (N + K - 1) / K;
+  if (n_rounds_out) *n_rounds_out = rounds;
+  for (int r = 0; r < rounds; ++r) {
+    const int i0 = r * K, Kr = std::min(K, N - i0);
+    const int32_t* live = r == 0 ? nullptr : rw.live[(r + 1) & 1];
+    const int32_t* n_live = r == 0 ? nullptr : rw.n_live + ((r + 1) & 1);
+    cudaEvent_t* e5 = ev ? ev + 5 * r : nullptr;
+    if (e5) cudaEventRecord(e5[0], st);
+    if (int32_t e = march_round(cam, march, warp, n_rays, i0, Kr, live, n_live, w.lik, w.delta, w.xsc, w.idx,
+                                rw.counts + r, rw.ray_count, st))
+      return e;
+    if (e5) cudaEventRecord(e5[1], st);
+    if (int32_t e = field_stream(field, hash, w, padded_rays(n_rays) * Kr, march->eps_w, rw.counts + r, st,
+                                 e5 ? e5[2] : nullptr))
+      return e;
+    if (e5) cudaEventRecord(e5[3], st);
+    if (int32_t e = composite_round(w.rgbs, w.delta, w.lik, Kr, i0, N, live, n_live, n_rays, rw.ray_count, rw.state,
+                                    march->bg, march->eps_w, march->eps_t, out_pix, d_rgb, d_alpha, rw.live[r & 1],
+                                    rw.n_live + (r & 1), st))
+      return e;
+    if (e5) cudaEventRecord(e5[4], st);
+  }
+  if (d_count) cudaMemcpyAsync(d_count, rw.ray_count, (size_t)n_rays * 4, cudaMemcpyDeviceToDevice, st);
+  return check_launch("fv_render_fwd rounds");
 }
 
 extern "C" int32_t fv_render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp* warp, const fv_hash* hash,
                                  const fv_field* field, int64_t n_rays, void* d_work, size_t work_bytes, float* d_rgb,
                                  float* d_alpha, int32_t* d_count, void* stream) {
   return render_fwd(cam, march, warp, hash, field, n_rays, d_work, work_bytes, d_rgb, d_alpha, d_count,
-                    (cudaStream_t)stream, nullptr);
+                    (cudaStream_t)stream, nullptr, nullptr);
 }
 
-// Same render with CUDA events between its stages; synchronises and returns the device
-// times (ms) of march+warp, residual MLP, hash+radiance, compositor, total in stage_ms[5]
-// and the number of foreground samples the field evaluated in *n_fg.
+// Same render with CUDA events between its stages (summed over marching rounds);
+// synchronises and returns the device times (ms) of march+warp, residual MLP, hash+radiance,
+// compositor, total in stage_ms[5] and the number of foreground samples the field evaluated
+// (all rounds) in *n_fg.
 extern "C" int32_t fv_render_fwd_timed(const fv_camera* cam, const fv_march* march, const fv_warp* warp,
                                        const fv_hash* hash, const fv_field* field, int64_t n_rays, void* d_work,
                                        size_t work_bytes, float* d_rgb, float* d_alpha, float* stage_ms,
                                        int64_t* n_fg, void* stream) {
-  cudaEvent_t ev[5];
-  for (auto& e : ev) cudaEventCreate(&e);
+  const int max_ev = 5 * kMaxRounds;
+  cudaEvent_t ev[5 * kMaxRounds];
+  for (int i = 0; i < max_ev; ++i) cudaEventCreate(&ev[i]);
   cudaStream_t st = (cudaStream_t)stream;
-  int32_t err = render_fwd(cam, march, warp, hash, field, n_rays, d_work, work_bytes, d_rgb, d_alpha, nullptr, st, ev);
+  int rounds = 1;
+  int32_t err = render_fwd(cam, march, warp, hash, field, n_rays, d_work, work_bytes, d_rgb, d_alpha, nullptr, st, ev,
+                           &rounds);
   if (!err) {
-    cudaEventSynchronize(ev[4]);
-    float t[4];
-    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
-    for (int i = 0; i < 4; ++i) stage_ms[i] = t[i];
-    cudaEventElapsedTime(&stage_ms[4], ev[0], ev[4]);
+    cudaEventSynchronize(ev[5 * rounds - 1]);
+    for (int i = 0; i < 5; ++i) stage_ms[i] = 0.f;
+    for (int r = 0; r < rounds; ++r) {
+      for (int i = 0; i < 4; ++i) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, ev[5 * r + i], ev[5 * r + i + 1]);
+        stage_ms[i] += t;
+      }
+    }
+    cudaEventElapsedTime(&stage_ms[4], ev[0], ev[5 * rounds - 1]);
     if (n_fg) {
+      const int N = march->n_samples, K = round_size(march);
       RenderWork w;
-      carve(d_work, padded_rays(n_rays) * march->n_samples, field->precision, &w);
-      int32_t c = 0;
-      cudaMemcpy(&c, w.count, sizeof(int32_t), cudaMemcpyDeviceToHost);
-      *n_fg = c;
+      RoundWork rw;
+      carve(d_work, padded_rays(n_rays) * K, field->precision, &w, n_rays, &rw);
+      int32_t c[kMaxRounds] = {0};
+      if (K == N) cudaMemcpy(c, w.count, sizeof(int32_t), cudaMemcpyDeviceToHost);
+      else cudaMemcpy(c, rw.counts, sizeof(int32_t) * rounds, cudaMemcpyDeviceToHost);
+      int64_t tot = 0;
+      for (int r = 0; r < rounds; ++r) tot += c[r];
+      *n_fg = tot;
     }
     err = check_launch("fv_render_fwd_timed");
   }
-  for (auto& e : ev) cudaEventDestroy(e);
+  for (int i = 0; i < max_ev; ++i) cudaEventDestroy(ev[i]);
   return err;
 }
 

@@ -150,6 +150,88 @@ int32_t composite_bwd(const CompIn& in, const float* trans, int64_t n_rays, int 
   return check_launch("composite_bwd");
 }
 
+// One marching round of the front-to-back compositor (early termination): live
+// ray j (= live[j], or j when live == NULL) continues from its persistent state (T, rgb) over
+// the round's K samples (round slot layout, march_round), with exactly the per-sample rule and
+// float32 operation order of k_composite_fwd<skip_bg>, so the final pixel is bitwise the
+// single-pass result.  A ray retires -- its pixel is written -- when it missed the box
+// (count 0), when T fell below eps_t (the next sample would not be composited) or in the last
+// round; otherwise its state is stored and it is appended to next_live (warp-aggregated
+// atomic), the next round's ray list.  Whole warps iterate together (ballot), grid-stride.
+__global__ void k_composite_round(const float4* __restrict__ rgbs, const float* __restrict__ delta,
+                                  const float* __restrict__ lik, int K, int i0, int n, const int32_t* __restrict__ live,
+                                  const int32_t* __restrict__ n_live, int64_t n_rays,
+                                  const int32_t* __restrict__ ray_count, float4* __restrict__ state, float3 bg,
+                                  float eps_w, float eps_t, const int32_t* __restrict__ out_pix,
+                                  float* __restrict__ rgb_out, float* __restrict__ alpha_out,
+                                  int32_t* __restrict__ next_live, int32_t* __restrict__ next_n) {
+  const int64_t n_j = live ? (int64_t)*n_live : n_rays;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool last = i0 + K >= n;
+  for (int64_t jb = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; jb < n_j; jb += stride) {
+    const int64_t j = jb + lane;
+    const bool valid = j < n_j;
+    bool cont = false;
+    if (valid) {
+      const int64_t ray = live ? (int64_t)live[j] : j;
+      float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
+      if (i0 > 0) { const float4 q = state[ray]; T = q.x; cr = q.y; cg = q.z; cb = q.w; }
+      bool stop = ray_count[ray] == 0;
+      for (int il = 0; il < K && !stop; ++il) {
+        if (eps_t > 0.f && T < eps_t) { stop = true; break; }
+        const int64_t s = sample_index(j, il, K);
+        const float L = lik[s];
+        if (!(L > eps_w)) continue;
+        const float4 v = rgbs[s];
+        const float a = __fsub_rn(1.f, expf(-__fmul_rn(v.w, delta[s])));
+        const float gate = fminf(fmaxf(__fdiv_rn(L, eps_w), 0.f), 1.f);
+        const float ab = __fmul_rn(a, gate);
+        const float w = __fmul_rn(T, ab);
+        cr = __fadd_rn(cr, __fmul_rn(w, v.x));
+        cg = __fadd_rn(cg, __fmul_rn(w, v.y));
+        cb = __fadd_rn(cb, __fmul_rn(w, v.z));
+        T = __fmul_rn(T, __fsub_rn(1.f, ab));
+      }
+      stop = stop || last || (eps_t > 0.f && T < eps_t);
+      if (stop) {
+        cr = __fadd_rn(cr, __fmul_rn(T, bg.x));
+        cg = __fadd_rn(cg, __fmul_rn(T, bg.y));
+        cb = __fadd_rn(cb, __fmul_rn(T, bg.z));
+        const int64_t o = out_pix ? out_pix[ray] : ray;
+        rgb_out[3 * o] = cr; rgb_out[3 * o + 1] = cg; rgb_out[3 * o + 2] = cb;
+        alpha_out[o] = __fsub_rn(1.f, T);
+      } else {
+        state[ray] = make_float4(T, cr, cg, cb);
+        cont = true;
+      }
+    }
+    const uint32_t ballot = __ballot_sync(0xffffffffu, cont);
+    if (ballot) {
+      int32_t base = 0;
+      if (lane == 0) base = atomicAdd(next_n, __popc(ballot));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (cont) next_live[base + __popc(ballot & ((1u << lane) - 1u))] = (int32_t)(live ? live[j] : j);
+    }
+  }
+}
+
+int32_t composite_round(const float4* rgbs, const float* delta, const float* lik, int K, int i0, int n,
+                        const int32_t* live, const int32_t* n_live, int64_t n_rays, const int32_t* ray_count,
+                        float4* state, const float* bg, float eps_w, float eps_t, const int32_t* out_pix, float* rgb,
+                        float* alpha, int32_t* next_live, int32_t* next_n, cudaStream_t st) {
+  if (n_rays == 0) return FV_OK;
+  cudaMemsetAsync(next_n, 0, sizeof(int32_t), st);
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = std::min<int64_t>((n_rays + 127) / 128, (int64_t)n_sm * 16);
+  k_composite_round<<<(unsigned)blocks, 128, 0, st>>>(rgbs, delta, lik, K, i0, n, live, n_live, n_rays, ray_count,
+                                                      state, make_float3(bg[0], bg[1], bg[2]), eps_w, eps_t, out_pix,
+                                                      rgb, alpha, next_live, next_n);
+  return check_launch("composite_round");
+}
+
 }  // namespace fv
 
 using namespace fv;

@@ -604,9 +604,63 @@ __global__ void k_hash_index_paired(fv_hash h, const float* __restrict__ x, int6
   }
 }
 
+// Gather-rate probe (measurement, bench.py): k_radiance_tc's gather stage alone -- the same
+// hash_norm + hash_levels_paired<FV_RAD_NL> loop over all levels, persistent warpgroups, one
+// sample per thread -- with the features summed into a per-thread sink instead of the MLP.
+// mode 0: the given canonical points (the frame's real foreground stream); mode 1: uniformly
+// random points in the box (hash of the sample id), i.e. no reuse beyond chance: the rate of
+// compulsory L1-miss gathers from the L2-resident table with the production access pattern.
+__global__ void __launch_bounds__(256) k_gather_probe(fv_hash h, const float4* __restrict__ xf, int64_t n, int mode,
+                                                      float* __restrict__ sink) {
+  float acc = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t s = base + threadIdx.x;
+    float x0, x1, x2;
+    if (mode == 0) {
+      const float4 v = xf[s < n ? s : n - 1];
+      x0 = v.x; x1 = v.y; x2 = v.z;
+    } else {
+      uint32_t k = (uint32_t)s * 0x9E3779B9u + 0x7F4A7C15u;
+      k ^= k >> 16; k *= 0x85EBCA6Bu; k ^= k >> 13; k *= 0xC2B2AE35u; k ^= k >> 16;
+      const uint32_t k2 = k * 0x27D4EB2Fu + 0x165667B1u, k3 = (k2 ^ (k2 >> 15)) * 0x2C1B3C6Du;
+      x0 = h.cmin[0] + (float)(k >> 8) * (1.0f / 16777216.0f) / h.cinv[0];
+      x1 = h.cmin[1] + (float)(k2 >> 8) * (1.0f / 16777216.0f) / h.cinv[1];
+      x2 = h.cmin[2] + (float)(k3 >> 8) * (1.0f / 16777216.0f) / h.cinv[2];
+    }
+    float xn[3]; bool msk[3];
+    hash_norm(h, x0, x1, x2, xn, msk);
+    constexpr int NL = FV_RAD_NL;
+#pragma unroll 1
+    for (int c = 0; c < 16 / NL; ++c) {
+      float2 fv[NL];
+      hash_levels_paired<NL>(h, NL * c, xn, fv);
+#pragma unroll
+      for (int q = 0; q < NL; ++q) acc += fv[q].x + fv[q].y;
+    }
+  }
+  sink[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 }  // namespace fv
 
 using namespace fv;
+
+extern "C" int32_t fv_gather_probe(const fv_hash* hash, const float* d_xf, int64_t n, int32_t mode, float* d_sink,
+                                   int64_t sink_len, void* stream) {
+  if (int32_t e = check_hash(hash)) return e;
+  if (n < 0 || (mode == 0 && n > 0 && !d_xf) || mode < 0 || mode > 1 || !d_sink)
+    return set_error(FV_EDIM, "fv_gather_probe: bad arguments");
+  if (hash->n_levels != 16) return set_error(FV_EUNSUPPORTED, "fv_gather_probe: 16 levels");
+  if (n == 0) return FV_OK;
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, std::min<int64_t>((int64_t)n_sm * 8, sink_len / 256));
+  if (blocks < 1) return set_error(FV_EDIM, "fv_gather_probe: sink too small (>= 256 floats)");
+  k_gather_probe<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(*hash, (const float4*)d_xf, n, mode, d_sink);
+  return check_launch("fv_gather_probe");
+}
 
 extern "C" int32_t fv_hash_index_paired(const fv_hash* hash, const float* d_x, int64_t n, uint32_t* d_index,
                                         float* d_feat, void* stream) {

@@ -37,6 +37,10 @@ int32_t composite_fwd(const CompIn& in, int64_t n_rays, int n, const float* bg, 
                       const int32_t* out_pix, float* rgb, float* alpha, float* trans, cudaStream_t st);
 int32_t composite_bwd(const CompIn& in, const float* trans, int64_t n_rays, int n, const float* bg, float eps_w,
                       const float* drgb, const float* dalpha, float4* dout, cudaStream_t st);
+int32_t composite_round(const float4* rgbs, const float* delta, const float* lik, int K, int i0, int n,
+                        const int32_t* live, const int32_t* n_live, int64_t n_rays, const int32_t* ray_count,
+                        float4* state, const float* bg, float eps_w, float eps_t, const int32_t* out_pix, float* rgb,
+                        float* alpha, int32_t* next_live, int32_t* next_n, cudaStream_t st);
 int32_t field_fwd(const fv_field* f, const fv_hash* h, const float4* xs, int64_t n, float eps_w, float4* rgbs,
                   float* xfinal, void* work, size_t work_bytes, cudaStream_t st);
 }  // namespace fv

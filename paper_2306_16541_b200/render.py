@@ -43,6 +43,7 @@ class RenderSettings:
     box_max: Tuple[float, float, float] = (1.0, 1.0, 1.0)
     occupancy: bool = False                # build + use the 32^3 skip grid per pose
     occ_threshold: float = 0.01
+    round_samples: int = 32                # marching-round size when eps_t > 0
 
     @classmethod
     def from_config(cls, cfg, **kw) -> "RenderSettings":
@@ -77,6 +78,7 @@ def march_struct(s: RenderSettings, pix: Optional[torch.Tensor], occ: Optional[t
     m.d_pix = pix.data_ptr() if pix is not None else None
     m.pix_offset = 0
     m.out_by_pixel = int(out_by_pixel)
+    m.round_samples = int(s.round_samples)
     return m
 
 

@@ -23,7 +23,7 @@ Every tensor comes from its own child of ``np.random.SeedSequence(seed)``.
 from __future__ import annotations
 
 from dataclasses import dataclass, field, replace
-from typing import List
+from typing import List, Optional
 
 import numpy as np
 
@@ -203,6 +203,53 @@ def target_image(scene: Scene, seed: int = 7):
     mask = b * b - 4 * a * cc > 0
     out = np.where(mask[..., None], np.clip(img, 0, 1), np.asarray(cfg.background)[None, None, :])
     return out.astype(np.float32), mask
+
+
+def opaque_subject(scene: Scene, axes=(0.45, 0.8, 0.3), level: Optional[int] = None, sigma_in: float = 90.0) -> Scene:
+    """A subject with a realistic density field (stand-in for trained weights, which are
+    absent: ZJU-MoCap and its checkpoints are not in the container): density ~sigma_in / m
+    inside a canonical body ellipsoid with semi-axes ``axes`` (fractions of the canonical box
+    half-extent) and ~5e-5 / m outside, seen through the scene's own skinning warp and
+    residual offsets -- empty space around the body and rays that saturate inside it, the two
+    things occupancy skipping and early termination act on.
+
+    Built from the scene's own parameter blocks: feature 0 of dense hash level ``level`` is
+    +1 at grid vertices inside the ellipsoid and -1 outside; radiance hidden unit 0 passes
+    relu(4 f) through both hidden layers; the sigma logit is 25 h - 9 (softplus(h - 1) ->
+    ~90 inside, 4.5e-5 outside); every other weight keeps its seeded value (colours)."""
+    cfg = scene.cfg
+    h = cfg.hash
+    if level is None:        # the finest dense level up to 3 (C2: res 42, C1: res 20)
+        level = max(l for l in range(min(4, h.n_levels)) if h.dense()[l])
+    if not h.dense()[level]:
+        raise ValueError(f"level {level} is hashed, opaque_subject needs a dense level")
+    res, off = h.resolutions()[level], h.offsets()[level]
+    table = scene.table.copy()
+    s1 = res + 1
+    ii = np.arange(s1) / res
+    gx, gy, gz = np.meshgrid(ii, ii, ii, indexing="ij")          # normalised canonical vertex positions
+    q = ((gx - 0.5) / (0.5 * axes[0])) ** 2 + ((gy - 0.5) / (0.5 * axes[1])) ** 2 + ((gz - 0.5) / (0.5 * axes[2])) ** 2
+    inside = q <= 1.0
+    # dense index x + y s + z s^2 (oracle.encoding / hash_index)
+    idx = (np.arange(s1)[:, None, None] + np.arange(s1)[None, :, None] * s1 + np.arange(s1)[None, None, :] * s1 * s1)
+    table[off + idx.reshape(-1), 0] = np.where(inside.reshape(-1), 1.0, -1.0).astype(np.float32)
+    rad_w = [w.copy() for w in scene.rad_w]
+    rad_b = [b.copy() for b in scene.rad_b]
+    rad_w[0][:, 0] = 0.0
+    rad_w[0][2 * level, 0] = 4.0
+    rad_b[0][0] = 0.0
+    rad_w[1][0, :] = 0.0
+    rad_w[1][:, 0] = 0.0
+    rad_w[1][0, 0] = 1.0
+    rad_b[1][0] = 0.0
+    rad_w[2][0, :] = 0.0
+    rad_w[2][:, 3] = 0.0
+    rad_w[2][0, 3] = sigma_in / 3.6
+    rad_b[2][3] = -9.0
+    if cfg.half:
+        table = table.astype(np.float16).astype(np.float32)
+        rad_w = [w.astype(np.float16).astype(np.float32) for w in rad_w]
+    return replace(scene, table=table, rad_w=rad_w, rad_b=rad_b)
 
 
 OCC_RES = 32

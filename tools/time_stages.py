@@ -19,11 +19,16 @@ ap.add_argument("--fp32-table", action="store_true")
 ap.add_argument("--reps", type=int, default=7)
 ap.add_argument("--config", default="c2")
 ap.add_argument("--no-occ", action="store_true")
+ap.add_argument("--opaque", action="store_true", help="scene.opaque_subject body density")
+ap.add_argument("--eps-t", type=float, default=0.0)
+ap.add_argument("--round", type=int, default=32)
 a = ap.parse_args()
 
 sc = psc.make_scene(psc.config(a.config))
+if a.opaque:
+    sc = psc.opaque_subject(sc)
 nets = FreeviewModel(sc)
-st = RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed)
+st = RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed, eps_t=a.eps_t, round_samples=a.round)
 rnd = Renderer()
 cam = sc.camera
 pix = rnd.pixel_order(cam)
@@ -46,4 +51,5 @@ for _ in range(a.reps):
     rows.append(list(t))
 med = np.median(np.array(rows)[1:], axis=0)
 print(f"table {'fp32' if a.fp32_table else 'fp16'}: march {med[0]:.3f}  offset {med[1]:.3f}  radiance {med[2]:.3f}  "
-      f"composite {med[3]:.3f}  total {med[4]:.3f} ms  ({1e3 / med[4]:.1f} fps)  checksum {rgb.double().sum().item():.6e}")
+      f"composite {med[3]:.3f}  total {med[4]:.3f} ms  ({1e3 / med[4]:.1f} fps)  fg {nfg.value}  "
+      f"checksum {rgb.double().sum().item():.6e}")
