@@ -396,6 +396,12 @@ KERNEL_UNITS = {
 }
 
 
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(path)) if os.path.exists(path) else {"hbm_gbs": 6650.0, "bf16_tflops": 2250.0,
+                                                               "bf16_tflops_sustained": 1400.0}
+
+
 def stage_rooflines(stages, cfg, n_all, n_fg):
     """Per-kernel roofline from the live CUDA-event stage times; peaks from MEASURED_PEAKS.json.
     The march and compositor touch every sample slot; the field kernels run on the compacted
@@ -482,7 +488,29 @@ def train_throughput(args, rank, world, dev):
         t = torch.tensor([ms, e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_ms = float(t[0]), float(t[1])
+    # per-op device times of one more step (CUDA events after every op on the launch stream)
+    # graded against HBM with each op's algorithmic bytes (Trainer._pm annotations)
+    peaks = _peaks()
+    ops = {}
+    for _ in range(3):
+        for lab, ops_ms, nb, _gbs in tr.profile_step(300):
+            o = ops.setdefault(lab, [0.0, 0.0, 0])
+            o[0] += ops_ms
+            o[1] += nb
+            o[2] += 1
+    prof_total = sum(o[0] for o in ops.values()) / 3.0
+    kernels = []
+    for lab, (t_ms, nb, cnt) in sorted(ops.items(), key=lambda kv: -kv[1][0]):
+        t = t_ms / 3.0
+        gbs = (nb / 3.0) / (t * 1e-3) / 1e9 if t > 0 else 0.0
+        kernels.append({"op": lab, "ms": round(t, 4), "share": round(t / prof_total, 4),
+                        "algorithmic_GB": round(nb / 3.0 / 1e9, 4), "achieved_GBps": round(gbs, 1),
+                        "frac_hbm": round(gbs / peaks["hbm_gbs"], 3)})
+    gemm_ms = sum(k["ms"] for k in kernels if k["op"].startswith("linear"))
     return {"metric": "train_iters_per_s", "value": 1000.0 / ms, "unit": "it/s", "ms_per_iter": ms,
+            "kernels": kernels, "profiled_step_ms": prof_total, "linear_layers_share": gemm_ms / prof_total,
+            "kernels_note": "per-op CUDA events (one step, mean of 3), algorithmic bytes per op (Trainer._pm), "
+                            "graded against MEASURED_PEAKS hbm_gbs",
             "e2e_iters_per_s": 1000.0 / e2e_ms,
             "e2e": {"value": 1000.0 / e2e_ms, "unit": "it/s", "h2d_bytes_per_step": tr.R * 4,
                     "d2h_bytes_per_step": 12},

@@ -182,6 +182,31 @@ class Trainer:
         self.residual = bool(residual)
 
     # ------------------------------------------------------------------------------------
+    # Per-op profiling (bench.py's training roofline): with ``self.prof`` a list, every op
+    # records a CUDA event on the launching stream after it, tagged with its ALGORITHMIC
+    # bytes per sample (activations read + written, gathers, atomics as 8-byte RMW).
+    prof = None
+
+    def _pm(self, label: str, bytes_per_sample: float, total: Optional[float] = None) -> None:
+        if self.prof is None:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(torch.cuda.current_stream())
+        self.prof.append((label, bytes_per_sample * self.S if total is None else total, ev))
+
+    def profile_step(self, step: int = 0):
+        """One full step with per-op events: [(op, ms, algorithmic bytes, GB/s)]."""
+        self.prof = []
+        self._pm("start", 0.0)
+        self.step(step)
+        torch.cuda.synchronize()
+        marks, self.prof = self.prof, None
+        out = []
+        for (_, _, e0), (lab, nb, e1) in zip(marks[:-1], marks[1:]):
+            ms = e0.elapsed_time(e1)
+            out.append((lab, ms, nb, nb / (ms * 1e-3) / 1e9 if ms > 0 else 0.0))
+        return out
+
     def _lin(self, x, w, b, y, k, n, act, sp, bits=None):
         bp = b.data_ptr() if b is not None else None
         if self.tc:
@@ -192,6 +217,7 @@ class Trainer:
         else:
             _lib.check(self.lib.fv_linear_fwd(x.data_ptr(), w.data_ptr(), bp, y.data_ptr(), self.S, k, n, act, sp),
                        "fv_linear_fwd")
+        self._pm(f"linear_fwd {k}x{n}", 4.0 * (x.shape[1] + n) + (4.0 * ((n + 31) // 32) if bits is not None else 0.0))
 
     def _lin_bwd_tc(self, x, w, dz, dx, xbits, dw, db, k, n, sp):
         """dz = masked pre-activation gradient of this layer; dx gets (dz W^T) * xbits, the
@@ -201,6 +227,8 @@ class Trainer:
                                                   dx.shape[1] if dx is not None else 0,
                                                   xbits.data_ptr() if xbits is not None else None, dw.data_ptr(),
                                                   db.data_ptr(), self.S, k, n, sp), "fv_linear_bwd_tc_bits")
+        dxb = (4.0 * n + 4.0 * k + (4.0 * ((k + 31) // 32) if xbits is not None else 0.0)) if dx is not None else 0.0
+        self._pm(f"linear_bwd {k}x{n} (dX+dW)", dxb + 4.0 * (x.shape[1] + n))
 
     def _lin_bwd(self, x, w, y, dy, dx, dw, db, k, n, act, sp):
         _lib.check(self.lib.fv_linear_bwd(x.data_ptr(), w.data_ptr(), y.data_ptr(), dy.data_ptr(),
@@ -238,24 +266,30 @@ class Trainer:
         h, eps = nets.hash_struct(), self.st.eps_w
         _lib.check(lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), self.R, self.xs.data_ptr(),
                                      self.delta.data_ptr(), self.x.data_ptr(), None, sp), "fv_march_warp")
+        self._pm("march_warp", 32.0 + nets.n_bones * (16.0 if nets.half else 32.0))
         V = nets.views
         if self.residual:
             _lib.check(lib.fv_posenc_fwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.pe.data_ptr(),
                                          self.pe_ld, sp))
+            self._pm("posenc_fwd", 16.0 + 4.0 * self.pe_ld)
             self._lin(self.pe, V["off_w0"], nets.b0_eff, self.h[0], self.d_pe, 128, 1, sp, self.hbits[0])
             for i in range(1, 4):
                 self._lin(self.h[i - 1], V[f"off_w{i}"], V[f"off_b{i}"], self.h[i], 128, 128, 1, sp, self.hbits[i])
             self._lin(self.h[3], V["off_w4"], V["off_b4"], self.xres, 128, 3, 0, sp)
         _lib.check(lib.fv_xfinal(self.xs.data_ptr(), self.xres.data_ptr() if self.residual else None, S, eps,
                                  self.xf.data_ptr(), sp))
+        self._pm("xfinal", 40.0)
         _lib.check(lib.fv_hash_fwd(C.byref(h), self.xf.data_ptr(), S, self.feat.data_ptr(), None, sp), "fv_hash_fwd")
+        self._pm("hash_fwd", 12.0 + 16 * 8 * (2.0 if nets.half else 8.0) + 128.0)
         self._lin(self.feat, V["rad_w0"], V["rad_b0"], self.r[0], 32, 64, 1, sp, self.rbits[0])
         self._lin(self.r[0], V["rad_w1"], V["rad_b1"], self.r[1], 64, 64, 1, sp, self.rbits[1])
         self._lin(self.r[1], V["rad_w2"], V["rad_b2"], self.hd, 64, 4, 0, sp)
         _lib.check(lib.fv_heads_fwd(self.xs.data_ptr(), self.hd.data_ptr(), S, eps, self.rgbs.data_ptr(), sp))
+        self._pm("heads_fwd", 48.0)
         _lib.check(lib.fv_composite_fwd(self.rgbs.data_ptr(), self.delta.data_ptr(), self.xs[:, 3:].data_ptr(), 4, 1,
                                         self.R, self.N, self.bg, eps, 0.0, self.rgb.data_ptr(), self.alpha.data_ptr(),
                                         self.trans.data_ptr(), sp), "fv_composite_fwd")
+        self._pm("composite_fwd", 28.0)
         if self.lam_perc == 0.0 and self.lam_mse == 1.0:   # config 3: plain L2
             _lib.check(lib.fv_mse_loss(self.rgb.data_ptr(), self.target.data_ptr(), self.pix.data_ptr(), self.R,
                                        self.loss.data_ptr(), self.drgb.data_ptr(), sp), "fv_mse_loss")
@@ -263,6 +297,7 @@ class Trainer:
             _lib.check(lib.fv_patch_loss(self.rgb.data_ptr(), self.target.data_ptr(), self.pix.data_ptr(),
                                          self.n_patches, self.patch, self.lam_mse, self.lam_perc,
                                          self.loss.data_ptr(), self.drgb.data_ptr(), sp), "fv_patch_loss")
+        self._pm("loss", 0.0, total=self.R * 40.0)
         return self.loss[0]
 
     def backward(self):
@@ -271,11 +306,14 @@ class Trainer:
         eps = self.st.eps_w
         self.grad.zero_()
         self.dvol.zero_()
+        self._pm("zero grads", 0.0, total=4.0 * (self.grad.numel() + self.dvol.numel()))
         _lib.check(lib.fv_composite_bwd(self.rgbs.data_ptr(), self.delta.data_ptr(), self.xs[:, 3:].data_ptr(), 4, 1,
                                         self.trans.data_ptr(), self.R, self.N, self.bg, eps, self.drgb.data_ptr(),
                                         None, self.d_rgbs.data_ptr(), sp), "fv_composite_bwd")
+        self._pm("composite_bwd", 44.0)
         _lib.check(lib.fv_heads_bwd(self.xs.data_ptr(), self.hd.data_ptr(), self.d_rgbs.data_ptr(), S, eps,
                                     self.dh.data_ptr(), sp))
+        self._pm("heads_bwd", 64.0)
         h = nets.hash_struct()
         # radiance MLP (tcgen05 dz-form: each dx epilogue applies the previous layer's ReLU bits)
         if self.tc:
@@ -288,6 +326,7 @@ class Trainer:
             self._lin_bwd(self.feat, V["rad_w0"], self.r[0], self.g64[1], self.dfeat, G["rad_w0"], G["rad_b0"], 32, 64, 1, sp)
         _lib.check(lib.fv_hash_bwd(C.byref(h), self.xf.data_ptr(), S, self.dfeat.data_ptr(),
                                    G["table"].data_ptr(), self.dxf.data_ptr(), sp), "fv_hash_bwd")
+        self._pm("hash_bwd", 2188.0)     # 128 B dfeat + 12 B pos + 256 fp32 atomics x 8 B RMW
         # table + radiance-MLP gradients are final: their all-reduce overlaps the rest
         self.buckets.launch(0, self.nets.segments[0][0])
         # residual MLP; when the stage is off x_final = x_skel and the gradient goes straight to the warp
@@ -311,6 +350,7 @@ class Trainer:
             self.dxs.copy_(self.dxf)
             _lib.check(lib.fv_posenc_bwd(self.xs.data_ptr(), S, eps, PE_BANDS, self.pe_w, self.dpe.data_ptr(),
                                          self.pe_ld, self.dxs.data_ptr(), sp))
+            self._pm("posenc_bwd (+dW0 pose rows, dx copy)", 16.0 + 4.0 * self.pe_ld + 24.0)
         w = nets.warp_struct()
         if self.pose_refiner is not None:
             self.dg.zero_()
@@ -319,9 +359,11 @@ class Trainer:
         else:
             _lib.check(lib.fv_warp_bwd(C.byref(w), eps, self.x.data_ptr(), S, self.dxs.data_ptr(),
                                        self.dvol.data_ptr(), sp), "fv_warp_bwd")
+        self._pm("warp_bwd", 24.0 + nets.n_bones * ((16.0 if nets.half else 32.0) + 8 * 8.0))
         k1, g = self.dvol.shape[0], self.dvol.shape[1]
         _lib.check(lib.fv_softmax0_bwd(nets.vol.data_ptr(), self.dvol.data_ptr(), k1, g ** 3,
                                        G["vol_logits"].data_ptr(), sp))
+        self._pm("softmax0_bwd", 0.0, total=12.0 * self.dvol.numel())
         if self.pose_refiner is not None:     # dL/dG_i and the pose input -> refiner parameters
             refined, g_r, g_t = self._refined
             dg = self.dg.double().cpu()
@@ -358,7 +400,9 @@ class Trainer:
                                          0.9, 0.99, 1e-8, half.data_ptr() if half is not None else None, 0,
                                          self.table_elems if half is not None else 0, self.flag.data_ptr(),
                                          _lib.stream_ptr()), "fv_adam_step")
+        self._pm("adam", 0.0, total=28.0 * nets.n_params + 2.0 * self.table_elems)
         nets.refresh_after_step()
+        self._pm("refresh (softmax, W^c pack, tc pack, pose fold)", 0.0, total=0.0)
         if self.weight_net is not None or self.pose_refiner is not None:
             # the torch-side optimizers follow the fused step's verdict: no update on a
             # non-finite gradient (ad:898-902); one host read, only on these optional paths
