@@ -167,16 +167,18 @@ class FreeviewModel:
         _lib.check(self.lib.fv_warp_pack(self.vol.data_ptr(), self.n_bones + 1, C.byref(w),
                                          self.vol_packed.data_ptr(), st), "fv_warp_pack")
 
+    PIN_SLOTS = 4     # frames the host may run ahead of the device before a slot is reused
+
     def _upload_pose(self, g_packed: np.ndarray, pose_vec: np.ndarray, stream=None) -> None:
-        """G_i and the pose vector -> device through a 2-slot pinned staging ring with
-        asynchronous copies: the host computes the next frame's motion bases while the GPU
-        still renders the current one (a pageable copy would wait for it)."""
+        """G_i and the pose vector -> device through a pinned staging ring (PIN_SLOTS slots)
+        with asynchronous copies: the host computes the next frames' motion bases while the
+        GPU still renders the current one (a pageable copy would wait for it)."""
         if self._pin is None:
             self._pin = [torch.empty(self.g.numel() + self.pose_dev.numel(), dtype=torch.float32,
-                                     pin_memory=True) for _ in range(2)]
-            self._pin_ev = [None, None]
+                                     pin_memory=True) for _ in range(self.PIN_SLOTS)]
+            self._pin_ev = [None] * self.PIN_SLOTS
         k = self._pin_slot
-        self._pin_slot ^= 1
+        self._pin_slot = (k + 1) % self.PIN_SLOTS
         if self._pin_ev[k] is not None:
             self._pin_ev[k].synchronize()          # the copy that last used this slot is done
         buf = self._pin[k]

@@ -262,6 +262,7 @@ class Trainer:
             self._wlogits = self.weight_net()
             nets.views["vol_logits"].copy_(self._wlogits.detach())
             nets._softmax_pack(sp)
+        self._pm("patch ids H2D (+ host latency)", 0.0, total=4.0 * self.R)
         m, cs, w = march_struct(self.st, self.pix, None), camera_struct(self.cam), nets.warp_struct()
         h, eps = nets.hash_struct(), self.st.eps_w
         _lib.check(lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), self.R, self.xs.data_ptr(),

@@ -270,3 +270,21 @@ def test_adam_step_matches_reference_and_refuses_nonfinite():
     assert s0.t == 3 and torch.equal(p0, before[0]) and torch.equal(s0.m[0], before[1])
     with pytest.raises(DimensionError):
         autodiff.adam_step([p0], [bad[:3]], s0, lr=5e-4)
+
+
+@pytest.mark.parametrize("n_in,n_out,depth,batch", [(1, 1, 1, 1), (64, 64, 4, 65536), (3, 4, 7, 1001),
+                                                    (39, 3, 2, 129), (32, 4, 2, 127)])
+def test_fused_forward_shapes(n_in, n_out, depth, batch):
+    """fv_fused_mlp_fwd over the FusedMlp shape range (in/out 1..64, 2..8 layers, ragged
+    batches around the 128-row chunk): equal to the layer-by-layer naive_forward to fp32
+    rounding and bitwise chunk-invariant."""
+    mlp = fused.FusedMlp.random(n_in, n_out, depth=depth, seed=n_in + depth)
+    x = torch.randn((batch, n_in), device=DEV)
+    y = fused.fused_forward(mlp, x)
+    ref = fused.naive_forward(mlp, x)
+    assert y.shape == (batch, n_out)
+    scale = float(ref.abs().max()) + 1e-6
+    assert float((y - ref).abs().max()) <= 2e-5 * scale
+    if batch > 3:
+        part = fused.fused_forward(mlp, x[1:batch - 1].clone())
+        assert torch.equal(part, y[1:batch - 1])
