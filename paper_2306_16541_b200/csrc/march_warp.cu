@@ -128,6 +128,11 @@ __device__ __forceinline__ bool occ_test_nb(const uint32_t* occ, const float* bm
 // and not kept: a persistent grid with the bone table staged once per CTA, 2.12 -> 2.40 ms;
 // warp 0 computing the 32 rays' setup for the tile's 4 depth warps through shared memory,
 // +0.15 ms -- the barrier costs more than the redundant ray setup.)
+#ifndef FV_MARCH_DPT
+#define FV_MARCH_DPT 8
+#endif
+constexpr int MARCH_DPT = FV_MARCH_DPT;   // consecutive depths per thread
+
 template <bool COMPACT>
 __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, fv_warp w, int64_t n_rays,
                                                     float4* __restrict__ xs_out, float* __restrict__ delta_out,
@@ -139,82 +144,104 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
   __syncthreads();
   const int N = m.n_samples, K = rd.K;
   const int64_t n_j = rd.n_live ? (int64_t)*rd.n_live : n_rays;     // rays in this round
-  const int64_t total = padded_rays(n_j) * K;
+  const int64_t n_rb = padded_rays(n_j) / RB;                         // blocks of 32 rays
+  constexpr int DPT = MARCH_DPT, TILE_DEPTHS = 4 * DPT;
+  const int64_t tiles_per_rb = (K + TILE_DEPTHS - 1) / TILE_DEPTHS;
+  const int64_t n_tiles = n_rb * tiles_per_rb;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = base + threadIdx.x;
-    // slot -> (live position j, local sample il): s / 32 = (j / 32) K + il (layout.cuh)
-    const uint64_t q = (uint64_t)s >> 5;
-    const int32_t il = (int32_t)(q % (uint64_t)K);
-    const int64_t j = (int64_t)(q / (uint64_t)K) * RB + lane;
-    const int32_t i = rd.i0 + il;
+  // tile = one block of 32 rays x 4 DPT consecutive depths, one ray per lane.  Iteration d
+  // covers the tile's depths [4 d, 4 d + 4), warp w depth 4 d + w (INTERLEAVED: the block's
+  // 128 slots of an iteration -- one compaction, contiguous in the foreground stream -- are 4
+  // consecutive depths of 32 neighbouring rays, the locality the field kernels' gathers
+  // want), or (FV_MARCH_INTERLEAVE 0) warp w takes depths [w DPT, (w + 1) DPT) and carries
+  // t_{i+1} over as t_i of its next slot.  Either way the ray setup (pixel, direction, slab,
+  // bin width) is computed once per DPT slots.
+#ifndef FV_MARCH_INTERLEAVE
+#define FV_MARCH_INTERLEAVE 1
+#endif
+  constexpr bool INTERLEAVE = FV_MARCH_INTERLEAVE;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t jb = tile / tiles_per_rb;
+    const int il0 = (int)(tile % tiles_per_rb) * TILE_DEPTHS + (INTERLEAVE ? wid : wid * DPT);
+    const int64_t j = jb * RB + lane;
     bool hit;
     const RaySetup rs = ray_setup(cam, m, rd, j, n_j, hit);
-    float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-    float delta = 0.f;
-    bool occ = false;
-    if (s < total && rs.ray >= 0) {
-      const int32_t pix = rs.pix;
-      if (hit) {
-        const float ui = m.jitter ? jitter_u(m.seed, (uint32_t)pix, i) : 0.5f;
-        const float t = sample_t(rs.t0, rs.step, i, ui);
-        if (i + 1 < N) {
-          const float un = m.jitter ? jitter_u(m.seed, (uint32_t)pix, i + 1) : 0.5f;
-          delta = __fsub_rn(sample_t(rs.t0, rs.step, i + 1, un), t);
-        } else {
-          const float u0 = m.jitter ? jitter_u(m.seed, (uint32_t)pix, 0) : 0.5f;
-          delta = __fadd_rn(__fsub_rn(rs.t1, t), __fsub_rn(sample_t(rs.t0, rs.step, 0, u0), rs.t0));
+    float t_carry = 0.f;
+    bool carry = false;
+#pragma unroll 1
+    for (int d = 0; d < DPT; ++d) {
+      const int il = il0 + (INTERLEAVE ? 4 * d : d);
+      const bool slot_ok = il < K;                                   // warp-uniform
+      const int64_t s = (jb * K + il) * RB + lane;
+      const int32_t i = rd.i0 + il;
+      float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+      float delta = 0.f;
+      bool occ = false;
+      if (slot_ok && rs.ray >= 0) {
+        const int32_t pix = rs.pix;
+        if (hit) {
+          const float t = carry ? t_carry
+                                : sample_t(rs.t0, rs.step, i, m.jitter ? jitter_u(m.seed, (uint32_t)pix, i) : 0.5f);
+          if (i + 1 < N) {
+            const float un = m.jitter ? jitter_u(m.seed, (uint32_t)pix, i + 1) : 0.5f;
+            t_carry = sample_t(rs.t0, rs.step, i + 1, un);
+            carry = !INTERLEAVE;
+            delta = __fsub_rn(t_carry, t);
+          } else {
+            const float u0 = m.jitter ? jitter_u(m.seed, (uint32_t)pix, 0) : 0.5f;
+            delta = __fadd_rn(__fsub_rn(rs.t1, t), __fsub_rn(sample_t(rs.t0, rs.step, 0, u0), rs.t0));
+          }
+          const float px = __fadd_rn(cam.center[0], __fmul_rn(t, rs.dx));
+          const float py = __fadd_rn(cam.center[1], __fmul_rn(t, rs.dy));
+          const float pz = __fadd_rn(cam.center[2], __fmul_rn(t, rs.dz));
+          if (x_out) { x_out[3 * s] = px; x_out[3 * s + 1] = py; x_out[3 * s + 2] = pz; }
+          occ = m.d_occ == nullptr || occ_test_nb(m.d_occ, m.obox_min, m.occ_scale, px, py, pz);
+          if (occ) {
+            float xsk[3];
+            const float L = warp_point<false>(w, sg, m.eps_w, px, py, pz, xsk);
+            out = make_float4(xsk[0], xsk[1], xsk[2], L);
+          }
+        } else if (x_out) {
+          x_out[3 * s] = x_out[3 * s + 1] = x_out[3 * s + 2] = 0.f;
         }
-        const float px = __fadd_rn(cam.center[0], __fmul_rn(t, rs.dx));
-        const float py = __fadd_rn(cam.center[1], __fmul_rn(t, rs.dy));
-        const float pz = __fadd_rn(cam.center[2], __fmul_rn(t, rs.dz));
-        if (x_out) { x_out[3 * s] = px; x_out[3 * s + 1] = py; x_out[3 * s + 2] = pz; }
-        occ = m.d_occ == nullptr || occ_test_nb(m.d_occ, m.obox_min, m.occ_scale, px, py, pz);
-        if (occ) {
-          float xsk[3];
-          const float L = warp_point<false>(w, sg, m.eps_w, px, py, pz, xsk);
-          out = make_float4(xsk[0], xsk[1], xsk[2], L);
-        }
-      } else if (x_out) {
+        if (i == 0 && count_out) count_out[rs.ray] = hit ? N : 0;
+      } else if (x_out && slot_ok) {
         x_out[3 * s] = x_out[3 * s + 1] = x_out[3 * s + 2] = 0.f;
       }
-      if (i == 0 && count_out) count_out[rs.ray] = hit ? N : 0;
-    } else if (x_out && s < total) {
-      x_out[3 * s] = x_out[3 * s + 1] = x_out[3 * s + 2] = 0.f;
-    }
-    if (!COMPACT) {
-      if (s < total) {
-        xs_out[s] = out;
-        delta_out[s] = delta;
+      if (!COMPACT) {
+        if (slot_ok) {
+          xs_out[s] = out;
+          delta_out[s] = delta;
+        }
+        continue;
       }
-      continue;
+      const bool fg = slot_ok && out.w > m.eps_w;
+      const uint32_t ballot = __ballot_sync(0xffffffffu, fg);
+      if (lane == 0) wcount[wid] = __popc(ballot);
+      __syncthreads();
+      if (threadIdx.x == 0) wbase = atomicAdd(cmp.count, wcount[0] + wcount[1] + wcount[2] + wcount[3]);
+      __syncthreads();
+      if (slot_ok) {
+        cmp.lik[s] = out.w;
+        delta_out[s] = delta;
+        if (cmp.flags) cmp.flags[s] = (uint8_t)((hit ? 1 : 0) | (occ ? 2 : 0) | (fg ? 4 : 0));
+      }
+      if (fg) {
+        int off = wbase;
+        for (int qq = 0; qq < wid; ++qq) off += wcount[qq];
+        off += __popc(ballot & ((1u << lane) - 1u));
+        cmp.xsc[off] = out;
+        cmp.idx[off] = (int32_t)s;
+      }
+      __syncthreads();                   // wcount / wbase are reused by the next slot
     }
-    const bool fg = s < total && out.w > m.eps_w;
-    const uint32_t ballot = __ballot_sync(0xffffffffu, fg);
-    if (lane == 0) wcount[wid] = __popc(ballot);
-    __syncthreads();
-    if (threadIdx.x == 0) wbase = atomicAdd(cmp.count, wcount[0] + wcount[1] + wcount[2] + wcount[3]);
-    __syncthreads();
-    if (s < total) {
-      cmp.lik[s] = out.w;
-      delta_out[s] = delta;
-      if (cmp.flags) cmp.flags[s] = (uint8_t)((hit ? 1 : 0) | (occ ? 2 : 0) | (fg ? 4 : 0));
-    }
-    if (fg) {
-      int off = wbase;
-      for (int qq = 0; qq < wid; ++qq) off += wcount[qq];
-      off += __popc(ballot & ((1u << lane) - 1u));
-      cmp.xsc[off] = out;
-      cmp.idx[off] = (int32_t)s;
-    }
-    __syncthreads();                     // wcount / wbase are reused by the next tile
   }
 }
 
-// Grid for k_march_warp: one 128-slot tile per block (capped at 64 waves of resident blocks;
-// the block loop covers the rest).
+// Grid for k_march_warp: one tile (32 rays x 4 MARCH_DPT depths) per block, capped at 64
+// waves of resident blocks (the block loop covers the rest).
 template <bool COMPACT>
-static unsigned march_grid(int64_t total) {
+static unsigned march_grid(int64_t n_rays, int K) {
   static int per_sm[2] = {0, 0};
   int& b = per_sm[COMPACT ? 1 : 0];
   if (b == 0) {
@@ -224,7 +251,8 @@ static unsigned march_grid(int64_t total) {
   int dev = 0, n_sm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 127) / 128, (int64_t)n_sm * b * 64));
+  const int64_t tiles = padded_rays(n_rays) / RB * ((K + 4 * MARCH_DPT - 1) / (4 * MARCH_DPT));
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)n_sm * b * 64));
 }
 
 // d x_skel -> d W^c (C,G,G,G) via dw_i = <dxs, p_i - x_skel>/L and the trilinear scatter.
@@ -482,8 +510,7 @@ extern "C" int32_t fv_march_warp(const fv_camera* cam, const fv_march* march, co
     return set_error(FV_EDIM, "fv_march_warp: bad arguments");
   if (int32_t e = check_warp(warp)) return e;
   if (n_rays == 0) return FV_OK;
-  const int64_t total = padded_rays(n_rays) * march->n_samples;
-  k_march_warp<false><<<march_grid<false>(total), 128, 0, (cudaStream_t)stream>>>(
+  k_march_warp<false><<<march_grid<false>(n_rays, march->n_samples), 128, 0, (cudaStream_t)stream>>>(
       *cam, *march, *warp, n_rays, (float4*)d_xs, d_delta, d_x, d_count, Compact{},
       MarchRound{0, march->n_samples, nullptr, nullptr});
   return check_launch("fv_march_warp");
@@ -494,9 +521,8 @@ namespace fv {
 int32_t march_compact(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays, float* lik,
                       float* delta, float4* xsc, int32_t* idx, int32_t* count, int32_t* ray_count, cudaStream_t st,
                       uint8_t* flags) {
-  const int64_t total = padded_rays(n_rays) * march->n_samples;
   cudaMemsetAsync(count, 0, sizeof(int32_t), st);
-  k_march_warp<true><<<march_grid<true>(total), 128, 0, st>>>(*cam, *march, *warp, n_rays, nullptr, delta,
+  k_march_warp<true><<<march_grid<true>(n_rays, march->n_samples), 128, 0, st>>>(*cam, *march, *warp, n_rays, nullptr, delta,
                                                                       nullptr, ray_count,
                                                                       Compact{lik, xsc, idx, count, flags},
                                                                       MarchRound{0, march->n_samples, nullptr, nullptr});
@@ -508,11 +534,11 @@ int32_t march_compact(const fv_camera* cam, const fv_march* march, const fv_warp
 int32_t march_round(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays, int32_t i0,
                     int32_t K, const int32_t* live, const int32_t* n_live, float* lik, float* delta, float4* xsc,
                     int32_t* idx, int32_t* count, int32_t* ray_count, cudaStream_t st) {
-  const int64_t total = padded_rays(n_rays) * K;
   cudaMemsetAsync(count, 0, sizeof(int32_t), st);
-  k_march_warp<true><<<march_grid<true>(total), 128, 0, st>>>(*cam, *march, *warp, n_rays, nullptr, delta, nullptr,
-                                                       ray_count, Compact{lik, xsc, idx, count, nullptr},
-                                                       MarchRound{i0, K, live, n_live});
+  k_march_warp<true><<<march_grid<true>(n_rays, K), 128, 0, st>>>(*cam, *march, *warp, n_rays, nullptr, delta,
+                                                                  nullptr, ray_count,
+                                                                  Compact{lik, xsc, idx, count, nullptr},
+                                                                  MarchRound{i0, K, live, n_live});
   return check_launch("march_round");
 }
 }  // namespace fv
