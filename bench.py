@@ -350,13 +350,15 @@ def run_ours(args, rank, world, local_rank):
     dominant = max(roofs, key=lambda k: stages.get(k, 0.0))
     roof = dict(roofs[dominant])
 
-    occ_var = occupancy_variants(nets, rnd, cam, st, dev) if rank == 0 and not args.no_occ_variants else None
-    trained = subject_variants(args, dev) if rank == 0 and not args.no_trained else None
+    # single-GPU extras (the N > 1 lines of a scaling run carry the headline, training and config 5)
+    solo = world == 1
+    occ_var = occupancy_variants(nets, rnd, cam, st, dev) if solo and not args.no_occ_variants else None
+    trained = subject_variants(args, dev) if solo and not args.no_trained else None
     train = None if args.no_train else train_throughput(args, rank, world, dev)
     multi = None if args.no_scene else scene_throughput(args, rank, world, dev)
 
     cpu = None
-    if rank == 0 and not args.skip_cpu_baseline:
+    if solo and not args.skip_cpu_baseline:      # cpu_baseline: rank 0 at N = 1 only
         base = CpuBaseline(name, args.cpu_tiles)
         v = float(np.median([base.rays_per_s() for _ in range(3)]))
         base.close()
