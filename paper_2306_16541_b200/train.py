@@ -197,7 +197,8 @@ class Trainer:
     def profile_step(self, step: int = 0):
         """One full step with per-op events: [(op, ms, algorithmic bytes, GB/s)]."""
         self.prof = []
-        self._pm("start", 0.0)
+        torch.cuda._sleep(8_000_000)      # ~4 ms device spin: the host enqueues the step ahead of
+        self._pm("start", 0.0)            # the device, so the marks time kernels, not launches
         self.step(step)
         torch.cuda.synchronize()
         marks, self.prof = self.prof, None
@@ -262,7 +263,7 @@ class Trainer:
             self._wlogits = self.weight_net()
             nets.views["vol_logits"].copy_(self._wlogits.detach())
             nets._softmax_pack(sp)
-        self._pm("patch ids H2D (+ host latency)", 0.0, total=4.0 * self.R)
+        self._pm("patch ids H2D", 0.0, total=4.0 * self.R)
         m, cs, w = march_struct(self.st, self.pix, None), camera_struct(self.cam), nets.warp_struct()
         h, eps = nets.hash_struct(), self.st.eps_w
         _lib.check(lib.fv_march_warp(C.byref(cs), C.byref(m), C.byref(w), self.R, self.xs.data_ptr(),
