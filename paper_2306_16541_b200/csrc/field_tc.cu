@@ -134,6 +134,13 @@ __device__ __forceinline__ void tc_prologue_sync() {
   tc::fence_after();
 }
 
+#ifndef FV_OFF_PROF
+#define FV_OFF_PROF 0
+#endif
+#if FV_OFF_PROF
+__device__ long long g_off_prof[2 * 32 * 10];
+#endif
+
 // ---- k_offset_tc: xs (x_skel, L) -> out (x_final, L) ------------------------------------
 // Activations never touch shared memory: each layer's A operand lives in TMEM next to its
 // accumulator (tcgen05.mma with A from TMEM), so the MMAs read only the weights from smem
@@ -265,30 +272,51 @@ __global__ void __launch_bounds__(TEAMS * 256, 1)
   // posenc of one sample -> this thread's 12 A-operand words (columns [12*half, +12) of the
   // 24 holding 39 values, zero pad, ones at k = 46/47): sin/cos(pi x) once per coordinate,
   // higher bands by double-angle recurrences (error 2^k ulp << fp16 resolution)
+  // posenc of one sample -> this thread's 12 A-operand words: the 48 fp16 columns hold the 39
+  // values, zero pad and ones at k = 46/47; warpgroup half 0 owns columns [0, 24) (raw xyz,
+  // bands 0-2, band 3 sine), half 1 columns [24, 48) (band 3 cosine, bands 4-5, pad, ones),
+  // so each half computes only its own 24 values: sin/cos(pi 2^k0 x) once per coordinate
+  // (k0 = 0 or 3), the other bands by double-angle recurrences (error 2^k ulp << fp16).
   auto posenc12 = [&](const float4 v, int64_t s, uint32_t (&w)[12]) {
     const bool fg = s < n && v.w > eps_w;
     const float xx[3] = {fg ? v.x : 0.f, fg ? v.y : 0.f, fg ? v.z : 0.f};
-    __half pe[48];
-    pe[0] = __float2half_rn(xx[0]); pe[1] = __float2half_rn(xx[1]); pe[2] = __float2half_rn(xx[2]);
+    __half pe[24];
+    if (half == 0) {
+      pe[0] = __float2half_rn(xx[0]); pe[1] = __float2half_rn(xx[1]); pe[2] = __float2half_rn(xx[2]);
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      float sv, cv;
-      sincospif(xx[j], &sv, &cv);
+      for (int j = 0; j < 3; ++j) {
+        float sv, cv;
+        sincospif(xx[j], &sv, &cv);
 #pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        const float wk = k < f.pe_bands ? f.pe_w[k] : 0.f;
-        pe[3 + 6 * k + j] = __float2half_rn(wk * sv);
-        pe[3 + 6 * k + 3 + j] = __float2half_rn(wk * cv);
-        const float s2 = 2.f * sv * cv, c2 = (cv - sv) * (cv + sv);
-        sv = s2; cv = c2;
+        for (int k = 0; k < 4; ++k) {
+          const float wk = k < f.pe_bands ? f.pe_w[k] : 0.f;
+          pe[3 + 6 * k + j] = __float2half_rn(wk * sv);                 // k = 3: column 21 + j
+          if (k < 3) pe[6 + 6 * k + j] = __float2half_rn(wk * cv);
+          const float s2 = 2.f * sv * cv, c2 = (cv - sv) * (cv + sv);
+          sv = s2; cv = c2;
+        }
       }
-    }
+    } else {
 #pragma unroll
-    for (int j = 39; j < 46; ++j) pe[j] = __float2half_rn(0.f);
-    pe[46] = pe[47] = __float2half_rn(1.f);
+      for (int j = 0; j < 3; ++j) {
+        float sv, cv;
+        sincospif(8.f * xx[j], &sv, &cv);                                // band 3: 2^3 pi x
+#pragma unroll
+        for (int k = 3; k < 6; ++k) {
+          const float wk = k < f.pe_bands ? f.pe_w[k] : 0.f;
+          if (k > 3) pe[3 + 6 * k + j - 24] = __float2half_rn(wk * sv);
+          pe[6 + 6 * k + j - 24] = __float2half_rn(wk * cv);             // k = 3: column 24 + j
+          const float s2 = 2.f * sv * cv, c2 = (cv - sv) * (cv + sv);
+          sv = s2; cv = c2;
+        }
+      }
+#pragma unroll
+      for (int j = 39 - 24; j < 46 - 24; ++j) pe[j] = __float2half_rn(0.f);
+      pe[46 - 24] = pe[47 - 24] = __float2half_rn(1.f);
+    }
     const uint32_t* pw = reinterpret_cast<const uint32_t*>(pe);
 #pragma unroll
-    for (int i = 0; i < 12; ++i) w[i] = half ? pw[12 + i] : pw[i];
+    for (int i = 0; i < 12; ++i) w[i] = pw[i];
   };
   // Software pipeline per team:
   //  * the input is loaded two tiles ahead and the next tile's posenc is computed (and
@@ -328,9 +356,19 @@ __global__ void __launch_bounds__(TEAMS * 256, 1)
       if (*p < FV_OFF_LEAD) *p = *p + 1;
     }
   };
+#if FV_OFF_PROF
+  // timeline probe (alt builds only): CTA 0, thread 0 of each team records clock64 at 10
+  // points per tile for its first 32 tiles -> g_off_prof[team][tile][10]
+  int ptile = 0;
+  const bool prec = blockIdx.x == 0 && tt == 0;
+  auto P = [&](int k) { if (prec && ptile < 32) g_off_prof[(team * 32 + ptile) * 10 + k] = clock64(); };
+#else
+  auto P = [&](int) {};
+#endif
   for (; tile < ntiles; tile += tstep) {
     const int64_t s = tile * 128 + row;
     const float4 v = vcur;
+    P(0);
     // [layer 4 of the previous tile] + layer 0 of this tile, one commit
     layer_issue_ts(bar, phase, tt, team, [&] {
       // De-phase the two teams: team 1 starts once team 0 has FV_OFF_LEAD batches done, so
@@ -348,26 +386,52 @@ __global__ void __launch_bounds__(TEAMS * 256, 1)
         tc::mma_f16_ts(tcol, tcol + OF_TPE + k * 8, tc::make_desc(b0 + k * 2 * 128 * 16, 128 * 16, 128),
                        tc::idesc_f16(128, 128), k > 0 ? 1u : 0u);
     });
+    P(1);
     lead();
-    if (sprev >= 0 && half == 0) emit(vprev, sprev);
+    P(2);
     epi_relu64_ts<true>(dsrc, adst);
-    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF1, bar, phase, tt, team, [&] {
-      const int64_t s1 = s + tstep * 128, s2 = s1 + tstep * 128;
+    P(3);
+    // Work hidden under the MMAs of layers 1-3 (which write D, not D4 or the posenc block):
+    // the next tile's posenc (each warpgroup half computes its own 24 columns) and input,
+    // and the previous tile's x_final (FV_OFF_SCHED picks the windows).  The next B0
+    // batch's tmem_st_wait + team barrier orders the posenc stores before its layer-0 MMAs.
+#ifndef FV_OFF_SCHED
+#define FV_OFF_SCHED 5
+#endif
+    const int64_t s1 = s + tstep * 128, s2 = s1 + tstep * 128;
+    const auto posenc_next = [&] {
       uint32_t pw[12];
       posenc12(vnext, s1, pw);
       tc::tmem_st8(pe_dst, pw);
       tc::tmem_st4(pe_dst + 8, pw + 8);
-      vcur = vnext;
-      vnext = s2 < n ? xs[s2] : zero4;
-    });
+    };
+    constexpr int SCHED = FV_OFF_SCHED;
+    // window of: posenc half 0, posenc half 1, input advance, emit
+    constexpr int W_PE0 = SCHED == 4 ? 2 : 1, W_PE1 = 1, W_IN = SCHED == 4 ? 2 : 1, W_EMIT = SCHED == 2 ? 2 : 3;
+    const auto window = [&](int wdx) {
+      if (wdx == W_PE0 && half == 0) posenc_next();
+      if (wdx == W_PE1 && half == 1) posenc_next();
+      if (wdx == W_IN) { vcur = vnext; vnext = s2 < n ? xs[s2] : zero4; }
+      if (wdx == W_EMIT && sprev >= 0 && half == 0) emit(vprev, sprev);
+    };
+    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF1, bar, phase, tt, team, [&] { window(1); });
+    P(4);
     lead();
     epi_relu64_ts<true>(dsrc, adst);
-    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF2, bar, phase, tt, team);
+    P(5);
+    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF2, bar, phase, tt, team, [&] { window(2); });
+    P(6);
     lead();
     epi_relu64_ts<true>(dsrc, adst);
-    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF3, bar, phase, tt, team);
+    P(7);
+    layer_mma_ts<OF_KH, 128, 256>(tcol, smem + PK_OFF3, bar, phase, tt, team, [&] { window(3); });
+    P(8);
     lead();
     epi_relu64_ts<true>(dsrc, adst);
+    P(9);
+#if FV_OFF_PROF
+    ++ptile;
+#endif
     const bool fg = s < n && v.w > eps_w;
     vprev = fg ? v : make_float4(0.f, 0.f, 0.f, v.w);
     sprev = s;
@@ -670,6 +734,13 @@ extern "C" int32_t fv_hash_index_paired(const fv_hash* hash, const float* d_x, i
   k_hash_index_paired<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*hash, d_x, n, d_index, d_feat);
   return check_launch("fv_hash_index_paired");
 }
+
+#if FV_OFF_PROF
+// alt builds only (tools/prof_offset.py): the timeline probe of k_offset_tc
+extern "C" int32_t fv_debug_offset_prof(long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, g_off_prof, sizeof(g_off_prof)) == cudaSuccess ? FV_OK : FV_ELAUNCH;
+}
+#endif
 
 extern "C" size_t fv_field_pack_bytes(void) { return PK_BYTES; }
 
