@@ -131,6 +131,9 @@ __device__ __forceinline__ bool occ_test_nb(const uint32_t* occ, const float* bm
 #ifndef FV_MARCH_DPT
 #define FV_MARCH_DPT 8
 #endif
+#ifndef FV_MARCH_STASH
+#define FV_MARCH_STASH 1
+#endif
 constexpr int MARCH_DPT = FV_MARCH_DPT;   // consecutive depths per thread
 
 template <bool COMPACT>
@@ -140,11 +143,21 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
                                                     Compact cmp, MarchRound rd) {
   __shared__ __align__(16) float sg[FV_MAX_BONES * 12];
   __shared__ int32_t wcount[4], wbase;
+#if FV_MARCH_STASH
+  // the tile's foreground samples, staged so the whole tile (32 rays x 4 DPT consecutive
+  // depths) lands contiguously in the compacted stream with one global atomic
+  __shared__ float4 stash_x[COMPACT ? 128 * MARCH_DPT : 1];
+  __shared__ int32_t stash_i[COMPACT ? 128 * MARCH_DPT : 1];
+  __shared__ int32_t scount;
+#endif
   fill_bones_x2(sg, w.d_g, w.n_bones);
   __syncthreads();
   const int N = m.n_samples, K = rd.K;
   const int64_t n_j = rd.n_live ? (int64_t)*rd.n_live : n_rays;     // rays in this round
   const int64_t n_rb = padded_rays(n_j) / RB;                         // blocks of 32 rays
+#ifndef FV_MARCH_INTERLEAVE
+#define FV_MARCH_INTERLEAVE 1
+#endif
   constexpr int DPT = MARCH_DPT, TILE_DEPTHS = 4 * DPT;
   const int64_t tiles_per_rb = (K + TILE_DEPTHS - 1) / TILE_DEPTHS;
   const int64_t n_tiles = n_rb * tiles_per_rb;
@@ -155,10 +168,12 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
   // consecutive depths of 32 neighbouring rays, the locality the field kernels' gathers
   // want), or (FV_MARCH_INTERLEAVE 0) warp w takes depths [w DPT, (w + 1) DPT) and carries
   // t_{i+1} over as t_i of its next slot.  Either way the ray setup (pixel, direction, slab,
-  // bin width) is computed once per DPT slots.
-#ifndef FV_MARCH_INTERLEAVE
-#define FV_MARCH_INTERLEAVE 1
-#endif
+  // bin width) is computed once per DPT slots.  (Measured and not kept: the block's 4 warps
+  // on 4 neighbouring ray blocks at the same depths -- k_radiance_tc 4.58 -> 4.71 ms: depth
+  // neighbours share more hash cells than ray neighbours.)  With FV_MARCH_STASH the tile's
+  // foreground samples are staged in shared memory and appended to the compacted stream with
+  // ONE atomic, so the whole tile (32 rays x 32 consecutive depths) is contiguous there:
+  // fewer barriers, and consecutive radiance tiles (on one SM's warpgroups) share lines.
   constexpr bool INTERLEAVE = FV_MARCH_INTERLEAVE;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t jb = tile / tiles_per_rb;
@@ -168,6 +183,10 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
     const RaySetup rs = ray_setup(cam, m, rd, j, n_j, hit);
     float t_carry = 0.f;
     bool carry = false;
+#if FV_MARCH_STASH
+    if (COMPACT && threadIdx.x == 0) scount = 0;
+    if (COMPACT) __syncthreads();
+#endif
 #pragma unroll 1
     for (int d = 0; d < DPT; ++d) {
       const int il = il0 + (INTERLEAVE ? 4 * d : d);
@@ -217,6 +236,24 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
       }
       const bool fg = slot_ok && out.w > m.eps_w;
       const uint32_t ballot = __ballot_sync(0xffffffffu, fg);
+#if FV_MARCH_STASH
+      {
+        int base = 0;
+        if (lane == 0 && ballot) base = atomicAdd(&scount, __popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (fg) {
+          const int k = base + __popc(ballot & ((1u << lane) - 1u));
+          stash_x[k] = out;
+          stash_i[k] = (int32_t)s;
+        }
+        if (slot_ok) {
+          cmp.lik[s] = out.w;
+          delta_out[s] = delta;
+          if (cmp.flags) cmp.flags[s] = (uint8_t)((hit ? 1 : 0) | (occ ? 2 : 0) | (fg ? 4 : 0));
+        }
+        continue;
+      }
+#endif
       if (lane == 0) wcount[wid] = __popc(ballot);
       __syncthreads();
       if (threadIdx.x == 0) wbase = atomicAdd(cmp.count, wcount[0] + wcount[1] + wcount[2] + wcount[3]);
@@ -235,6 +272,18 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
       }
       __syncthreads();                   // wcount / wbase are reused by the next slot
     }
+#if FV_MARCH_STASH
+    if (COMPACT) {
+      __syncthreads();
+      if (threadIdx.x == 0) wbase = scount ? atomicAdd(cmp.count, scount) : 0;
+      __syncthreads();
+      for (int k = threadIdx.x; k < scount; k += blockDim.x) {
+        cmp.xsc[wbase + k] = stash_x[k];
+        cmp.idx[wbase + k] = stash_i[k];
+      }
+      __syncthreads();                   // the stash is refilled by the next tile
+    }
+#endif
   }
 }
 
