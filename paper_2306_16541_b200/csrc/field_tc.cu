@@ -142,6 +142,11 @@ __device__ long long g_off_prof[2 * 32 * 10];
 #endif
 
 // ---- k_offset_tc: xs (x_skel, L) -> out (x_final, L) ------------------------------------
+// (Measured in round 2 and not kept: 16 worker warps + 1 MMA-issuer warp
+// serving two tile slots through mbarriers, 2.91 -> 4.22 ms -- the issuing thread blocks
+// ~850 cycles per 9-MMA batch and the two slots then serialise; the hidden-layer bias added
+// in the epilogue instead of the K = 144 bias group, 2.91 -> 3.22 ms -- 3 fewer MMAs per
+// tile, but the longer epilogue is on each team's critical chain.)
 // Activations never touch shared memory: each layer's A operand lives in TMEM next to its
 // accumulator (tcgen05.mma with A from TMEM), so the MMAs read only the weights from smem
 // (64 of the SM's 128 B/cycle) and the epilogue is tcgen05.ld -> ReLU+fp16 cvt ->
