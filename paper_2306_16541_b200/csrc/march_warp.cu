@@ -137,7 +137,10 @@ __device__ __forceinline__ bool occ_test_nb(const uint32_t* occ, const float* bm
 constexpr int MARCH_DPT = FV_MARCH_DPT;   // consecutive depths per thread
 
 template <bool COMPACT>
-__global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, fv_warp w, int64_t n_rays,
+#ifndef FV_MARCH_MINB
+#define FV_MARCH_MINB 8   // <= 64 registers: 8 blocks of 4 warps per SM
+#endif
+__global__ void __launch_bounds__(128, FV_MARCH_MINB) k_march_warp(fv_camera cam, fv_march m, fv_warp w, int64_t n_rays,
                                                     float4* __restrict__ xs_out, float* __restrict__ delta_out,
                                                     float* __restrict__ x_out, int32_t* __restrict__ count_out,
                                                     Compact cmp, MarchRound rd) {
@@ -217,7 +220,8 @@ __global__ void __launch_bounds__(128) k_march_warp(fv_camera cam, fv_march m, f
           occ = m.d_occ == nullptr || occ_test_nb(m.d_occ, m.obox_min, m.occ_scale, px, py, pz);
           if (occ) {
             float xsk[3];
-            const float L = warp_point<false>(w, sg, m.eps_w, px, py, pz, xsk);
+            const float L = w.vol_half ? warp_point<false, 1>(w, sg, m.eps_w, px, py, pz, xsk)
+                                       : warp_point<false, 0>(w, sg, m.eps_w, px, py, pz, xsk);
             out = make_float4(xsk[0], xsk[1], xsk[2], L);
           }
         } else if (x_out) {
