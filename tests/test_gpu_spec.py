@@ -86,6 +86,49 @@ def test_warp_single_bone_exact_far_background_and_normalisation(cfg):
     assert np.array_equal(xs.cpu().numpy()[interior], p[interior])
 
 
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_warp_grid_boundaries_bitexact(cfg):
+    """The grid-coordinate edge cases of ad:746-753 (inside iff 0 <= u <= G+1, floor clamped
+    to [0, G]) on the kernel's bit-pattern inside test and round-down floor: runs of
+    consecutive float32 points across u = 0, 1, G, G+1 on each axis (identity bones, so the
+    bone point is x itself), plus NaN / inf coordinates, bit-exact against the oracle."""
+    sc = make(cfg)
+    nets = FreeviewModel(sc)
+    k = nets.n_bones
+    eye, zero = np.broadcast_to(np.eye(3, dtype=np.float32), (k, 3, 3)).copy(), np.zeros((k, 3), np.float32)
+    nets.set_pose_bases(eye, zero, np.zeros(3 * k))
+    osc = oracle_scene(sc, nets=nets)
+    g = nets.vol_res
+    wmin = np.asarray(osc["wbox_min"], np.float32)
+    scale = ((np.float32(g) - np.float32(1.0)) / (np.asarray(osc["wbox_max"], np.float32) - wmin)).astype(np.float32)
+    pts = []
+    for ax in range(3):
+        for u_edge in (0.0, 1.0, float(g), float(g + 1)):
+            xb = np.float32(wmin[ax] + (u_edge - 1.0) / scale[ax])
+            run = [xb]
+            for _ in range(40):
+                run.append(np.nextafter(run[-1], np.float32(np.inf), dtype=np.float32))
+                run.insert(0, np.nextafter(run[0], np.float32(-np.inf), dtype=np.float32))
+            p = np.zeros((len(run), 3), np.float32)
+            p[:, ax] = run
+            p[:, (ax + 1) % 3] = 0.1
+            p[:, (ax + 2) % 3] = -0.2
+            pts.append(p)
+    odd = np.array([[np.nan, 0, 0], [0, np.inf, 0], [0, 0, -np.inf], [np.inf, np.inf, np.inf]], np.float32)
+    x = np.concatenate(pts)
+    xs, lik, fg = skeleton_warp(nets, torch.from_numpy(x).to(DEV))
+    wr = owarp.skeleton_warp(x, eye, zero, osc["vol"], osc["wbox_min"], osc["wbox_max"], 1e-4, np.float32)
+    assert np.array_equal(lik.cpu().numpy(), wr["L"])
+    assert np.array_equal(fg.cpu().numpy(), wr["fg"])
+    m = wr["fg"]
+    assert 0.2 < m.mean() < 1.0
+    assert np.array_equal(xs.cpu().numpy()[m], wr["x_skel"][m])
+    # non-finite coordinates: every bone outside (NaN fails both comparisons of ad:746-753),
+    # the clamped cell keeps the gather in bounds (the oracle's integer cast is undefined there)
+    _, lk, fgo = skeleton_warp(nets, torch.from_numpy(odd).to(DEV))
+    assert torch.all(lk == 0) and not bool(fgo.any())
+
+
 def test_posenc_known_answers():
     pe = posenc(torch.zeros((1, 3), device=DEV), 6, 6.0).cpu().numpy()[0]
     assert np.all(pe[:3] == 0)
