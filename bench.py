@@ -412,6 +412,17 @@ KERNEL_UNITS = {
 }
 
 
+# what ncu says limits each kernel (profiles/r02_*_ncu.txt); the "bound" above is the
+# roofline the contract grades against, this is the measured limiter behind the fraction
+LIMITERS = {
+    "march_warp": "instruction issue (ncu: 83% issue-active, IPC ~3.3; the W^c gathers are L1/L2 hits, DRAM ~5% busy, "
+                  "so the HBM fraction of the algorithmic bytes can exceed 1)",
+    "offset": "tensor pipe (~94-cycle M128 N128 K16 fp16 MMA; ~80% pipe occupancy counting the padded K)",
+    "radiance": "L1 miss-request interface to L2 (l1tex__m_l1tex2xbar_req_cycles_active ~90%; table L2-resident)",
+    "composite": "HBM streaming",
+}
+
+
 def _peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     return json.load(open(path)) if os.path.exists(path) else {"hbm_gbs": 6650.0, "bf16_tflops": 2250.0,
@@ -448,7 +459,7 @@ def stage_rooflines(stages, cfg, n_all, n_fg):
         tr = traffic.get(kname)
         out[key] = {"kernel": kname, "bound": bound, "achieved": ach, "peak": pk, "unit": u, "frac": ach / pk,
                     "traffic": tr, "ms": stages[key], "algorithmic": f"{algo} x {n_samples} samples/launch",
-                    "peak_source": psrc}
+                    "peak_source": psrc, "limiter": LIMITERS.get(key)}
         if bound == "tensor":
             out[key]["frac_vs_sustained"] = ach / peaks.get("bf16_tflops_sustained", 1394.7)
     return out
