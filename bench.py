@@ -331,13 +331,22 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # the read-back of frame i runs on a copy stream while frame i+1 renders (the frame's
+    # buffers are handed to the copy stream with record_stream, so they are not recycled
+    # before their copy); the timed region ends only after the last frame is on the host
+    copy_stream = torch.cuda.Stream(device=dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda._sleep(4_000_000)
     e0.record(stream)
     for i in range(args.steps):
         im, al = render_image(nets, cam, pose_of(i), st)
-        host_img.copy_(im, non_blocking=True)
-        host_alpha.copy_(al, non_blocking=True)
+        copy_stream.wait_stream(stream)
+        with torch.cuda.stream(copy_stream):
+            host_img.copy_(im, non_blocking=True)
+            host_alpha.copy_(al, non_blocking=True)
+        im.record_stream(copy_stream)
+        al.record_stream(copy_stream)
+    stream.wait_stream(copy_stream)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
@@ -670,13 +679,25 @@ def scene_throughput(args, rank, world, dev):
     torch.cuda.synchronize()
     ms_frame = float(np.mean([a.elapsed_time(b) for a, b in times]))
     # e2e: host poses in, host image + alpha out (pinned) every frame
-    host = torch.empty((cam.height * cam.width, 4), dtype=torch.float32, pin_memory=True)
+    # (contiguous pinned destinations, read-back on a copy stream overlapping the next frame)
+    host_img = torch.empty((cam.height, cam.width, 3), dtype=torch.float32, pin_memory=True)
+    host_alpha = torch.empty((cam.height, cam.width), dtype=torch.float32, pin_memory=True)
+    host_frame = torch.empty((cam.height, cam.width, 4), dtype=torch.float32, pin_memory=True)
+    copy_stream = torch.cuda.Stream(device=dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
         img, alpha = render_frame()
-        host[:, :3].copy_(img.reshape(-1, 3), non_blocking=True)
-        host[:, 3].copy_(alpha.reshape(-1), non_blocking=True)
+        if world > 1:     # the gathered RGBA frame: one persistent buffer, read back in order
+            host_frame.copy_(frame, non_blocking=True)
+            continue
+        copy_stream.wait_stream(stream)
+        with torch.cuda.stream(copy_stream):
+            host_img.copy_(img, non_blocking=True)
+            host_alpha.copy_(alpha, non_blocking=True)
+        img.record_stream(copy_stream)
+        alpha.record_stream(copy_stream)
+    stream.wait_stream(copy_stream)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / steps
