@@ -309,13 +309,16 @@ int32_t fv_march_warp(const fv_camera* cam, const fv_march* march, const fv_warp
  * per sample slot (ray-block-major, R padded to 32) lik (L, 0 where skipped), delta, and
  * optional flags (uint8: 1 ray hits the box, 2 occupancy cell on or no grid, 4 L > eps_w);
  * the compacted foreground stream xsc (<= S, 4) = [x_skel, L] with its slot ids idx and its
- * length *d_n_fg (device int32); per-ray sample counts d_count (may be NULL). */
+ * length *d_n_fg (device int32); per-ray sample counts d_count (may be NULL).
+ * padded(n_rays) x n_samples must stay below 2^31 (int32 slot ids; FV_EDIM otherwise). */
 int32_t fv_march_compact(const fv_camera* cam, const fv_march* march, const fv_warp* warp, int64_t n_rays,
                          float* d_lik, float* d_delta, float* d_xsc, int32_t* d_idx, int32_t* d_n_fg,
                          int32_t* d_count, uint8_t* d_flags, void* stream);
 
 /* Full forward: rays -> rgb (3 floats) and alpha per ray (or per pixel, out_by_pixel),
- * per-ray sample counts (may be NULL).  d_work >= fv_render_workspace_bytes(). */
+ * per-ray sample counts (may be NULL).  d_work >= fv_render_workspace_bytes().
+ * padded(n_rays) x n_samples must stay below 2^31 sample slots (FV_EDIM otherwise; the
+ * Python Renderer splits larger ray sets into chunks of whole 32-ray blocks). */
 int32_t fv_render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp* warp,
                       const fv_hash* hash, const fv_field* field, int64_t n_rays,
                       void* d_work, size_t work_bytes, float* d_rgb, float* d_alpha,

@@ -1,5 +1,6 @@
 // C-ABI glue: errors, version, the fused render orchestration and the occupancy builder.
 #include <cuda_runtime.h>
+#include <climits>
 #include <cstring>
 #include "fv_common.cuh"
 #include "fv_internal.h"
@@ -188,6 +189,9 @@ static int32_t render_fwd(const fv_camera* cam, const fv_march* march, const fv_
   if (int32_t e = check_warp(warp)) return e;
   if (n_rays == 0) return FV_OK;
   const int N = march->n_samples;
+  if (padded_rays(n_rays) * (int64_t)N > (int64_t)INT32_MAX)
+    return set_error(FV_EDIM, "fv_render_fwd: n_rays x n_samples exceeds 2^31 - 1 sample slots (sample ids are "
+                              "int32): render the rays in chunks");
   const int K = round_size(march);
   const int64_t S = padded_rays(n_rays) * K;
   if (work_bytes < carve(nullptr, padded_rays(n_rays) * N, field->precision, nullptr, n_rays))

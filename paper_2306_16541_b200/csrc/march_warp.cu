@@ -1,4 +1,5 @@
 // Ray march + skeleton warp kernels (S:410-413 sampling, S:327-336 warp; ad:728-773).
+#include <climits>
 #include <cuda_runtime.h>
 #include "fv_common.cuh"
 #include "layout.cuh"
@@ -607,6 +608,8 @@ extern "C" int32_t fv_march_compact(const fv_camera* cam, const fv_march* march,
       !d_n_fg)
     return set_error(FV_EDIM, "fv_march_compact: bad arguments");
   if (int32_t e = check_warp(warp)) return e;
+  if (padded_rays(n_rays) * (int64_t)march->n_samples > (int64_t)INT32_MAX)
+    return set_error(FV_EDIM, "fv_march_compact: n_rays x n_samples exceeds 2^31 - 1 sample slots (int32 sample ids)");
   if (n_rays == 0) return cudaMemsetAsync(d_n_fg, 0, sizeof(int32_t), (cudaStream_t)stream) == cudaSuccess
                               ? FV_OK : check_launch("fv_march_compact");
   return march_compact(cam, march, warp, n_rays, d_lik, d_delta, (float4*)d_xsc, d_idx, d_n_fg, d_count,

@@ -85,6 +85,8 @@ def march_struct(s: RenderSettings, pix: Optional[torch.Tensor], occ: Optional[t
 class Renderer:
     """Owns the reusable device workspace, pixel orders and the occupancy bitfield."""
 
+    MAX_SAMPLES_PER_LAUNCH = 1 << 28    # 2048^2 rays x 64 samples; 11.8 GB of workspace
+
     def __init__(self, device: str = "cuda"):
         self.lib = _lib.load()
         self.device = torch.device(device)
@@ -130,15 +132,23 @@ class Renderer:
             out_rgb = torch.empty((n_out, 3), dtype=torch.float32, device=self.device)
         if out_alpha is None:
             out_alpha = torch.empty(n_out, dtype=torch.float32, device=self.device)
-        m = march_struct(settings, pix, occ, by_pixel)
         cs = camera_struct(cam)
         w, h, f = nets.warp_struct(), nets.hash_struct(), nets.field_struct()
-        nb = self.lib.fv_render_workspace_bytes(n, settings.n_samples, f.precision)
-        work = self.workspace(nb)
-        _lib.check(self.lib.fv_render_fwd(C.byref(cs), C.byref(m), C.byref(w), C.byref(h), C.byref(f), n,
-                                          work.data_ptr(), nb, out_rgb.data_ptr(), out_alpha.data_ptr(),
-                                          counts.data_ptr() if counts is not None else None,
-                                          _lib.stream_ptr(stream)), "fv_render_fwd")
+        # one launch holds at most MAX_SAMPLES_PER_LAUNCH sample slots (sample ids are int32 in
+        # the C ABI, and the workspace is ~44 B per slot): larger ray sets go in chunks of
+        # whole 32-ray blocks -- jitter is keyed by pixel id, so the pixels are bitwise the same
+        per = max(32, self.MAX_SAMPLES_PER_LAUNCH // settings.n_samples // 32 * 32)
+        for r0 in range(0, max(n, 1), per):
+            r1 = min(n, r0 + per)
+            p = pix[r0:r1]
+            m = march_struct(settings, p, occ, by_pixel)
+            nb = self.lib.fv_render_workspace_bytes(r1 - r0, settings.n_samples, f.precision)
+            work = self.workspace(nb)
+            o_rgb, o_alpha = (out_rgb, out_alpha) if by_pixel else (out_rgb[r0:r1], out_alpha[r0:r1])
+            _lib.check(self.lib.fv_render_fwd(C.byref(cs), C.byref(m), C.byref(w), C.byref(h), C.byref(f), r1 - r0,
+                                              work.data_ptr(), nb, o_rgb.data_ptr(), o_alpha.data_ptr(),
+                                              counts[r0:r1].data_ptr() if counts is not None else None,
+                                              _lib.stream_ptr(stream)), "fv_render_fwd")
         return out_rgb, out_alpha
 
     def render_image(self, nets: FreeviewModel, cam: CameraModel, pose: Optional[Pose], settings: RenderSettings,

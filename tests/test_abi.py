@@ -88,3 +88,22 @@ def test_fused_mlp_random_draws_the_reference_weights():
         fused.FusedMlp([torch.zeros((32, 64)), torch.zeros((64, 65))])
     with pytest.raises(DimensionError):
         fused.FusedMlp([torch.zeros((32, 64)), torch.zeros((64, 4))], [torch.zeros(64), torch.zeros(3)])
+
+
+def test_sample_slot_limit_is_a_loud_error_without_gpu():
+    """Sample ids are int32 in the ABI: a launch whose padded(n_rays) x n_samples reaches
+    2^31 slots is refused with FV_EDIM before anything touches the device (the Python
+    Renderer splits such ray sets into chunks, tests/test_gpu_edge.py)."""
+    from paper_2306_16541_b200.errors import DimensionError
+    lib = _lib.load()
+    cam, mar, war, hsh, fld = _lib.FvCamera(), _lib.FvMarch(), _lib.FvWarp(), _lib.FvHash(), _lib.FvField()
+    war.n_bones, war.vol_res = 24, 32
+    hsh.n_levels, hsh.n_feat, hsh.log2_T, hsh.d_table = 16, 2, 19, 16   # never dereferenced
+    mar.n_samples = 128
+    n_rays = (1 << 31) // 128 + 32                                       # just past the limit
+    for fn, args in (("fv_render_fwd", (ctypes.byref(cam), ctypes.byref(mar), ctypes.byref(war), ctypes.byref(hsh),
+                                         ctypes.byref(fld), n_rays, None, 0, None, None, None, None)),
+                     ("fv_march_compact", (ctypes.byref(cam), ctypes.byref(mar), ctypes.byref(war), n_rays, 16, 16,
+                                           16, 16, 16, None, None, None))):
+        with pytest.raises(DimensionError, match="2\\^31"):
+            _lib.check(getattr(lib, fn)(*args), fn)

@@ -127,3 +127,25 @@ def test_full_size_c2_spot_parity(c2full):
         ref = opipe.render_rays(osc, cc, pix, 512, osettings(sc.cfg, seed=sc.jitter_seed, occupancy=occ), np.float32)
         assert np.abs(img[pix] - ref["rgb"]).max() < 1e-3
         assert np.abs(alpha[pix] - ref["alpha"]).max() < 1e-3
+
+
+def test_launch_chunking_is_bitwise_invisible(c2full, monkeypatch):
+    """Ray sets above Renderer.MAX_SAMPLES_PER_LAUNCH sample slots go in chunks of whole
+    32-ray blocks (the C ABI refuses >= 2^31 slots, int32 sample ids): the full 512^2 frame
+    (image-sized by-pixel outputs) and a per-ray batch with counts (sliced outputs) are
+    bitwise the single-launch result in chunks of 1184 rays (37 ray blocks)."""
+    sc, nets = c2full
+    st = RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed)
+    rnd = Renderer()
+    a_rgb, a_alpha = rnd.render_image(nets, sc.camera, None, st)
+    a_rgb, a_alpha = a_rgb.clone(), a_alpha.clone()
+    rng = np.random.default_rng(4)
+    pix = rng.choice(512 * 512, 3000, replace=False).astype(np.int32)
+    b_rgb, b_alpha, b_cnt = _render_pix(nets, sc.camera, pix, st, rnd)
+    monkeypatch.setattr(Renderer, "MAX_SAMPLES_PER_LAUNCH", 32 * 128 * 37 // 32 * 32 + 100)
+    rnd2 = Renderer()
+    c_rgb, c_alpha = rnd2.render_image(nets, sc.camera, None, st)
+    torch.cuda.synchronize()
+    assert torch.equal(c_rgb, a_rgb) and torch.equal(c_alpha, a_alpha)
+    d_rgb, d_alpha, d_cnt = _render_pix(nets, sc.camera, pix, st, rnd2)
+    assert np.array_equal(d_rgb, b_rgb) and np.array_equal(d_alpha, b_alpha) and np.array_equal(d_cnt, b_cnt)
