@@ -318,7 +318,12 @@ int32_t fv_march_compact(const fv_camera* cam, const fv_march* march, const fv_w
 /* Full forward: rays -> rgb (3 floats) and alpha per ray (or per pixel, out_by_pixel),
  * per-ray sample counts (may be NULL).  d_work >= fv_render_workspace_bytes().
  * padded(n_rays) x n_samples must stay below 2^31 sample slots (FV_EDIM otherwise; the
- * Python Renderer splits larger ray sets into chunks of whole 32-ray blocks). */
+ * Python Renderer splits larger ray sets into chunks of whole 32-ray blocks).
+ * There is no single fv_render_bwd: the training step differentiates the
+ * render by the per-op sequence of the reference Tape (ad:114-134) -- fv_composite_bwd,
+ * fv_heads_bwd, fv_linear_bwd_tc_bits (radiance MLP), fv_hash_bwd, fv_linear_bwd_tc_bits
+ * (residual MLP), fv_posenc_bwd, fv_warp_bwd[_g], fv_softmax0_bwd -- over activations its
+ * forward keeps (the render path's compacted streams are not kept); INTEGRATION.md. */
 int32_t fv_render_fwd(const fv_camera* cam, const fv_march* march, const fv_warp* warp,
                       const fv_hash* hash, const fv_field* field, int64_t n_rays,
                       void* d_work, size_t work_bytes, float* d_rgb, float* d_alpha,
