@@ -27,3 +27,14 @@ def blocked_to_ray_major(a, n_rays, n):
     b = a.reshape((rp // 32, n, 32) + tail)
     b = np.swapaxes(b, 1, 2).reshape((rp, n) + tail)
     return b[:n_rays]
+
+
+def trained_scene(scene, nets):
+    """The scene with the model's current (trained) fp32 master parameters, for the oracle."""
+    import dataclasses
+    v = {k: t.detach().cpu().numpy().copy() for k, t in nets.views.items()}
+    return dataclasses.replace(scene, table=v["table"], vol_logits=v["vol_logits"],
+                               off_w=[v[f"off_w{i}"] for i in range(len(scene.off_w))],
+                               off_b=[v[f"off_b{i}"] for i in range(len(scene.off_b))],
+                               rad_w=[v[f"rad_w{i}"] for i in range(len(scene.rad_w))],
+                               rad_b=[v[f"rad_b{i}"] for i in range(len(scene.rad_b))])
