@@ -13,7 +13,8 @@ indices bit-exact; rendered RGB/alpha and gradients within 1e-3 absolute.
   the oracle's float64 backward;
 * config 4 (pose sigma 0.3) renders at 64x64 and on 512x512 crops;
 * config 5 (4 subjects, 1024x1024, 192 samples per subject box) spot crops;
-* a trained config-3 model (300 Adam steps) rendered against the oracle on its weights.
+* a trained config-3 model (200-300 Adam steps): its render and one more step's gradients
+  against the oracle on the trained parameters.
 """
 
 import ctypes as C
@@ -182,10 +183,36 @@ def test_c3_training_step_fp16_grid_gradients_match_oracle():
     st = RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed)
     tr = Trainer(nets, sc.camera, target, mask, st, n_patches=2, patch=32, seed=11, precision="tf32")
     pix = patch_pixels(sample_patches(mask, 2, 32, 11, 0), 32, sc.cfg.width)
+    _check_step_gradients(sc, nets, tr, target, pix, oracle_scene(sc, nets=nets))
+
+
+def test_trained_model_step_gradients_match_oracle():
+    """One more training step's gradients after 200 Adam steps (trained table, MLPs and W^c
+    logits), config-3 fp16 grid at 64x64 with 2 x 16x16 patches, against the oracle's float64
+    backward on the trained master parameters -- same bars as the init-weights test above."""
+    sc = make("c3", width=64, height=64)
+    nets = FreeviewModel(sc)
+    target, mask = target_image(sc)
+    st = RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed)
+    tr = Trainer(nets, sc.camera, target, mask, st, n_patches=2, patch=16, seed=7, precision="tf32")
+    for i in range(200):
+        tr.step(i)
+    torch.cuda.synchronize()
+    pix = patch_pixels(sample_patches(mask, 2, 16, 7, 999), 16, sc.cfg.width)
+    ts = trained_scene(sc, nets)
+    osc = oracle_scene(ts, nets=nets)
+    # the training forward runs the MLPs on the fp32 master weights (3xTF32) and reads the
+    # fp16 table copy: the oracle gets the same (its scene view fp16-rounds every block of a
+    # half config, which only the render path's packed weights match)
+    osc["off_w"] = [np.asarray(w, np.float32) for w in ts.off_w]
+    osc["rad_w"] = [np.asarray(w, np.float32) for w in ts.rad_w]
+    _check_step_gradients(sc, nets, tr, target, pix, osc)
+
+
+def _check_step_gradients(sc, nets, tr, target, pix, osc):
     loss = float(tr.forward(pix).item())
     tr.backward()
     torch.cuda.synchronize()
-    osc = oracle_scene(sc, nets=nets)
     cc = ocam.camera_consts(sc.camera.intrinsics, sc.camera.world_to_camera)
     tgt = target.reshape(-1, 3)[pix]
     ost = osettings(sc.cfg, seed=sc.jitter_seed)
