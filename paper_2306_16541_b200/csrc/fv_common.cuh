@@ -92,9 +92,6 @@ __device__ __forceinline__ bool occ_test(const uint32_t* occ, const float* bmin,
 }
 
 // ---------------------------------------------------------------- skeleton warp
-#ifndef FV_WARP_V2
-#define FV_WARP_V2 1
-#endif
 #ifndef FV_WARP_UNROLL
 #define FV_WARP_UNROLL 2
 #endif
@@ -207,14 +204,12 @@ __device__ __forceinline__ float warp_point(const fv_warp& w, const float* sg, f
   const float2 one2 = make_float2(1.f, 1.f), mone2 = make_float2(-1.f, -1.f);
   const float2 X0 = make_float2(x0, x0), X1 = make_float2(x1, x1), X2 = make_float2(x2, x2);
   const int half = HALF < 0 ? w.vol_half : HALF;
-#if FV_WARP_V2
   // cell index from the bit patterns of t = u_clamped +rd 2^23 (bits = 0x4B000000 + floor):
   // idx = ((i s + fx) s + fy) s + fz with the 0x4B000000 (s^2 + s + 1) bias folded into the
   // per-bone base (uint32 wrap-around; the true index fits)
   const uint32_t s1 = (uint32_t)G + 1u, s2c = s1 * s1;
   const uint32_t bias = 0x4B000000u * (s2c + s1 + 1u);
   const uint32_t gbits = __float_as_uint(gp1);
-#endif
 #pragma unroll kWarpUnroll
   for (int i = 0; i < K; ++i) {
     const float4* g4 = reinterpret_cast<const float4*>(sg + 12 * i);   // 48-byte rows
@@ -227,7 +222,6 @@ __device__ __forceinline__ float warp_point(const fv_warp& w, const float* sg, f
     // grid position (warp_cell): u = (p - min) * scale + 1, inside iff u in [0, G+1]
     const float2 u01 = __ffma2_rn(__fadd2_rn(p01, nmin01), sc01, one2);
     const float u2 = __fmaf_rn(__fsub_rn(p2, w.wbox_min[2]), w.wscale[2], 1.0f);
-#if FV_WARP_V2
     // inside <=> 0 <= u <= G+1 on all axes <=> max of the bit patterns <= bits(G+1): u >= 0
     // has the sign bit clear (u = q s + 1 never rounds to -0) and NaN / negative patterns
     // compare above.  For an inside u only the top clamp remains, and floor needs no XU op:
@@ -250,23 +244,6 @@ __device__ __forceinline__ float warp_point(const fv_warp& w, const float* sg, f
       const float2 q = lerp_fma2(lerp_fma2(z[0], z[1], tz), lerp_fma2(z[2], z[3], tz), ty);   // (c_{a=0}, c_{a=1})
       wi = lerp_fma(q.x, q.y, fr01.x);
     }
-#else
-    const bool inside = (u01.x >= 0.f) && (u01.x <= gp1) && (u01.y >= 0.f) && (u01.y <= gp1) && (u2 >= 0.f) &&
-                        (u2 <= gp1);
-    float wi = 0.f;
-    if (inside) {
-      const float f0 = fminf(fmaxf(floorf(u01.x), 0.f), gmax), f1 = fminf(fmaxf(floorf(u01.y), 0.f), gmax);
-      const float fl2 = fminf(fmaxf(floorf(u2), 0.f), gmax);
-      const float2 fr01 = __ffma2_rn(make_float2(f0, f1), mone2, u01);      // u - floor(u)
-      const float fr2 = __fsub_rn(u2, fl2);
-      const int i0[3] = {(int)f0, (int)f1, (int)fl2};
-      float2 z[4];
-      load_corners_x2(w.d_vol_packed, half, vol_cell_index(i, G, i0), z);
-      const float2 tz = make_float2(fr2, fr2), ty = make_float2(fr01.y, fr01.y);
-      const float2 q = lerp_fma2(lerp_fma2(z[0], z[1], tz), lerp_fma2(z[2], z[3], tz), ty);   // (c_{a=0}, c_{a=1})
-      wi = lerp_fma(q.x, q.y, fr01.x);
-    }
-#endif
     if (STORE_W) w_out[(size_t)i * w_stride] = wi;
     lik = __fadd_rn(lik, wi);
     s01 = __ffma2_rn(make_float2(wi, wi), p01, s01);
