@@ -77,3 +77,21 @@ def test_defaults_and_flags(argv, monkeypatch):
         assert a.gpus == 1 and a.impl == "ours" and a.config == "c2" and a.warmup >= 3 and 1 <= a.steps <= 50
     else:
         assert a.gpus == 8 and a.steps == 20 and a.warmup == 5
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    """The driver launches the reference arm like ours for N > 1 (torchrun, one process per
+    GPU): rank 0 alone runs the CPU timing and prints the line, the other ranks exit 0."""
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    port = bench._free_port()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1", "--cpu-tiles", "1"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
