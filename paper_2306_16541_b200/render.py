@@ -93,7 +93,6 @@ class Renderer:
         self._work = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._orders = {}
         self.occ = torch.zeros(1024, dtype=torch.int32, device=self.device)
-        self._occ_key = None
 
     def workspace(self, nbytes: int) -> torch.Tensor:
         if self._work.numel() < nbytes:
