@@ -830,6 +830,20 @@ def subject_variants(args, dev, iters=1500, reps=5):
     out = {}
     sc = psc.opaque_subject(psc.make_scene(psc.config("c2")))
     out["opaque_subject"] = _skip_variants(FreeviewModel(sc, device=str(dev)), sc, dev, reps)
+    # the headline frame with SPEC:300's initialisation of the residual net (final layer zero:
+    # x_res = 0 until trained): identical work per sample (the offset MLP still runs), but
+    # x_final keeps the march's spatial coherence instead of being scrambled by the seeded
+    # Xavier last layer's ~0.23 m offsets -- the hash gathers' locality a trained model has
+    sc = psc.make_scene(psc.config("c2"))
+    sc.off_w[-1] = np.zeros_like(sc.off_w[-1])
+    sc.off_b[-1] = np.zeros_like(sc.off_b[-1])
+    st = RenderSettings.from_config(sc.cfg, seed=sc.jitter_seed)
+    from paper_2306_16541_b200.render import Renderer
+    s = stage_times(FreeviewModel(sc, device=str(dev)), Renderer(str(dev)), sc.camera, st, dev, True, reps=reps)
+    out["spec_init_residual"] = {"render_ms": s["render_total"], "frames_per_s": 1000.0 / s["render_total"],
+                                 "stages_ms": {k: round(s[k], 4) for k in ("march_warp", "offset", "radiance",
+                                                                           "composite")},
+                                 "what": "config 2 with the residual net's final layer zero (SPEC:300 init)"}
     sc = psc.make_scene(psc.config("c3"))
     nets = FreeviewModel(sc, device=str(dev))
     target, mask = psc.target_image(sc)
