@@ -8,10 +8,29 @@
 // hash indices, foreground flags) match the oracle bit for bit.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_fp16.h>
 #include "../../include/fv_api.h"
 
 namespace fv {
+
+// Debug builds (-DFV_DEBUG=1; compute-sanitizer is not available on the GPU pool): bounds
+// checks on the gathers and staging writes that trap with the failing condition.
+#ifndef FV_DEBUG
+#define FV_DEBUG 0
+#endif
+#if FV_DEBUG
+#define FV_ASSERT(cond)                                                                     \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("FV_ASSERT %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,      \
+             (int)blockIdx.x, (int)threadIdx.x);                                            \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define FV_ASSERT(cond) do {} while (0)
+#endif
 
 constexpr uint32_t PRIME_Y = 2654435761u;
 constexpr uint32_t PRIME_Z = 805459861u;
@@ -238,6 +257,7 @@ __device__ __forceinline__ float warp_point(const fv_warp& w, const float* sg, f
       const float fr2 = __fsub_rn(u2, __fsub_rn(t2, 8388608.f));
       const uint32_t cell = ((uint32_t)i * s1 * s2c - bias) + __float_as_uint(t0) * s2c +
                             __float_as_uint(t1) * s1 + __float_as_uint(t2);
+      FV_ASSERT(cell < (uint32_t)K * s1 * s2c);
       float2 z[4];
       load_corners_x2(w.d_vol_packed, half, (size_t)cell, z);
       const float2 tz = make_float2(fr2, fr2), ty = make_float2(fr01.y, fr01.y);
@@ -343,6 +363,11 @@ __device__ __forceinline__ float2 hash_level_feat(const fv_hash& h, int l, const
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc)
         gidx[a * 4 + b * 2 + cc] = off + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + a, c.i0[1] + b, c.i0[2] + cc);
+#if FV_DEBUG
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    FV_ASSERT(gidx[q] - off < (h.dense[l] ? (uint32_t)(h.res[l] + 1) * (h.res[l] + 1) * (h.res[l] + 1) : maskT + 1u));
+#endif
   float2 v[8];
   if (h.table_half) {
     const __half2* t = reinterpret_cast<const __half2*>(h.d_table);
@@ -431,6 +456,15 @@ __device__ __forceinline__ void hash_levels_paired(const fv_hash& h, int l0, con
       iB[q * 4 + 2] = (xb ^ yB1 ^ zB0) & maskT; iB[q * 4 + 3] = (xb ^ yB1 ^ zB1) & maskT;
     }
   }
+#if FV_DEBUG
+#pragma unroll
+  for (int q = 0; q < NL; ++q) {
+    const int l = l0 + q < h.n_levels ? l0 + q : h.n_levels - 1;
+    const uint32_t lim = h.dense[l] ? (uint32_t)(h.res[l] + 1) * (h.res[l] + 1) * (h.res[l] + 1) : maskT + 1u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) FV_ASSERT(iA[q * 4 + k] < lim && iB[q * 4 + k] < lim);
+  }
+#endif
   if constexpr (IDX) {
 #pragma unroll
     for (int q = 0; q < NL; ++q)

@@ -86,9 +86,12 @@ __global__ void __launch_bounds__(128) k_hash_bwd(fv_hash h, const float* __rest
   auto corners = [&](int l, HashCell& c, uint32_t (&gi)[8], float2 (&tv)[8]) {
     hash_level_cell(xn, h.res[l], c);
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
+    for (int q = 0; q < 8; ++q) {
       gi[q] = h.offset[l] + hash_index(h.dense[l], h.res[l], maskT, c.i0[0] + (q >> 2), c.i0[1] + ((q >> 1) & 1),
                                        c.i0[2] + (q & 1));
+      FV_ASSERT(gi[q] - h.offset[l] <
+                (h.dense[l] ? (uint32_t)(h.res[l] + 1) * (h.res[l] + 1) * (h.res[l] + 1) : maskT + 1u));
+    }
     if (dx) {
       if (h.table_half) {
 #pragma unroll

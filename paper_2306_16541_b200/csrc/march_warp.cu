@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(128, FV_MARCH_MINB) k_march_warp(fv_camera cam
         base = __shfl_sync(0xffffffffu, base, 0);
         if (fg) {
           const int k = base + __popc(ballot & ((1u << lane) - 1u));
+          FV_ASSERT(k < 128 * MARCH_DPT);
           stash_x[k] = out;
           stash_i[k] = (int32_t)s;
         }
