@@ -527,6 +527,9 @@ __global__ void __launch_bounds__(NWG * 128, 1)
   }
   uint64_t* bar = &bars[wg];
   uint32_t phase = 0;
+#if FV_DEBUG
+  const int64_t n_slots = n;              // the full layout's size: every scatter slot is below it
+#endif
   if (d_count) n = min((int64_t)*d_count, n);
   const int64_t ntiles = (n + 127) / 128;
   const int64_t tstep = (int64_t)gridDim.x * NWG;
@@ -574,6 +577,7 @@ __global__ void __launch_bounds__(NWG * 128, 1)
     if (s < n) {
       float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
       if (fg) r = make_float4(sigmoid_fast(o[0]), sigmoid_fast(o[1]), sigmoid_fast(o[2]), softplus_fast(o[3] - 1.f));
+      FV_ASSERT(o_s >= 0 && o_s < n_slots);
       rgbs[o_s] = r;                         // scatter back to the full sample layout
     }
   }
