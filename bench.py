@@ -282,7 +282,7 @@ def run_ours(args, rank, world, local_rank):
     def pose_of(step):
         return sc.poses[shard.frame_of(rank, world, step, len(sc.poses))]
 
-    # march(+compaction), k_offset_tc, k_radiance_tc, composite, pose-bias fold; occupancy: points, 2 field, bits
+    # march(+compaction), k_offset_tc, k_radiance_ws, composite, pose-bias fold; occupancy: points, 2 field, bits
     launches_per_step = 5 + (4 if occ_on else 0)
 
     def step(i):
@@ -425,7 +425,7 @@ def run_ours(args, rank, world, local_rank):
 KERNEL_UNITS = {
     "march_warp": ("k_march_warp", "hbm", "24 bones x 16 B corner-packed fp16 gathers + 28 B in/out = 412 B/sample", 412.0),
     "offset": ("k_offset_tc", "tensor", "residual MLP 109,056 FLOP/sample (pose term folded into a per-frame bias)", 109056.0),
-    "radiance": ("k_radiance_tc", "hbm", "hash gathers 16 levels x 8 corners x 4 B = 512 B + 32 B in/out = 544 B/sample", 544.0),
+    "radiance": ("k_radiance_ws", "hbm", "hash gathers 16 levels x 8 corners x 4 B = 512 B + 32 B in/out = 544 B/sample", 544.0),
     "composite": ("k_composite_fwd", "hbm", "per sample 16 B [c,sigma] + 4 B delta + 4 B L (+16 B/ray out) = 24 B/sample", 24.0),
 }
 
@@ -436,7 +436,7 @@ LIMITERS = {
     "march_warp": "instruction issue (ncu: 83% issue-active, IPC ~3.3; the W^c gathers are L1/L2 hits, DRAM ~5% busy, "
                   "so the HBM fraction of the algorithmic bytes can exceed 1)",
     "offset": "tensor pipe (~94-cycle M128 N128 K16 fp16 MMA; ~80% pipe occupancy counting the padded K)",
-    "radiance": "L1 miss-request interface to L2 (l1tex__m_l1tex2xbar_req_cycles_active ~90%; table L2-resident)",
+    "radiance": "L1 miss-request interface to L2 (l1tex__m_l1tex2xbar_req_cycles_active ~90%; table L2-resident); 6 gather warpgroups + 1 MLP warpgroup, within 8% of the gather stage alone",
     "composite": "HBM streaming",
 }
 
@@ -743,7 +743,7 @@ def fused_mlp_throughput(dev, batch=65536, depth=4, reps=20):
 
 def stage_times(nets, rnd, cam, st, dev, occ_on, reps=5, occ_grid=None):
     """Device time of each stage of the actual render path (fv_render_fwd_timed: CUDA
-    events between march+warp+compaction, k_offset_tc, k_radiance_tc and the compositor),
+    events between march+warp+compaction, k_offset_tc, k_radiance_ws and the compositor),
     median over `reps` frames; plus the occupancy rebuild."""
     import ctypes as C
     import torch

@@ -586,6 +586,240 @@ __global__ void __launch_bounds__(NWG * 128, 1)
   if (warp == 0) tc::tmem_free<TCOLS>(tmem_base);
 }
 
+// ---- k_radiance_ws: warp-specialised variant (FV_RAD_WS) -------------------------------
+// NG gather warpgroups only gather: each writes its tile's 32 fp16 features into one of two
+// TMEM slots (16 columns each) and arrives on the slot's `full` barrier; ONE MLP warpgroup
+// runs the radiance MLP of every tile (layer-0 A = the slot, commit -> the slot's `empty`
+// barrier) and scatters (c, sigma).  The gathering warps never wait on an MMA.
+// TMEM: MLP D [0, 64), hidden A [64, 96), bias ones [96, 104); slots from column 128.
+#ifndef FV_RAD_WS_SLEEP
+#define FV_RAD_WS_SLEEP 0   // ns of __nanosleep between the MLP warpgroup's polls of a slot
+#endif
+// bounded mbarrier wait: traps instead of hanging if a phase never completes; SLEEP > 0
+// backs off between polls so an idle waiter does not take issue slots from the gathers
+template <int SLEEP = 0>
+__device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = tc::smem_u32(bar);
+  for (uint32_t it = 0;; ++it) {
+    if (SLEEP > 0 && it > 0) __nanosleep(SLEEP);
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, P1;\n\t}\n" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    if (ok) return;
+    if (it > (1u << 26)) {   // a phase that never completes is a bug: report and fail, do not hang
+      printf("k_radiance_ws: mbarrier wait timed out (block %d thread %d)\n", (int)blockIdx.x, (int)threadIdx.x);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(tc::smem_u32(bar)) : "memory");
+}
+
+#ifndef FV_RAD_WS_SLOTS
+#define FV_RAD_WS_SLOTS 2   // feature slots per gather warpgroup
+#endif
+#ifndef FV_RAD_WS_POLL
+#define FV_RAD_WS_POLL 0    // 1: the MLP takes whichever slot is ready (else strict round robin)
+#endif
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+               "selp.u32 %0, 1, 0, P1;\n\t}\n" : "=r"(ok) : "r"(tc::smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+
+template <int NG>
+__global__ void __launch_bounds__((NG + 1) * 128, 1)
+    k_radiance_ws(fv_field f, fv_hash h, const float4* __restrict__ xf, int64_t n, float eps_w,
+                  float4* __restrict__ rgbs, const int32_t* __restrict__ d_count, const int32_t* __restrict__ idx) {
+  constexpr int SL = FV_RAD_WS_SLOTS;
+  static_assert(128 + NG * SL * 16 <= 512, "TMEM");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[1];
+  __shared__ uint64_t full[NG][SL], empty[NG][SL];
+  __shared__ int32_t meta[NG][SL][128];     // scatter slot (>= 0 fg, <= -2 background at -(m+2), -1 none)
+  __shared__ int sel[2];
+  __shared__ uint32_t tmem_base;
+  tc_prologue<1, 512>(reinterpret_cast<const uint8_t*>(f.d_tc_pack), PK_RAD0, PK_WEND, 0, 0, smem, nullptr, bars,
+                      &tmem_base);
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < NG; ++g)
+      for (int k = 0; k < SL; ++k) { tc::mbar_init(&full[g][k], 128); tc::mbar_init(&empty[g][k], 1); }
+    tc::mbar_fence_init();
+  }
+  tc_prologue_sync();
+  const int warp = threadIdx.x >> 5, wg = threadIdx.x >> 7, t = threadIdx.x & 127;
+  const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t tb = tmem_base;
+  if (d_count) n = min((int64_t)*d_count, n);
+  const int64_t ntiles = (n + 127) / 128;
+  const int64_t tstep = (int64_t)gridDim.x * NG;
+  if (wg < NG) {
+    // ------------------------------------------------------------ gather warpgroup wg
+    const uint32_t slot0 = tb + lane + 128 + (uint32_t)(wg * SL) * 16;
+    int64_t tile = (int64_t)blockIdx.x * NG + wg;
+    float4 vnext = make_float4(0.f, 0.f, 0.f, 0.f);
+    int32_t onext = 0;
+    if (tile * 128 + t < n) {
+      vnext = xf[tile * 128 + t];
+      onext = idx ? idx[tile * 128 + t] : (int32_t)(tile * 128 + t);
+    }
+    for (int i = 0; tile < ntiles; tile += tstep, ++i) {
+      const int k = i % SL;
+      const int64_t s = tile * 128 + t;
+      const float4 v = vnext;
+      const int32_t o_s = idx ? onext : (int32_t)s;
+      if (s + tstep * 128 < n) {
+        vnext = xf[s + tstep * 128];
+        if (idx) onext = idx[s + tstep * 128];
+      }
+      const bool fg = s < n && v.w > eps_w;
+      float xn[3]; bool msk[3];
+      hash_norm(h, fg ? v.x : 0.f, fg ? v.y : 0.f, fg ? v.z : 0.f, xn, msk);
+      if (i >= SL) mbar_wait_guard(&empty[wg][k], ((i / SL) - 1) & 1);   // the MLP took this slot's last tile
+      tc::fence_after();
+      const uint32_t slot = slot0 + (uint32_t)k * 16;
+      constexpr int NL = FV_RAD_NL;
+#pragma unroll 1
+      for (int c = 0; c < 16 / NL; ++c) {
+        float2 fv[NL];
+        hash_levels_paired<NL>(h, NL * c, xn, fv);
+        uint32_t w[NL];
+#pragma unroll
+        for (int q = 0; q < NL; ++q) w[q] = tc::pack_half2(fg ? fv[q].x : 0.f, fg ? fv[q].y : 0.f);
+        if constexpr (NL == 1) tc::tmem_st1(slot + NL * c, w);
+        else if constexpr (NL == 2) tc::tmem_st2(slot + NL * c, w);
+        else if constexpr (NL == 4) tc::tmem_st4(slot + NL * c, w);
+        else tc::tmem_st8(slot + NL * c, w);
+      }
+      meta[wg][k][t] = s < n ? (fg ? o_s : -o_s - 2) : -1;
+      tc::tmem_st_wait();
+      tc::fence_before();
+      mbar_arrive_cta(&full[wg][k]);
+    }
+  } else {
+    // ------------------------------------------------------------ MLP warpgroup
+    const uint32_t trow = tb + lane, arow = tb + lane + RA_TA, bias_a = tb + 96;
+    {
+      const uint32_t ones[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      tc::tmem_st8(tb + lane + 96, ones);
+      tc::tmem_st_wait();
+    }
+    uint64_t* bar = &bars[0];
+    uint32_t phase = 0;
+    const auto mlp_layer = [&](int K_ACT16, uint32_t a_act, const uint8_t* Wt, int N) {
+      tc::fence_before();
+      named_bar(1, 128);
+      if (t == 0) {
+        tc::fence_after();
+        const uint32_t idesc = tc::idesc_f16(128, N);
+        const uint32_t b0 = tc::smem_u32(Wt);
+        for (int kk = 0; kk <= K_ACT16; ++kk) {
+          const uint32_t a = kk < K_ACT16 ? a_act + kk * 8 : bias_a;
+          tc::mma_f16_ts(tb, a, tc::make_desc(b0 + kk * 2 * N * 16, N * 16, 128), idesc, kk > 0 ? 1u : 0u);
+        }
+      }
+    };
+    const auto epi = [&] {   // D (64 columns) -> ReLU -> fp16 -> hidden A, in 16-column pieces
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        float v[16];
+        tc::tmem_ld16(trow + g * 16, v);
+        tc::tmem_ld_wait();
+        uint32_t w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = cvt_relu_h2(v[2 * j], v[2 * j + 1]);
+        tc::tmem_st8(arow + g * 8, w);
+      }
+      tc::tmem_st_wait();
+    };
+    const auto process = [&](int g, int i) {
+      const int k = i % SL;
+      mbar_wait_guard<FV_RAD_WS_SLEEP>(&full[g][k], (i / SL) & 1);
+      tc::fence_after();
+      const int32_t m = meta[g][k][t];
+      const uint32_t slot = tb + 128 + (uint32_t)(g * SL + k) * 16;
+      mlp_layer(2, slot, smem + (PK_RAD0 - PK_RAD0), 64);
+      if (t == 0) { tc::mma_commit(&empty[g][k]); tc::mma_commit(bar); }
+      __syncwarp();
+      mbar_wait_guard(bar, phase); phase ^= 1u;
+      tc::fence_after();
+      epi();
+      mlp_layer(4, tb + RA_TA, smem + (PK_RAD1 - PK_RAD0), 64);
+      if (t == 0) tc::mma_commit(bar);
+      __syncwarp();
+      mbar_wait_guard(bar, phase); phase ^= 1u;
+      tc::fence_after();
+      epi();
+      mlp_layer(4, tb + RA_TA, smem + (PK_RAD2 - PK_RAD0), 16);
+      if (t == 0) tc::mma_commit(bar);
+      __syncwarp();
+      mbar_wait_guard(bar, phase); phase ^= 1u;
+      tc::fence_after();
+      float o[16];
+      tc::tmem_ld16(trow, o);
+      tc::tmem_ld_wait();
+      if (m != -1) {
+        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m >= 0) r = make_float4(sigmoid_fast(o[0]), sigmoid_fast(o[1]), sigmoid_fast(o[2]), softplus_fast(o[3] - 1.f));
+        rgbs[m >= 0 ? m : -m - 2] = r;
+      }
+    };
+#if FV_RAD_WS_POLL
+    int cnt[NG], nxt[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const int64_t first = (int64_t)blockIdx.x * NG + g;
+      cnt[g] = first < ntiles ? (int)((ntiles - first + tstep - 1) / tstep) : 0;
+      nxt[g] = 0;
+    }
+    int start = 0;
+    for (;;) {
+      if (t == 0) {
+        int pick = -1;
+        bool left = false;
+        for (uint32_t it = 0; pick < 0; ++it) {
+          left = false;
+#pragma unroll
+          for (int gg = 0; gg < NG; ++gg) {
+            const int g = (start + gg) % NG;
+            if (nxt[g] >= cnt[g]) continue;
+            left = true;
+            if (pick < 0 && mbar_test(&full[g][nxt[g] % SL], (nxt[g] / SL) & 1)) pick = g;
+          }
+          if (!left) break;
+          if (it > (1u << 28)) __trap();
+        }
+        sel[0] = left ? pick : -1;
+      }
+      named_bar(1, 128);
+      const int g = sel[0];
+      if (g < 0) break;
+      const int i = nxt[g];
+#pragma unroll
+      for (int gg = 0; gg < NG; ++gg) if (gg == g) nxt[gg] = i + 1;
+      start = g + 1;
+      process(g, i);
+    }
+#else
+    for (int i = 0;; ++i) {
+      bool any = false;
+      for (int g = 0; g < NG; ++g) {
+        const int64_t tile = (int64_t)blockIdx.x * NG + g + (int64_t)i * tstep;
+        if (tile >= ntiles) continue;
+        any = true;
+        process(g, i);
+      }
+      if (!any) break;
+    }
+#endif
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<512>(tmem_base);
+}
+
 // Tuned configuration (round-1 sweeps on B200, SS4): residual MLP with 2
 // 8-warp teams per SM (all 512 TMEM columns; 124 KB of weights in smem), hash+radiance
 // with 4 warpgroups and 4-level batched gathers.
@@ -610,8 +844,21 @@ static void launch_offset(const fv_field* f, const float4* xs, int64_t n, float 
   k_offset_tc<OFF_TEAMS><<<grid, OFF_TEAMS * 256, smem, st>>>(*f, xs, n, eps_w, out, xfinal, d_count);
 }
 
+#ifndef FV_RAD_WS
+#define FV_RAD_WS 6   // k_radiance_ws with 6 gather warpgroups + 1 MLP warpgroup (0: k_radiance_tc)
+#endif
 static void launch_radiance(const fv_field* f, const fv_hash* h, const float4* xf, int64_t n, float eps_w,
                             float4* rgbs, const int32_t* d_count, const int32_t* idx, cudaStream_t st) {
+#if FV_RAD_WS
+  {
+    constexpr int NG = FV_RAD_WS;
+    cudaFuncSetAttribute(k_radiance_ws<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RA_SMEM);
+    const int64_t ntiles = (n + 127) / 128;
+    const int grid = (int)std::min<int64_t>((ntiles + NG - 1) / NG, sm_count());
+    k_radiance_ws<NG><<<grid, (NG + 1) * 128, RA_SMEM, st>>>(*f, *h, xf, n, eps_w, rgbs, d_count, idx);
+    return;
+  }
+#endif
   const size_t smem = RA_SMEM;
   cudaFuncSetAttribute(k_radiance_tc<RAD_NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = (n + 127) / 128;

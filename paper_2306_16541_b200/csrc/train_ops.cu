@@ -126,21 +126,23 @@ __global__ void k_softmax0_bwd(const float* __restrict__ out, const float* __res
 }
 
 // loss = mean((rgb - target[pix])^2) over R*3 values; drgb = 2 (rgb - t) / (3R)
+// One block, rays strided over its threads, a fixed reduction tree: the loss value is the
+// same bits on every run (a cross-block atomic sum would depend on the blocks' order).
 __global__ void k_mse(const float* __restrict__ rgb, const float* __restrict__ target, const int32_t* __restrict__ pix,
                       int64_t R, float* __restrict__ loss, float* __restrict__ drgb) {
-  __shared__ float red[8];
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  __shared__ float red[32];
+  const float inv = 1.f / (3.f * (float)R);
   float acc = 0.f;
-  if (r < R) {
+  for (int64_t r = threadIdx.x; r < R; r += blockDim.x) {
     const int64_t q = pix ? pix[r] : r;
-    const float inv = 1.f / (3.f * (float)R);
+    float a = 0.f;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const float d = rgb[3 * r + c] - target[3 * q + c];
-      acc += d * d;
+      a += d * d;
       drgb[3 * r + c] = 2.f * d * inv;
     }
-    acc *= inv;
+    acc += a * inv;
   }
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
@@ -148,7 +150,7 @@ __global__ void k_mse(const float* __restrict__ rgb, const float* __restrict__ t
   if (threadIdx.x == 0) {
     float s = 0.f;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-    atomicAdd(loss, s);
+    loss[0] = s;
   }
 }
 
@@ -223,19 +225,24 @@ extern "C" int32_t fv_softmax0_bwd(const float* d_out, const float* d_g, int32_t
 // SPEC compute_loss on S x S patches: lam_mse * mean((r - t)^2) + lam_perc *
 // multi-scale gradient difference (sum over scales 1, 2 of mean |d_x e| + mean |d_y e|,
 // e = r - t, scale 2 = 2x2 average pooling; oracle/loss.py restates the reference ops
-// diff_axis ad:844, avgpool2 ad:862, absval ad:243).  One CTA per patch; e and its pooled
-// copy in shared memory; loss[0..2] = (total, mse, perc) accumulated with atomics.
+// diff_axis ad:844, avgpool2 ad:862, absval ad:243).  e and its pooled
+// copy in shared memory; loss[0..2] = (total, mse, perc).  ONE block walks the patches in
+// order, so the reported loss is bitwise reproducible (no cross-block atomic sum).
 __device__ __forceinline__ float sgnf(float d) { return (float)((d > 0.f) - (d < 0.f)); }
 
 __global__ void k_patch_loss(const float* __restrict__ rgb, const float* __restrict__ target,
                              const int32_t* __restrict__ pix, int S, float lam_mse, float lam_perc, float inv_mse,
-                             float inv_d1, float inv_d2, float* __restrict__ loss, float* __restrict__ drgb) {
+                             float inv_d1, float inv_d2, float* __restrict__ loss, float* __restrict__ drgb,
+                             int n_patches) {
   extern __shared__ float sh[];
   float* e = sh;                       // [S][S][3]
   float* e2 = sh + S * S * 3;          // [S/2][S/2][3]
   __shared__ float red[3][32];
   const int S2 = S / 2;
-  const int64_t base = (int64_t)blockIdx.x * S * S;
+  float sq = 0.f, d1 = 0.f, d2 = 0.f;
+  for (int patch = 0; patch < n_patches; ++patch) {   // one block: a fixed summation order
+  const int64_t base = (int64_t)patch * S * S;
+  __syncthreads();                     // the previous patch's e / e2 are read
   for (int i = threadIdx.x; i < S * S * 3; i += blockDim.x) {
     const int64_t r = base + i / 3;
     const int64_t q = pix ? pix[r] : r;
@@ -250,7 +257,6 @@ __global__ void k_patch_loss(const float* __restrict__ rgb, const float* __restr
     }
     __syncthreads();
   }
-  float sq = 0.f, d1 = 0.f, d2 = 0.f;
   for (int i = threadIdx.x; i < S * S * 3; i += blockDim.x) {
     const int c = i % 3, x = (i / 3) % S, y = i / 3 / S;
     const float v = e[i];
@@ -277,6 +283,7 @@ __global__ void k_patch_loss(const float* __restrict__ rgb, const float* __restr
     }
     drgb[3 * (base + i / 3) + c] = g;
   }
+  }
   for (int o = 16; o; o >>= 1) {
     sq += __shfl_xor_sync(0xffffffffu, sq, o);
     d1 += __shfl_xor_sync(0xffffffffu, d1, o);
@@ -288,9 +295,9 @@ __global__ void k_patch_loss(const float* __restrict__ rgb, const float* __restr
     float a = 0.f, b = 0.f, c = 0.f;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += red[0][w]; b += red[1][w]; c += red[2][w]; }
     const float mse = a * inv_mse, perc = b * inv_d1 + c * inv_d2;
-    atomicAdd(loss + 1, mse);
-    atomicAdd(loss + 2, perc);
-    atomicAdd(loss, lam_mse * mse + lam_perc * perc);
+    loss[1] = mse;
+    loss[2] = perc;
+    loss[0] = lam_mse * mse + lam_perc * perc;
   }
 }
 
@@ -309,8 +316,9 @@ extern "C" int32_t fv_patch_loss(const float* d_rgb, const float* d_target, cons
   const int s2 = size / 2;
   const float inv_d2 = s2 > 1 ? (float)(1.0 / (3.0 * n_patches * s2 * (s2 - 1))) : 0.f;
   const size_t smem = (size_t)(size * size * 3 + s2 * s2 * 3) * sizeof(float);
-  k_patch_loss<<<n_patches, 256, smem, st>>>(d_rgb, d_target, d_pix, size, lam_mse, lam_perc, inv_mse, inv_d1,
-                                             inv_d2, d_loss, d_drgb);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_patch_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_patch_loss<<<1, 1024, smem, st>>>(d_rgb, d_target, d_pix, size, lam_mse, lam_perc, inv_mse, inv_d1, inv_d2,
+                                      d_loss, d_drgb, n_patches);
   return check_launch("fv_patch_loss");
 }
 
@@ -320,6 +328,6 @@ extern "C" int32_t fv_mse_loss(const float* d_rgb, const float* d_target, const 
   cudaStream_t st = (cudaStream_t)stream;
   cudaMemsetAsync(d_loss, 0, sizeof(float), st);
   if (n_rays == 0) return FV_OK;
-  k_mse<<<(unsigned)((n_rays + 255) / 256), 256, 0, st>>>(d_rgb, d_target, d_pix, n_rays, d_loss, d_drgb);
+  k_mse<<<1, 1024, 0, st>>>(d_rgb, d_target, d_pix, n_rays, d_loss, d_drgb);
   return check_launch("fv_mse_loss");
 }

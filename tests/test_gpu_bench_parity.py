@@ -8,7 +8,7 @@ indices bit-exact; rendered RGB/alpha and gradients within 1e-3 absolute.
   full 512x512 x 128 config-2 frame: per-ray counts, per-sample box-hit / occupancy-skip /
   foreground flags and the compacted foreground stream, under the density-built grid of
   the frame's pose and under the seeded body-ellipsoid grid;
-* the production gather arithmetic of ``k_radiance_tc`` (``fv_hash_index_paired``);
+* the production gather arithmetic of ``k_radiance_ws`` (and ``k_radiance_tc``) (``fv_hash_index_paired``);
 * the config-3 training step (T = 2^19 fp16 grid, 128 samples, 2 x 32x32 patches) against
   the oracle's float64 backward;
 * config 4 (pose sigma 0.3) renders at 64x64 and on 512x512 crops;

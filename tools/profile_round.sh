@@ -10,7 +10,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --
   python bench.py --steps 2 --warmup 3 --skip-cpu-baseline --no-occ-variants --no-trained > $o/bench_ncu_$tag.log 2>&1; echo "launch list rc=$?"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $o/train_launches_$tag.csv \
   python tools/time_train.py 2 > $o/train_ncu_$tag.log 2>&1; echo "train launch list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_march_warp|k_offset_tc|k_radiance_tc" \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_march_warp|k_offset_tc|k_radiance_tc|k_radiance_ws" \
   -s 3 -c 3 -o $o/infer_$tag -f python tools/time_stages.py --reps 2 > $o/infer_ncu_$tag.log 2>&1; echo "infer full rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_march_warp" -s 1 -c 1 \
   -o $o/march_opaque_$tag -f python tools/time_stages.py --opaque --reps 2 > $o/march_opaque_ncu_$tag.log 2>&1; echo "sparse march rc=$?"
