@@ -9,9 +9,11 @@
 //    memory as fp16 UMMA B operands (loaded once per CTA):
 //      k_offset_tc   posenc + residual MLP (112 KB of weights), pure tensor-core work,
 //                    writes x_final in place of x_skel;
-//      k_radiance_tc hash-grid gathers + radiance MLP + heads (14 KB of weights), so
-//                    ~150 KB of the SM's L1 stays free for the table gathers (profiling
+//      k_radiance_ws hash-grid gathers + radiance MLP + heads (19 KB of weights), so
+//                    ~200 KB of the SM's L1 stays free for the table gathers (profiling
 //                    the single fused kernel showed its 126-230 KB of smem starving L1);
+//                    warp-specialised: 6 gather warpgroups feed TMEM feature slots to one
+//                    MLP warpgroup (k_radiance_tc: every warpgroup gathers and runs its MLP);
 //  * NWG warpgroups per CTA each own a 128-sample tile: thread t <-> sample row t <->
 //    TMEM lane t.  Activations live in an fp16 A-operand buffer rewritten in place
 //    layer after layer; accumulators live in TMEM;
