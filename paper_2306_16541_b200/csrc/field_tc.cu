@@ -594,16 +594,10 @@ __global__ void __launch_bounds__(NWG * 128, 1)
 // runs the radiance MLP of every tile (layer-0 A = the slot, commit -> the slot's `empty`
 // barrier) and scatters (c, sigma).  The gathering warps never wait on an MMA.
 // TMEM: MLP D [0, 64), hidden A [64, 96), bias ones [96, 104); slots from column 128.
-#ifndef FV_RAD_WS_SLEEP
-#define FV_RAD_WS_SLEEP 0   // ns of __nanosleep between the MLP warpgroup's polls of a slot
-#endif
-// bounded mbarrier wait: traps instead of hanging if a phase never completes; SLEEP > 0
-// backs off between polls so an idle waiter does not take issue slots from the gathers
-template <int SLEEP = 0>
+// bounded mbarrier wait: traps (with a message) instead of hanging if a phase never completes
 __device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
   const uint32_t a = tc::smem_u32(bar);
   for (uint32_t it = 0;; ++it) {
-    if (SLEEP > 0 && it > 0) __nanosleep(SLEEP);
     uint32_t ok;
     asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
                  "selp.u32 %0, 1, 0, P1;\n\t}\n" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
@@ -621,15 +615,6 @@ __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
 #ifndef FV_RAD_WS_SLOTS
 #define FV_RAD_WS_SLOTS 2   // feature slots per gather warpgroup
 #endif
-#ifndef FV_RAD_WS_POLL
-#define FV_RAD_WS_POLL 0    // 1: the MLP takes whichever slot is ready (else strict round robin)
-#endif
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-               "selp.u32 %0, 1, 0, P1;\n\t}\n" : "=r"(ok) : "r"(tc::smem_u32(bar)), "r"(parity) : "memory");
-  return ok != 0;
-}
 
 template <int NG>
 __global__ void __launch_bounds__((NG + 1) * 128, 1)
@@ -738,7 +723,7 @@ __global__ void __launch_bounds__((NG + 1) * 128, 1)
     };
     const auto process = [&](int g, int i) {
       const int k = i % SL;
-      mbar_wait_guard<FV_RAD_WS_SLEEP>(&full[g][k], (i / SL) & 1);
+      mbar_wait_guard(&full[g][k], (i / SL) & 1);
       tc::fence_after();
       const int32_t m = meta[g][k][t];
       const uint32_t slot = tb + 128 + (uint32_t)(g * SL + k) * 16;
@@ -768,43 +753,6 @@ __global__ void __launch_bounds__((NG + 1) * 128, 1)
         rgbs[m >= 0 ? m : -m - 2] = r;
       }
     };
-#if FV_RAD_WS_POLL
-    int cnt[NG], nxt[NG];
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      const int64_t first = (int64_t)blockIdx.x * NG + g;
-      cnt[g] = first < ntiles ? (int)((ntiles - first + tstep - 1) / tstep) : 0;
-      nxt[g] = 0;
-    }
-    int start = 0;
-    for (;;) {
-      if (t == 0) {
-        int pick = -1;
-        bool left = false;
-        for (uint32_t it = 0; pick < 0; ++it) {
-          left = false;
-#pragma unroll
-          for (int gg = 0; gg < NG; ++gg) {
-            const int g = (start + gg) % NG;
-            if (nxt[g] >= cnt[g]) continue;
-            left = true;
-            if (pick < 0 && mbar_test(&full[g][nxt[g] % SL], (nxt[g] / SL) & 1)) pick = g;
-          }
-          if (!left) break;
-          if (it > (1u << 28)) __trap();
-        }
-        sel[0] = left ? pick : -1;
-      }
-      named_bar(1, 128);
-      const int g = sel[0];
-      if (g < 0) break;
-      const int i = nxt[g];
-#pragma unroll
-      for (int gg = 0; gg < NG; ++gg) if (gg == g) nxt[gg] = i + 1;
-      start = g + 1;
-      process(g, i);
-    }
-#else
     for (int i = 0;; ++i) {
       bool any = false;
       for (int g = 0; g < NG; ++g) {
@@ -815,7 +763,6 @@ __global__ void __launch_bounds__((NG + 1) * 128, 1)
       }
       if (!any) break;
     }
-#endif
   }
   tc::fence_before();
   __syncthreads();
